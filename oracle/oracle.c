@@ -1,0 +1,500 @@
+/*
+ * oracle.c — plain, slow, fp64 CPU ORACLE for the OS-LALM CT hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_1402_4381_b200/) never links, imports or calls it,
+ * and it shares no code, headers or tables with the CUDA path.
+ *
+ * What it computes (citations: P:n = /root/reference/PAPER.md line n;
+ * O1..O7 / G1..G21 = the readings in SURVEY.md §8(c), restated in DESIGN.md):
+ *   O1  scan geometry (fan / cone axial / cone helical, arc detector)
+ *   O2  separable-footprint SF-TR system matrix with A1 amplitude
+ *       ("A is the system matrix of a CT scan"; reading G1)
+ *   O4  SQS denominator D_L = A'(W (A 1_S))        (L_diag = diag{A'WA1})
+ *   O5  Fair-potential regulariser R, grad R, Huber curvature D_R  (G3, G14)
+ *   O6  cost Psi(x) = 1/2 ||y - Ax||_W^2 + R(x)      (eq. ct_recon)
+ *   O7  OS-LALM with deterministic downward continuation and restart
+ *       (P:380-397 eq. os_lalm_iterates; P:495-516 eqs. period_indicator_qp,
+ *        rho_l_formula_qp; P:529-537 substitution + SQS; n = 1 FISTA step)
+ *
+ * Layouts (the oracle's own textbook layout; tests permute to/from the ABI):
+ *   image     x[iz][iy][ix]          (nz = 1 for 2D fan)
+ *   sinogram  p[v][r][c]             (view, detector row, channel; nt = 1 in 2D)
+ *
+ * Arithmetic: fp64 throughout.  Parallelism: OpenMP over independent outputs
+ * only (views for forward, image rows for back), so results are deterministic.
+ * No blocking, fusion or reordering beyond the definitions.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_FAN2D 0
+#define OR_CONE_AXIAL 1
+#define OR_CONE_HELICAL 2
+
+typedef struct {
+    int kind;
+    int nx, ny, nz;
+    double dx, dy, dz, offx, offy, offz;
+    int ns, nt;
+    double ds, dt, offs, offt;
+    double dso, dsd;
+    int na;
+    double orbit_deg, orbit_start_deg, pitch;
+} or_geom;
+
+/* ---------------- O1: geometry ---------------- */
+
+static double vox_x(const or_geom* g, int ix) { return (ix - (g->nx - 1) / 2.0) * g->dx + g->offx; }
+static double vox_y(const or_geom* g, int iy) { return (iy - (g->ny - 1) / 2.0) * g->dy + g->offy; }
+static double vox_z(const or_geom* g, int iz) {
+    if (g->kind == OR_FAN2D) return 0.0;
+    return (iz - (g->nz - 1) / 2.0) * g->dz + g->offz;
+}
+
+/* beta_v = beta_0 + 2 pi turns v / na  (O1) */
+double or_view_angle(const or_geom* g, int v) {
+    double turns = g->orbit_deg / 360.0;
+    return g->orbit_start_deg * M_PI / 180.0 + 2.0 * M_PI * turns * v / g->na;
+}
+
+/* z_s(v) = (v - (na-1)/2) * h / (na/turns), h = pitch nt dt dso/dsd  (O1, G17) */
+double or_source_z(const or_geom* g, int v) {
+    if (g->kind != OR_CONE_HELICAL) return 0.0;
+    double turns = g->orbit_deg / 360.0;
+    double h = g->pitch * g->nt * g->dt * g->dso / g->dsd;
+    return (v - (g->na - 1) / 2.0) * h / (g->na / turns);
+}
+
+/* channel centre arc position s_c = dsd * gamma_c */
+static double chan_s(const or_geom* g, int c) { return (c - (g->ns - 1) / 2.0 - g->offs) * g->ds; }
+static double row_t(const or_geom* g, int r) { return (r - (g->nt - 1) / 2.0 - g->offt) * g->dt; }
+
+/* ---------------- O2: SF-TR footprint ---------------- */
+
+/* Antiderivative of the unit-height trapezoid rising on [t0,t1], flat on
+ * [t1,t2], falling on [t2,t3], evaluated at s. */
+static double trap_cdf(const double t[4], double s) {
+    double total = 0.5 * (t[3] + t[2] - t[1] - t[0]);
+    if (s <= t[0]) return 0.0;
+    if (s >= t[3]) return total;
+    if (s <= t[1]) return (s - t[0]) * (s - t[0]) / (2.0 * (t[1] - t[0]));
+    if (s <= t[2]) return 0.5 * (t[1] - t[0]) + (s - t[1]);
+    return total - (t[3] - s) * (t[3] - s) / (2.0 * (t[3] - t[2]));
+}
+
+typedef struct {
+    double tau[4];     /* sorted transaxial breakpoints (arc length on detector) */
+    double lphi;       /* dx / max(|cos phi0|, |sin phi0|) */
+    double rho_h;      /* in-plane source-to-voxel-centre distance */
+} or_trans;
+
+static void sort4(double a[4]) {
+    for (int i = 1; i < 4; i++) {
+        double k = a[i];
+        int j = i - 1;
+        while (j >= 0 && a[j] > k) { a[j + 1] = a[j]; j--; }
+        a[j + 1] = k;
+    }
+}
+
+static void transaxial(const or_geom* g, double beta, double xc, double yc, or_trans* out) {
+    double sb = sin(beta), cb = cos(beta);
+    /* e_c = (sin b, -cos b) points from the source through the isocentre;
+     * e_perp = (cos b, sin b); source at -dso e_c. */
+    double cx[4] = {xc - g->dx / 2, xc + g->dx / 2, xc - g->dx / 2, xc + g->dx / 2};
+    double cy[4] = {yc - g->dy / 2, yc - g->dy / 2, yc + g->dy / 2, yc + g->dy / 2};
+    for (int k = 0; k < 4; k++) {
+        double along = g->dso + cx[k] * sb - cy[k] * cb;
+        double perp = cx[k] * cb + cy[k] * sb;
+        out->tau[k] = g->dsd * atan2(perp, along);
+    }
+    sort4(out->tau);
+    double along = g->dso + xc * sb - yc * cb;
+    double perp = xc * cb + yc * sb;
+    out->rho_h = sqrt(along * along + perp * perp);
+    double sx = -g->dso * sb, sy = g->dso * cb;
+    double rx = xc - sx, ry = yc - sy, rn = sqrt(rx * rx + ry * ry);
+    double cphi = fabs(rx / rn), sphi = fabs(ry / rn);
+    out->lphi = g->dx / (cphi > sphi ? cphi : sphi);
+}
+
+/* F_s(c) = (1/ds) * integral over channel c of the trapezoid */
+static double Fs(const or_geom* g, const or_trans* tr, int c) {
+    double s = chan_s(g, c);
+    return (trap_cdf(tr->tau, s + g->ds / 2) - trap_cdf(tr->tau, s - g->ds / 2)) / g->ds;
+}
+
+/* Axial rect footprint [t-, t+] of voxel iz for source height zs */
+static void axial_rect(const or_geom* g, const or_trans* tr, double zj, double zs,
+                       double* tm, double* tp, double* lth) {
+    double mag = g->dsd / tr->rho_h;
+    *tm = (zj - g->dz / 2 - zs) * mag;
+    *tp = (zj + g->dz / 2 - zs) * mag;
+    double tz = (zj - zs) / tr->rho_h;
+    *lth = sqrt(1.0 + tz * tz);
+}
+
+static double Ft(const or_geom* g, double tm, double tp, int r) {
+    double lo = row_t(g, r) - g->dt / 2, hi = lo + g->dt;
+    double a = tm > lo ? tm : lo, b = tp < hi ? tp : hi;
+    return b > a ? (b - a) / g->dt : 0.0;
+}
+
+/* a_ij for one (voxel, cell); exported for brute-force tests */
+double or_weight(const or_geom* g, int v, int ix, int iy, int iz, int r, int c) {
+    or_trans tr;
+    double beta = or_view_angle(g, v);
+    transaxial(g, beta, vox_x(g, ix), vox_y(g, iy), &tr);
+    double fs = Fs(g, &tr, c);
+    if (g->kind == OR_FAN2D) return tr.lphi * fs;
+    double tm, tp, lth;
+    axial_rect(g, &tr, vox_z(g, iz), or_source_z(g, v), &tm, &tp, &lth);
+    return tr.lphi * lth * fs * Ft(g, tm, tp, r);
+}
+
+/* transaxial footprint data for tests: tau[4], lphi, rho_h */
+void or_transaxial(const or_geom* g, int v, int ix, int iy, double* out6) {
+    or_trans tr;
+    transaxial(g, or_view_angle(g, v), vox_x(g, ix), vox_y(g, iy), &tr);
+    for (int k = 0; k < 4; k++) out6[k] = tr.tau[k];
+    out6[4] = tr.lphi;
+    out6[5] = tr.rho_h;
+}
+
+/* Channel range [c0,c1] whose bins intersect [t0,t3] (possibly empty). */
+static void chan_range(const or_geom* g, const or_trans* tr, int* c0, int* c1) {
+    double base = -(g->ns - 1) / 2.0 - g->offs;
+    int a = (int)floor(tr->tau[0] / g->ds - base - 0.5) - 1;
+    int b = (int)floor(tr->tau[3] / g->ds - base + 0.5) + 1;
+    if (a < 0) a = 0;
+    if (b > g->ns - 1) b = g->ns - 1;
+    *c0 = a;
+    *c1 = b;
+}
+
+static int nzv(const or_geom* g) { return g->kind == OR_FAN2D ? 1 : g->nz; }
+static int ntv(const or_geom* g) { return g->kind == OR_FAN2D ? 1 : g->nt; }
+
+/* Forward projection  p[k][r][c] = sum_j a_{(v_k,r,c), j} x_j  over views
+ * v_k = first + k*stride, k < count.  x may be masked by mask (NULL = all). */
+void or_fwd(const or_geom* g, int first, int stride, int count, const double* x, double* p) {
+    int NZ = nzv(g), NT = ntv(g);
+    size_t cells = (size_t)NT * g->ns;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int k = 0; k < count; k++) {
+        int v = first + k * stride;
+        double* pv = p + (size_t)k * cells;
+        memset(pv, 0, cells * sizeof(double));
+        double beta = or_view_angle(g, v), zs = or_source_z(g, v);
+        for (int iy = 0; iy < g->ny; iy++)
+            for (int ix = 0; ix < g->nx; ix++) {
+                or_trans tr;
+                transaxial(g, beta, vox_x(g, ix), vox_y(g, iy), &tr);
+                int c0, c1;
+                chan_range(g, &tr, &c0, &c1);
+                for (int c = c0; c <= c1; c++) {
+                    double fs = Fs(g, &tr, c);
+                    if (fs == 0.0) continue;
+                    for (int iz = 0; iz < NZ; iz++) {
+                        double xv = x[((size_t)iz * g->ny + iy) * g->nx + ix];
+                        if (xv == 0.0) continue;
+                        if (g->kind == OR_FAN2D) {
+                            pv[c] += tr.lphi * fs * xv;
+                            continue;
+                        }
+                        double tm, tp, lth;
+                        axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
+                        for (int r = 0; r < NT; r++) {
+                            double ft = Ft(g, tm, tp, r);
+                            if (ft != 0.0) pv[(size_t)r * g->ns + c] += tr.lphi * lth * fs * ft * xv;
+                        }
+                    }
+                }
+            }
+    }
+}
+
+/* Back projection  x_j = sum_i a_ij p_i  (exact adjoint of or_fwd). */
+void or_back(const or_geom* g, int first, int stride, int count, const double* p, double* x) {
+    int NZ = nzv(g), NT = ntv(g);
+    size_t cells = (size_t)NT * g->ns;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int iy = 0; iy < g->ny; iy++)
+        for (int ix = 0; ix < g->nx; ix++) {
+            for (int iz = 0; iz < NZ; iz++) x[((size_t)iz * g->ny + iy) * g->nx + ix] = 0.0;
+            for (int k = 0; k < count; k++) {
+                int v = first + k * stride;
+                const double* pv = p + (size_t)k * cells;
+                double beta = or_view_angle(g, v), zs = or_source_z(g, v);
+                or_trans tr;
+                transaxial(g, beta, vox_x(g, ix), vox_y(g, iy), &tr);
+                int c0, c1;
+                chan_range(g, &tr, &c0, &c1);
+                for (int c = c0; c <= c1; c++) {
+                    double fs = Fs(g, &tr, c);
+                    if (fs == 0.0) continue;
+                    for (int iz = 0; iz < NZ; iz++) {
+                        double acc = 0.0;
+                        if (g->kind == OR_FAN2D) {
+                            acc = tr.lphi * fs * pv[c];
+                        } else {
+                            double tm, tp, lth;
+                            axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
+                            for (int r = 0; r < NT; r++) {
+                                double ft = Ft(g, tm, tp, r);
+                                if (ft != 0.0) acc += tr.lphi * lth * fs * ft * pv[(size_t)r * g->ns + c];
+                            }
+                        }
+                        x[((size_t)iz * g->ny + iy) * g->nx + ix] += acc;
+                    }
+                }
+            }
+        }
+}
+
+/* U = number of (view, voxel in mask) pairs with a non-empty footprint
+ * (SURVEY §8d metric definition), over views first + k*stride. */
+long long or_count_vv(const or_geom* g, int first, int stride, int count, const uint8_t* mask) {
+    int NZ = nzv(g);
+    double s_lo = chan_s(g, 0) - g->ds / 2, s_hi = chan_s(g, g->ns - 1) + g->ds / 2;
+    double t_lo = row_t(g, 0) - g->dt / 2, t_hi = row_t(g, ntv(g) - 1) + g->dt / 2;
+    long long total = 0;
+#pragma omp parallel for reduction(+ : total) schedule(dynamic, 1)
+    for (int k = 0; k < count; k++) {
+        int v = first + k * stride;
+        double beta = or_view_angle(g, v), zs = or_source_z(g, v);
+        for (int iy = 0; iy < g->ny; iy++)
+            for (int ix = 0; ix < g->nx; ix++) {
+                or_trans tr;
+                transaxial(g, beta, vox_x(g, ix), vox_y(g, iy), &tr);
+                double a = tr.tau[0] > s_lo ? tr.tau[0] : s_lo, b = tr.tau[3] < s_hi ? tr.tau[3] : s_hi;
+                if (!(b > a)) continue;
+                for (int iz = 0; iz < NZ; iz++) {
+                    if (mask && !mask[((size_t)iz * g->ny + iy) * g->nx + ix]) continue;
+                    if (g->kind != OR_FAN2D) {
+                        double tm, tp, lth;
+                        axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
+                        double ta = tm > t_lo ? tm : t_lo, tb = tp < t_hi ? tp : t_hi;
+                        if (!(tb > ta)) continue;
+                    }
+                    total++;
+                }
+            }
+    }
+    return total;
+}
+
+/* ---------------- O4: SQS denominator ---------------- */
+
+/* D_L = A'(W (A 1_S)) over all views; S <- S and {D_L > 0}; D_L := 0 off S. */
+void or_sqs_denom(const or_geom* g, const double* w, uint8_t* mask, double* dl) {
+    size_t N = (size_t)nzv(g) * g->ny * g->nx;
+    size_t cells = (size_t)g->na * ntv(g) * g->ns;
+    double* one = (double*)malloc(N * sizeof(double));
+    double* p = (double*)malloc(cells * sizeof(double));
+    for (size_t j = 0; j < N; j++) one[j] = mask[j] ? 1.0 : 0.0;
+    or_fwd(g, 0, 1, g->na, one, p);
+    for (size_t i = 0; i < cells; i++) p[i] *= w[i];
+    or_back(g, 0, 1, g->na, p, dl);
+    for (size_t j = 0; j < N; j++) {
+        if (!(mask[j] && dl[j] > 0.0)) {
+            mask[j] = 0;
+            dl[j] = 0.0;
+        }
+    }
+    free(one);
+    free(p);
+}
+
+/* ---------------- O5: Fair regulariser ---------------- */
+/* psi(t) = delta^2 (|t|/delta - ln(1 + |t|/delta));  psi'(t) = t / (1 + |t|/delta);
+ * omega(t) = 1 / (1 + |t|/delta)  (Huber curvature, G14).
+ * R(x) = beta sum_{unordered pairs {j,k} in S, k in N(j)} w_jk psi(x_j - x_k),
+ * w_jk = 1 / ||offset||; N = 8-neighbourhood in-plane (nbr = 8) or 26 in 3D. */
+
+static double fair_psi(double t, double d) { double a = fabs(t) / d; return d * d * (a - log1p(a)); }
+
+static int nbr_ok(const or_geom* g, int nbr, int oz) { return !(nbr == 8 && oz != 0) && !(nzv(g) == 1 && oz != 0); }
+
+double or_reg_value(const or_geom* g, double beta, double delta, int nbr, const uint8_t* mask, const double* x) {
+    int NZ = nzv(g);
+    double total = 0.0;
+    for (int iz = 0; iz < NZ; iz++)
+        for (int iy = 0; iy < g->ny; iy++)
+            for (int ix = 0; ix < g->nx; ix++) {
+                size_t j = ((size_t)iz * g->ny + iy) * g->nx + ix;
+                if (!mask[j]) continue;
+                for (int oz = -1; oz <= 1; oz++)
+                    for (int oy = -1; oy <= 1; oy++)
+                        for (int ox = -1; ox <= 1; ox++) {
+                            if (!nbr_ok(g, nbr, oz) || (ox == 0 && oy == 0 && oz == 0)) continue;
+                            int kx = ix + ox, ky = iy + oy, kz = iz + oz;
+                            if (kx < 0 || ky < 0 || kz < 0 || kx >= g->nx || ky >= g->ny || kz >= NZ) continue;
+                            size_t k = ((size_t)kz * g->ny + ky) * g->nx + kx;
+                            if (k <= j || !mask[k]) continue; /* each unordered pair once */
+                            double w = 1.0 / sqrt((double)(ox * ox + oy * oy + oz * oz));
+                            total += w * fair_psi(x[j] - x[k], delta);
+                        }
+            }
+    return beta * total;
+}
+
+void or_reg_grad(const or_geom* g, double beta, double delta, int nbr, const uint8_t* mask, const double* x,
+                 double* grad, double* curv) {
+    int NZ = nzv(g);
+#pragma omp parallel for
+    for (int iz = 0; iz < NZ; iz++)
+        for (int iy = 0; iy < g->ny; iy++)
+            for (int ix = 0; ix < g->nx; ix++) {
+                size_t j = ((size_t)iz * g->ny + iy) * g->nx + ix;
+                double gr = 0.0, cu = 0.0;
+                if (mask[j]) {
+                    for (int oz = -1; oz <= 1; oz++)
+                        for (int oy = -1; oy <= 1; oy++)
+                            for (int ox = -1; ox <= 1; ox++) {
+                                if (!nbr_ok(g, nbr, oz) || (ox == 0 && oy == 0 && oz == 0)) continue;
+                                int kx = ix + ox, ky = iy + oy, kz = iz + oz;
+                                if (kx < 0 || ky < 0 || kz < 0 || kx >= g->nx || ky >= g->ny || kz >= NZ) continue;
+                                size_t k = ((size_t)kz * g->ny + ky) * g->nx + kx;
+                                if (!mask[k]) continue;
+                                double w = 1.0 / sqrt((double)(ox * ox + oy * oy + oz * oz));
+                                double t = x[j] - x[k];
+                                double om = 1.0 / (1.0 + fabs(t) / delta);
+                                gr += w * t * om;
+                                cu += w * om;
+                            }
+                }
+                grad[j] = beta * gr;
+                if (curv) curv[j] = 2.0 * beta * cu;
+            }
+}
+
+/* ---------------- O6: cost ---------------- */
+double or_cost(const or_geom* g, const double* y, const double* w, double beta, double delta, int nbr,
+               const uint8_t* mask, const double* x) {
+    size_t cells = (size_t)g->na * ntv(g) * g->ns;
+    double* p = (double*)malloc(cells * sizeof(double));
+    or_fwd(g, 0, 1, g->na, x, p);
+    double d = 0.0;
+    for (size_t i = 0; i < cells; i++) d += 0.5 * w[i] * (p[i] - y[i]) * (p[i] - y[i]);
+    free(p);
+    return d + or_reg_value(g, beta, delta, nbr, mask, x);
+}
+
+/* ---------------- O7: OS-LALM ---------------- */
+
+/* Bit-reversal visiting order (pad to 2^ceil(log2 M), drop >= M, G11). */
+void or_bit_reversal(int M, int* order) {
+    int bits = 0;
+    while ((1 << bits) < M) bits++;
+    int n = 0;
+    for (int i = 0; i < (1 << bits); i++) {
+        int r = 0;
+        for (int b = 0; b < bits; b++)
+            if (i & (1 << b)) r |= 1 << (bits - 1 - b);
+        if (r < M) order[n++] = r;
+    }
+}
+
+/* rho_l (eq. rho_l_formula_qp): 1 if l = 0, else
+ * max{ pi/(l+1) sqrt(1 - (pi/(2l+2))^2), rho_min }. */
+double or_rho_l(long l, double rho_min) {
+    if (l == 0) return 1.0;
+    double a = M_PI / (l + 1.0), b = M_PI / (2.0 * l + 2.0);
+    double r = a * sqrt(1.0 - b * b);
+    return r > rho_min ? r : rho_min;
+}
+
+/* G = M * A_m'(W (A_m x - y)) for subset m (views v = m mod M). */
+static void subset_grad(const or_geom* g, int M, int m, const double* y, const double* w, const double* x,
+                        double* G, double* pbuf) {
+    int count = (g->na - m + M - 1) / M;
+    size_t cells = (size_t)ntv(g) * g->ns;
+    or_fwd(g, m, M, count, x, pbuf);
+    for (int k = 0; k < count; k++) {
+        size_t off = (size_t)(m + k * M) * cells;
+        for (size_t i = 0; i < cells; i++) {
+            size_t q = (size_t)k * cells + i;
+            pbuf[q] = M * w[off + i] * (pbuf[q] - y[off + i]);
+        }
+    }
+    or_back(g, m, M, count, pbuf, G);
+}
+
+/* Exported for tests: M * A_m'(W (A_m x - y)). */
+void or_subset_grad(const or_geom* g, int M, int m, const double* y, const double* w, const double* x,
+                    double* G) {
+    size_t cells = (size_t)ntv(g) * g->ns;
+    int count = (g->na - m + M - 1) / M;
+    double* pbuf = (double*)malloc((size_t)count * cells * sizeof(double));
+    subset_grad(g, M, m, y, w, x, G, pbuf);
+    free(pbuf);
+}
+
+/*
+ * OS-LALM run:
+ *   x <- x0 (caller, 0 on S); G <- M A_{pi0}'(W(A x - y)); g <- G; l <- 0
+ *   for k = 1..K, j = 0..M-1:
+ *     rho <- FIXED ? rho_fixed : rho_l(l)
+ *     x <- max(0, x - (rho G + (1-rho) g + gradR(x)) / (rho D_L + D_R(x)))   on S, 0 off S
+ *     [if trailing == 0 and last step: stop]
+ *     G+ <- M A_{pi[(j+1)%M]}'(W(A x - y))
+ *     xi <- sum_S (g - G+)(G+ - G);  g <- (rho G+ + g)/(1 + rho);  G <- G+
+ *     CONTINUATION: l <- (xi > 0) ? 0 : l + 1
+ * mode 0 = FIXED, 1 = CONTINUATION.  trailing = 1 also computes the final
+ * projection pair (so the state is ready for another iteration; x unchanged).
+ * log (nullable) receives per inner step: rho, xi, restart flag (3 doubles).
+ * g_out, G_out (nullable) receive the final split gradient and subset gradient.
+ */
+void or_oslalm_run(const or_geom* g, const double* y, const double* w, const double* dl, const uint8_t* mask,
+                   int M, int mode, double rho_fixed, double rho_min, double beta, double delta, int nbr,
+                   int n_iter, int trailing, double* x, double* log, double* g_out, double* G_out) {
+    size_t N = (size_t)nzv(g) * g->ny * g->nx;
+    size_t cells = (size_t)ntv(g) * g->ns;
+    int maxcount = (g->na + M - 1) / M;
+    int* order = (int*)malloc(M * sizeof(int));
+    or_bit_reversal(M, order);
+    double* G = (double*)malloc(N * sizeof(double));
+    double* Gp = (double*)malloc(N * sizeof(double));
+    double* sg = (double*)malloc(N * sizeof(double));
+    double* gr = (double*)malloc(N * sizeof(double));
+    double* cu = (double*)malloc(N * sizeof(double));
+    double* pbuf = (double*)malloc((size_t)maxcount * cells * sizeof(double));
+    for (size_t j = 0; j < N; j++)
+        if (!mask[j]) x[j] = 0.0;
+    subset_grad(g, M, order[0], y, w, x, G, pbuf);
+    memcpy(sg, G, N * sizeof(double));
+    long l = 0;
+    int step = 0;
+    for (int k = 1; k <= n_iter; k++)
+        for (int j = 0; j < M; j++, step++) {
+            double rho = mode == 0 ? rho_fixed : or_rho_l(l, rho_min);
+            or_reg_grad(g, beta, delta, nbr, mask, x, gr, cu);
+            for (size_t q = 0; q < N; q++) {
+                if (!mask[q]) { x[q] = 0.0; continue; }
+                double s = rho * G[q] + (1.0 - rho) * sg[q];
+                double xn = x[q] - (s + gr[q]) / (rho * dl[q] + cu[q]);
+                x[q] = xn > 0.0 ? xn : 0.0;
+            }
+            if (log) { log[3 * step] = rho; log[3 * step + 1] = 0.0; log[3 * step + 2] = 0.0; }
+            if (!trailing && k == n_iter && j == M - 1) break;
+            subset_grad(g, M, order[(j + 1) % M], y, w, x, Gp, pbuf);
+            double xi = 0.0;
+            for (size_t q = 0; q < N; q++)
+                if (mask[q]) xi += (sg[q] - Gp[q]) * (Gp[q] - G[q]);
+            for (size_t q = 0; q < N; q++) {
+                sg[q] = (rho * Gp[q] + sg[q]) / (1.0 + rho);
+                G[q] = Gp[q];
+            }
+            int restart = xi > 0.0;
+            if (mode == 1) l = restart ? 0 : l + 1;
+            if (log) { log[3 * step + 1] = xi; log[3 * step + 2] = restart; }
+        }
+    if (g_out) memcpy(g_out, sg, N * sizeof(double));
+    if (G_out) memcpy(G_out, G, N * sizeof(double));
+    free(order); free(G); free(Gp); free(sg); free(gr); free(cu); free(pbuf);
+}
