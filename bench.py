@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""bench.py — OS-LALM CT hot path on B200 (BASELINE.json metric).
+
+A step = one complete reconstruction job of the chosen config (default c2 = BASELINE
+configs[1]): the SQS denominator D_L = A'WA1 (one full forward/back pair, S8), then
+n_iter OS-LALM iterations (M inner steps each: K3 update, K1 forward + fused residual,
+K2 back-projection + fused g-update/xi, K4 rho continuation).  Inputs are synthetic
+(seeded phantom, Poisson noise) and resident in HBM when the timed region starts.
+
+value  = voxel-ray updates/s = (work of every projection in the step, counted as U per
+         projection, U = #(view, voxel in S) pairs with a non-empty footprint) / time.
+iters_per_s = n_iter / (time of the n_iter iterations, D_L excluded).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+For N > 1 launch with torch.distributed.run (one rank per GPU); views of every subset
+are split into contiguous blocks per rank and the partial back-projections are summed
+with NCCL (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "voxel-ray updates/s (fwd+back proj)"
+UNIT = "voxel-ray updates/s"
+FP32_LANES_PER_SM = 128
+N_SM = 148
+
+
+def peaks():
+    p = {"hbm_gbs": 6553.0, "sm_max_mhz": 1965.0, "src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        p.update(hbm_gbs=float(mp["hbm_gbs"]), sm_max_mhz=float(mp.get("sm_max_mhz", 1965.0)), src="measured")
+    except Exception:
+        pass
+    # FP32 ALU peak derived from unit counts and the max SM clock
+    p["fp32_tflops"] = N_SM * FP32_LANES_PER_SM * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def allreduce_max(v, ws):
+    if ws == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def workload_name(cfg):
+    g = cfg.geom
+    shape = f"{g['nx']}x{g['ny']}" + ("" if cfg.is2d else f"x{g['nz']}")
+    det = f"{g['ns']}ch" + ("" if cfg.is2d else f"x{g['nt']}rows")
+    return (f"{cfg.name}: {g['kind']} {shape} image, {det}, {g['na']} views, M={cfg.M}, "
+            f"{cfg.n_iter} OS-LALM iterations + D_L setup")
+
+
+def cpu_oracle_sample(cfg, budget_s=10.0):
+    """The fp64 oracle as it stands, on whole subsets of the workload (fwd + back)."""
+    import oracle as O
+    from paper_1402_4381_b200 import inputs as I
+    g = cfg.geom
+    m = I.support_mask(cfg)
+    mo = I.to_oracle_image(m).astype(np.uint8)
+    rng = np.random.default_rng(0)
+    x = rng.random(O.img_shape(g)) * 0.02 * mo
+    order = O.bit_reversal(cfg.M)
+    done, work, t0 = 0, 0, time.perf_counter()
+    while True:
+        sub = order[done % cfg.M]
+        cnt = O.nviews(g, sub, cfg.M)
+        p = O.fwd(g, x, sub, cfg.M, cnt)
+        O.back(g, p, sub, cfg.M, cnt)
+        work += 2 * O.count_vv(g, mo, sub, cfg.M, cnt)
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    el = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": work / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done} whole subset(s) of {cfg.name} (forward + back projection, fp64, OpenMP), {el:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle is this tier's reference arm (CPU, rank 0 only)."""
+    ws, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return 0
+    from paper_1402_4381_b200 import inputs as I
+    import oracle as O
+    O.build()
+    cfg = I.config(args.config)
+    g = cfg.geom
+    m = I.support_mask(cfg)
+    mo = I.to_oracle_image(m).astype(np.uint8)
+    x = np.random.default_rng(0).random(O.img_shape(g)) * 0.02 * mo
+    order = O.bit_reversal(cfg.M)
+
+    def step(i):
+        sub = order[i % cfg.M]
+        cnt = O.nviews(g, sub, cfg.M)
+        p = O.fwd(g, x, sub, cfg.M, cnt)
+        O.back(g, p, sub, cfg.M, cnt)
+        return 2 * O.count_vv(g, mo, sub, cfg.M, cnt)
+
+    for i in range(args.warmup):
+        step(i)
+    times, work = [], 0
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        w = step(args.warmup + i)
+        times.append(time.perf_counter() - t0)
+        work += w
+    T = sum(times)
+    value = work / T
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": workload_name(cfg) + " [reference step: one subset fwd+back]"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"one whole subset of {cfg.name} per step (forward + back projection, fp64)"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--iters", type=int, default=None, help="override n_iter (default: the config's)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    from paper_1402_4381_b200 import build, ctlib
+    from paper_1402_4381_b200 import inputs as I
+    if rank == 0:
+        build.build()
+    if ws > 1:
+        barrier(ws)
+    ctlib.load()
+    cfg = I.config(args.config)
+    n_iter = args.iters or cfg.n_iter
+    g = cfg.geom
+    dev = torch.device("cuda", local)
+
+    # ---- inputs (synthetic, seeded), resident in HBM
+    data = I.synthesize(cfg, device=dev, views_per_chunk=8 if not cfg.is2d else 128)
+    y, w = data["y"].contiguous(), data["w"].contiguous()
+    del data
+    m0 = I.support_mask(cfg, device=dev)
+    geo = ctlib.Geometry(g, local)
+    if ws > 1:
+        import torch.distributed as dist
+        uid = [ctlib.ct_comm_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        geo.comm_init(rank, ws, uid[0])
+    mask = m0.clone()
+    dl = torch.empty(geo.img_shape, dtype=torch.float32, device=dev)
+    scratch = torch.empty(ctlib.ct_sqs_denom_scratch_bytes(geo.h), dtype=torch.uint8, device=dev)
+    x = torch.zeros(geo.img_shape, dtype=torch.float32, device=dev)
+    sol = ctlib.OSLALM(geo, cfg.M, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr)
+    sol.set_data(y, w, dl, mask)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(ev=None):
+        mask.copy_(m0)
+        ctlib.ct_sqs_denom(geo.h, w, mask, dl, scratch)
+        if ev is not None:
+            ev.record()
+        sol.reset()
+        x.zero_()
+        for _ in range(n_iter):
+            sol.iterate(x)
+
+    # ---- work counts (fp64 geometry on the device; once, outside any timed region)
+    step()
+    torch.cuda.synchronize()
+    U0, nnz0, C0 = geo.counts(m0)
+    U, nnz, C = geo.counts(mask)
+    from paper_1402_4381_b200.host import subset_views
+    # the first subset of the bit-reversal order is subset 0 (initial G, reading G10)
+    Ui = geo.counts(mask, subset_views(g["na"], cfg.M, 0))[0]
+    work = 2 * U0 + 2 * Ui + n_iter * 2 * U
+
+    # ---- warm-up (also captures the CUDA graph)
+    for _ in range(args.warmup):
+        step()
+    barrier(ws)
+
+    # ---- timed region: K steps, L2 flushed between steps (not timed)
+    st = torch.cuda.current_stream()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = ctlib.ct_kernel_launches()
+    with ClockSampler(local) as clk:
+        barrier(ws)
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(st)
+            step(mids[i])
+            ends[i].record(st)
+        barrier(ws)
+    launches = ctlib.ct_kernel_launches() - l0
+    T = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / 1e3
+    Ti = sum(m.elapsed_time(e) for m, e in zip(mids, ends)) / 1e3
+    T = allreduce_max(T, ws)
+    Ti = allreduce_max(Ti, ws)
+    value = work * args.steps / T
+    iters_per_s = n_iter * args.steps / Ti
+
+    # ---- per-kernel timing pass (CUDA events around every kernel, same stream)
+    sol.set_timing(True)
+    flush.zero_()
+    step()
+    torch.cuda.synchronize()
+    kt = sol.timing()
+    sol.set_timing(False)
+    sol.reset()
+    pk = peaks()
+    M = cfg.M
+    # algorithmic FLOPs per projection launch: 2 nnz + 15 U + 150 C, per subset = full / M
+    flop_launch = (2 * nnz + 15 * U + 150 * C) / M / ws
+    dom = max(("fwd_resid", "back_gupd"), key=lambda k: kt[k][0])
+    ms_launch = kt[dom][0] / max(kt[dom][1], 1)
+    achieved = flop_launch / (ms_launch / 1e3) / 1e12
+    total_kt = sum(v[0] for v in kt.values())
+    N = int(np.prod(geo.img_shape))
+    upd_ms = kt["sqs_update"][0] / max(kt["sqs_update"][1], 1)
+    upd_bytes = 21 * N        # x, G, g, D_L read (16 B) + mask (1 B) + x' write (4 B) per voxel
+    roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["fp32_tflops"], "traffic": None,
+                "peak_src": f"derived: {N_SM} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
+                "flop_per_launch": flop_launch, "ms_per_launch": ms_launch,
+                "share_of_step": kt[dom][0] / total_kt}
+    streaming = {"bound": "hbm", "kernel": "sqs_update", "achieved": upd_bytes / (upd_ms / 1e3) / 1e9,
+                 "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": upd_bytes / (upd_ms / 1e3) / 1e9 / pk["hbm_gbs"],
+                 "traffic": None, "bytes_per_launch": upd_bytes, "ms_per_launch": upd_ms}
+    kernel_ms = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / total_kt} for k, v in kt.items() if v[1]}
+
+    # ---- end to end: host (pinned) inputs in, image out, inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        y_h = y.cpu().pin_memory(); w_h = w.cpu().pin_memory()
+        x_h = torch.empty(x.shape, dtype=torch.float32).pin_memory()
+        y2, w2 = torch.empty_like(y), torch.empty_like(w)
+        sol.set_data(y2, w2, dl, mask)
+        es = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+        y2.copy_(y_h); w2.copy_(w_h)
+        step()                                   # capture the graph for the new buffers
+        x_h.copy_(x)
+        barrier(ws)
+        for i in range(args.steps):
+            flush.zero_()
+            es[2 * i].record(st)
+            y2.copy_(y_h, non_blocking=True)
+            w2.copy_(w_h, non_blocking=True)
+            step()
+            x_h.copy_(x, non_blocking=True)
+            es[2 * i + 1].record(st)
+        barrier(ws)
+        Te = sum(es[2 * i].elapsed_time(es[2 * i + 1]) for i in range(args.steps)) / 1e3
+        Te = allreduce_max(Te, ws)
+        e2e = {"value": work * args.steps / Te, "unit": UNIT,
+               "h2d_bytes_per_step": int(y.numel() * 4 + w.numel() * 4), "d2h_bytes_per_step": int(x.numel() * 4),
+               "ms_per_step": 1e3 * Te / args.steps}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_oracle_sample(cfg, args.cpu_budget)
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "iters_per_s": iters_per_s, "setup_ms_per_step": 1e3 * (T - Ti) / args.steps,
+            "config": {"workload": workload_name(cfg), "config_id": cfg.name, "M": cfg.M, "n_iter": n_iter,
+                       "views_per_subset": (g["na"] + cfg.M - 1) // cfg.M, "U_full_scan": U,
+                       "nnz_full_scan": nnz, "work_per_step": work,
+                       "l2": "flushed between steps (512 MiB write, untimed)",
+                       "parallelism": f"views of each subset split over {ws} GPU(s), NCCL all-reduce of G+"},
+            "gpu_launches": int(launches), "roofline": roofline, "roofline_streaming": streaming,
+            "kernel_ms": kernel_ms, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+            "peaks": {"fp32_tflops": pk["fp32_tflops"], "hbm_gbs": pk["hbm_gbs"], "src": pk["src"]},
+        }
+        print(json.dumps(out))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,266 @@
+/*
+ * ct_oslalm.h — C ABI of the B200 (sm_100a) OS-LALM CT hot path.
+ *
+ * Method: Nien & Fessler, "Fast X-ray CT image reconstruction using a linearized
+ * augmented Lagrangian method with ordered subsets" (arXiv 1402.4381).
+ * Citations "P:n" are lines of that paper's text; "O1..O7", "G1..G21"
+ * are the readings of silent/ambiguous passages listed in DESIGN.md §Readings.
+ *
+ * Problem solved (eq. ct_recon):
+ *     x_hat in argmin_{x in Omega} 1/2 ||y - A x||_W^2 + R(x),   Omega = {x >= 0}
+ * with OS-LALM (eq. os_lalm_iterates), the SQS majoriser
+ * L_diag = diag{A' W A 1} and bit-reversal subset order, one warm-started
+ * FISTA step for the inner denoising problem (n = 1) and the
+ * deterministic downward rho-continuation with adaptive restart.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions for every call
+ * ---------------------------------------------------------------------------
+ * Pointers: every array argument is a DEVICE pointer on the geometry's device,
+ *   allocated and owned by the caller (the Python binding uses torch).  The
+ *   library owns only the opaque handles it returns (ct_geom, ct_oslalm_state)
+ *   and frees them on destroy.  No allocations happen after create.
+ * Layouts (z / detector-row fastest, chosen so that the separable footprint's
+ *   axial loops are unit-stride):
+ *     image     x[iy][ix][iz]        (nz = 1 for FAN2D)         fp32
+ *     sinogram  y[k][c][r]           (k = index into a view list, c = channel,
+ *                                     r = detector row; nt = 1 for FAN2D) fp32
+ *     mask      m[iy][ix][iz]        uint8, nonzero = voxel in the support S
+ * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *   stream).  Work is enqueued asynchronously; only the calls documented as
+ *   synchronising block the host.
+ * Errors: return CT_OK (0) or a ct_status code; ct_last_error() returns a
+ *   thread-local one-line message.  Arguments are validated before any launch
+ *   (no partial writes on CT_EINVAL).  No C++ exception crosses the boundary.
+ *   Asynchronous device faults surface at the next synchronising call.
+ */
+#ifndef CT_OSLALM_H
+#define CT_OSLALM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CT_OK = 0,
+    CT_EINVAL = 1,       /* bad argument, shape or geometry                     */
+    CT_EUNSUPPORTED = 2, /* valid but not implemented (e.g. n_inner != 1)       */
+    CT_ENOMEM = 3,       /* workspace too small / device allocation failed     */
+    CT_ECUDA = 4,        /* CUDA runtime error                                 */
+    CT_ENCCL = 5,        /* NCCL error                                         */
+    CT_ESTATE = 6        /* state/handle used inconsistently                   */
+} ct_status;
+
+typedef enum { CT_FAN2D = 0, CT_CONE_AXIAL = 1, CT_CONE_HELICAL = 2 } ct_geom_kind;
+
+/*
+ * Scan geometry (reading O1).  Arc (equi-angular) detector of radius dsd centred
+ * on the source.  Voxel centres x_i = (i - (nx-1)/2) dx + offx (same for y, z).
+ * View v: beta_v = orbit_start + 2 pi turns v / na, turns = orbit_deg / 360;
+ * source at (-dso sin beta, dso cos beta, z_s(v)) with
+ * z_s(v) = (v - (na-1)/2) * pitch * nt * dt * (dso/dsd) / (na/turns) (helical; 0 otherwise).
+ * Channel c sits at fan angle gamma_c = (c - (ns-1)/2 - offs) ds / dsd; row r at
+ * height t_r = (r - (nt-1)/2 - offt) dt on the cylindrical detector.
+ * Lengths in mm, angles in degrees.  dx must equal dy.
+ */
+typedef struct {
+    int kind;                 /* ct_geom_kind */
+    int nx, ny, nz;
+    double dx, dy, dz;
+    double offx, offy, offz;
+    int ns, nt;
+    double ds, dt;
+    double offs, offt;
+    double dso, dsd;
+    int na;
+    double orbit_deg, orbit_start_deg;
+    double pitch;
+    int device;               /* CUDA device ordinal for all calls on this geometry */
+} ct_geom_desc;
+
+typedef struct ct_geom ct_geom;
+
+/* A view list {first + k*stride : 0 <= k < count}.  Subset m of M (reading G12):
+ * {m, M, ceil((na-m)/M)}; the full scan: {0, 1, na}. */
+typedef struct {
+    int first, stride, count;
+} ct_views;
+
+/* Validate the description and build per-view tables on the device.
+ * The geometry is immutable afterwards and may be shared between streams.
+ * Returns CT_EINVAL for inconsistent sizes, CT_EUNSUPPORTED if some voxel's
+ * transaxial footprint could span more than 7 channels (kernel window limit). */
+int ct_geom_create(const ct_geom_desc* desc, ct_geom** out);
+void ct_geom_destroy(ct_geom* g);
+const char* ct_last_error(void);
+
+/*
+ * Forward projection y = A_v x over the view list v ("one multiplication
+ * by A"; system matrix A = separable-footprint SF-TR with A1 amplitude, reading
+ * O2 / G1):  a_ij = l_phi * l_theta * F_s(c) * F_t(r).
+ * x: [ny][nx][nz]; y: [count][ns][nt], overwritten.  Deterministic, no atomics.
+ */
+int ct_fwd_proj(const ct_geom* g, ct_views v, const float* x, float* y, void* stream);
+
+/*
+ * Back projection x (+)= A_v' y, the exact adjoint of ct_fwd_proj (same a_ij).
+ * y: [count][ns][nt]; x: [ny][nx][nz]; accumulate != 0 adds to x, else overwrites.
+ */
+int ct_back_proj(const ct_geom* g, ct_views v, const float* y, float* x, int accumulate, void* stream);
+
+/*
+ * SQS denominator (L_diag = diag{A' W A 1}; reading O4/G13):
+ *   D_L = A'(W .* (A 1_S)) over all na views, then S <- S and {D_L > 0},
+ *   D_L := 0 off S.
+ * w: [na][ns][nt] statistical weights; mask_inout: [ny][nx][nz] (updated in place);
+ * dl: [ny][nx][nz] output.  `scratch` is a device buffer of at least
+ * ct_sqs_denom_scratch_bytes() bytes (caller-owned).
+ */
+int ct_sqs_denom_scratch_bytes(const ct_geom* g, size_t* out);
+int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask_inout, float* dl, void* scratch,
+                 void* stream);
+
+/*
+ * Edge-preserving regulariser ("R is an edge-preserving regularizer";
+ * reading G3/G14):  R(x) = beta sum_{unordered pairs {j,k} in S, k in N(j)} w_jk psi(x_j - x_k)
+ * with the Fair potential psi(t) = delta^2 (|t|/delta - ln(1 + |t|/delta)),
+ * N = 8 in-plane neighbours (nbr = 8) or the 26-neighbourhood (nbr = 26, 3D),
+ * w_jk = 1/||offset||.  Writes grad_j = beta sum_k w_jk psi'(x_j - x_k) and,
+ * if curv != NULL, the Huber curvature D_R,j = 2 beta sum_k w_jk / (1 + |x_j - x_k|/delta).
+ * Both are 0 off S.
+ */
+typedef struct {
+    double beta, delta;
+    int nbr; /* 8 or 26 */
+} ct_reg;
+
+int ct_reg_grad(const ct_geom* g, const ct_reg* r, const uint8_t* mask, const float* x, float* grad,
+                float* curv, void* stream);
+
+/*
+ * Work counts of a view list (the throughput metric's units):
+ *   out_host[0] = U   = #(view, voxel in mask) pairs with a non-empty footprint,
+ *   out_host[1] = nnz = #non-zero a_ij of those pairs (channels x rows overlapped),
+ *   out_host[2] = C   = #(view, voxel column) pairs with >= 1 voxel counted in U.
+ * Evaluated with fp64 geometry.  SYNCHRONISING.  `scratch`: device buffer >= 32 bytes.
+ */
+int ct_count_vv(const ct_geom* g, ct_views v, const uint8_t* mask, void* scratch, long long* out_host,
+                void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* OS-LALM                                                                  */
+/* ------------------------------------------------------------------------ */
+
+typedef enum { CT_RHO_FIXED = 0, CT_RHO_CONTINUATION = 1 } ct_rho_mode;
+
+typedef struct {
+    int M;            /* number of ordered subsets, 1 <= M <= na            */
+    int mode;         /* ct_rho_mode                                        */
+    double rho_fixed; /* FIXED mode: AL penalty rho in (0, 1]               */
+    double rho_min;   /* CONTINUATION floor, P:516 uses 1e-3                */
+    int n_inner;      /* FISTA steps for the inner problem; only 1 supported */
+    ct_reg reg;
+} ct_oslalm_cfg;
+
+/* Caller-owned device arrays describing the problem. */
+typedef struct {
+    const float* y;      /* [na][ns][nt] post-log sinogram                     */
+    const float* w;      /* [na][ns][nt] statistical weights W                 */
+    const float* dl;     /* [ny][nx][nz] D_L from ct_sqs_denom (0 off S)       */
+    const uint8_t* mask; /* [ny][nx][nz] support S from ct_sqs_denom           */
+} ct_oslalm_data;
+
+typedef struct ct_oslalm_state ct_oslalm_state;
+
+/* Per inner step diagnostics (host memory, caller-owned). */
+typedef struct {
+    double* rho;   /* rho used in the step                              */
+    double* xi;    /* restart indicator xi, fp64            */
+    int* restart;  /* 1 if xi > 0 (counter l reset), else 0             */
+    int capacity;  /* entries available                                 */
+    int count;     /* entries written (output)                          */
+} ct_oslalm_log;
+
+/* Device pointers into a state's workspace (for tests and checkpointing). */
+typedef struct {
+    float* g;        /* split gradient g                          */
+    float* G;        /* current scaled subset gradient M grad l_m(x)      */
+    double* rho;     /* rho for the next inner step                       */
+    long long* l;    /* continuation counter                              */
+    long long* step; /* inner steps taken                                 */
+    int initialised; /* 0 until the first ct_oslalm_iter/run              */
+} ct_oslalm_state_view;
+
+/*
+ * Workspace bytes for a state (g, two G buffers, the alternate image, one
+ * subset's residual sinogram, fp64 reduction partials, scalars and a device log).
+ */
+int ct_oslalm_state_bytes(const ct_geom* g, const ct_oslalm_cfg* cfg, size_t* out);
+
+/* Create a state over a caller-owned device workspace of `bytes` bytes.
+ * The handle keeps the cfg, an internal capture stream and CUDA-graph caches. */
+int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* cfg, void* workspace, size_t bytes,
+                           ct_oslalm_state** out);
+void ct_oslalm_state_destroy(ct_oslalm_state* s);
+int ct_oslalm_state_get(const ct_oslalm_state* s, ct_oslalm_state_view* out);
+
+/* Forget the iterate history (next iter re-initialises G, g, l, rho); keeps graphs. */
+int ct_oslalm_state_reset(ct_oslalm_state* s);
+
+/*
+ * Diagnostic per-kernel timing (CUDA events on the launching stream around every
+ * kernel of the inner step; disables graph replay while enabled).  Classes:
+ * 0 sqs_update (K3), 1 forward+residual (K1), 2 back-projection+epilogue (K2),
+ * 3 xi/rho finalize (K4), 4 multi-rank exchange (all-reduce + g-update).
+ * get_timing returns accumulated milliseconds and launch counts per class.
+ */
+int ct_oslalm_set_timing(ct_oslalm_state* s, int enable);
+int ct_oslalm_get_timing(const ct_oslalm_state* s, double* ms5, long long* count5);
+
+/*
+ * One outer iteration = M inner steps in bit-reversal order (reading O7):
+ *   rho <- FIXED ? rho_fixed : rho_l(l)
+ *   x   <- max(0, x - (rho G + (1-rho) g + grad R(x)) / (rho D_L + D_R(x)))   on S, 0 off S
+ *   G+  <- M A_m'(W (A_m x - y)),  m = next subset    (fused residual in the projection)
+ *   xi  <- sum_S (g - G+)(G+ - G);  g <- (rho G+ + g)/(1 + rho);  G <- G+   
+ *   CONTINUATION: l <- (xi > 0) ? 0 : l + 1
+ * The first call also initialises G = g = M A_{m0}'(W(A_{m0} x - y)), l = 0
+ * (reading G10).  x [ny][nx][nz] is read and updated in place.  With one rank
+ * the whole iteration is captured once as a CUDA graph and replayed.
+ */
+int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_data* data, ct_oslalm_state* s,
+                   float* x, void* stream);
+
+/*
+ * n_iter iterations (n_iter forward/back-projection pairs).
+ * SYNCHRONISING at the end (returns the status of the whole run).  If log is
+ * non-NULL the per-inner-step rho, xi and restart flags are copied into it.
+ */
+int ct_oslalm_run(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_data* data, ct_oslalm_state* s,
+                  float* x, int n_iter, ct_oslalm_log* log, void* stream);
+
+/*
+ * Multi-GPU: attach an NCCL communicator to the geometry.
+ * `nccl_uid` points to the 128-byte ncclUniqueId created by rank 0 and broadcast
+ * by the caller (torch.distributed).  Afterwards ct_oslalm_iter/run on this
+ * geometry process only this rank's contiguous block of each subset's views and
+ * sum the partial back-projections with ncclAllReduce (fp32) before the g-update.
+ * NCCL is loaded at run time (libnccl.so.2); CT_ENCCL if unavailable.
+ */
+int ct_comm_init(ct_geom* g, int rank, int nranks, const void* nccl_uid);
+int ct_comm_get_unique_id(void* nccl_uid_out128);
+
+/* Library identification string (kernel names, target). */
+const char* ct_build_info(void);
+
+/* Number of CUDA kernels this library has launched in the process so far (a graph
+ * replay counts its kernel nodes).  Used by the benchmark's gpu_launches report. */
+unsigned long long ct_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CT_OSLALM_H */

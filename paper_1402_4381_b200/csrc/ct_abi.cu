@@ -1,0 +1,797 @@
+// ct_abi.cu — C ABI of the OS-LALM CT hot path on B200 (sm_100a):
+// geometry tables, kernel launches, the OS-LALM inner-step sequence with CUDA
+// graph replay, and the NCCL (multi-GPU) exchange.  See include/ct_oslalm.h for
+// the contract of every entry point and DESIGN.md for the design.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/ct_oslalm.h"
+#include "ct_kernels.cuh"
+
+using namespace ct;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local char g_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+static int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CT_CUDA(call)                                                                          \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) return fail(CT_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CT_LAUNCHED(nk)                                                                        \
+    do {                                                                                       \
+        cudaError_t e_ = cudaGetLastError();                                                   \
+        if (e_ != cudaSuccess) return fail(CT_ECUDA, "kernel launch: %s", cudaGetErrorString(e_)); \
+        g_launches += (nk);                                                                    \
+    } while (0)
+
+extern "C" const char* ct_last_error(void) { return g_err; }
+extern "C" unsigned long long ct_kernel_launches(void) { return g_launches.load(); }
+extern "C" const char* ct_build_info(void) {
+    return "ct_oslalm sm_100a: fwd2d fwd3d back2d back3d sqs_update reg_grad gupd xi_finalize count_vv";
+}
+
+// ---------------------------------------------------------------------------
+// NCCL (loaded at run time; torch has already loaded libnccl.so.2)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+static std::mutex g_nccl_mu;
+
+static bool load_nccl() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.ok) return true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+    g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+    return g_nccl.ok;
+}
+
+// ---------------------------------------------------------------------------
+// geometry
+// ---------------------------------------------------------------------------
+struct ct_geom {
+    ct_geom_desc d;
+    DevGeom dg;
+    DevGeomD dgd;
+    float4* d_views = nullptr;
+    double2* d_vz = nullptr;
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
+};
+
+static inline int nz_of(const ct_geom* g) { return g->d.kind == CT_FAN2D ? 1 : g->d.nz; }
+static inline int nt_of(const ct_geom* g) { return g->d.kind == CT_FAN2D ? 1 : g->d.nt; }
+static inline size_t n_vox(const ct_geom* g) { return (size_t)g->d.nx * g->d.ny * nz_of(g); }
+static inline size_t n_cells_view(const ct_geom* g) { return (size_t)g->d.ns * nt_of(g); }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
+    if (!d || !out) return fail(CT_EINVAL, "ct_geom_create: null argument");
+    *out = nullptr;
+    if (d->kind < CT_FAN2D || d->kind > CT_CONE_HELICAL) return fail(CT_EINVAL, "unknown geometry kind %d", d->kind);
+    bool is2d = d->kind == CT_FAN2D;
+    int nz = is2d ? 1 : d->nz, nt = is2d ? 1 : d->nt;
+    if (d->nx < 1 || d->ny < 1 || nz < 1 || d->ns < 1 || nt < 1 || d->na < 1)
+        return fail(CT_EINVAL, "sizes must be positive (nx=%d ny=%d nz=%d ns=%d nt=%d na=%d)", d->nx, d->ny, nz, d->ns,
+                    nt, d->na);
+    if (!(d->dx > 0 && d->dy > 0 && d->ds > 0 && d->dso > 0 && d->dsd > d->dso) || (!is2d && !(d->dz > 0 && d->dt > 0)))
+        return fail(CT_EINVAL, "spacings must be positive and dsd > dso");
+    if (fabs(d->dx - d->dy) > 1e-9 * d->dx) return fail(CT_EINVAL, "dx must equal dy (square voxels)");
+    if (!is2d && nt > 128) return fail(CT_EUNSUPPORTED, "nt = %d > 128 detector rows", nt);
+    if (d->kind == CT_CONE_HELICAL && !(d->pitch > 0)) return fail(CT_EINVAL, "helical geometry needs pitch > 0");
+    // footprint width bound: voxel half-diagonal magnified at the closest approach
+    double hx = 0.5 * (d->nx - 1) * d->dx + fabs(d->offx) + d->dx, hy = 0.5 * (d->ny - 1) * d->dy + fabs(d->offy) + d->dy;
+    double rmax = sqrt(hx * hx + hy * hy);
+    if (rmax >= d->dso) return fail(CT_EINVAL, "image (radius %.1f mm) reaches the source orbit (dso %.1f)", rmax, d->dso);
+    double wmax = d->dx * sqrt(2.0) * d->dsd / ((d->dso - rmax) * d->ds) + 1.0;
+    if (wmax > kMaxFoot - 1)
+        return fail(CT_EUNSUPPORTED, "voxel footprint may span %.1f channels (> %d)", wmax, kMaxFoot - 1);
+
+    int dev = d->device;
+    DeviceGuard guard(dev);
+    ct_geom* g = new ct_geom();
+    g->d = *d;
+    g->d.nz = nz;
+    g->d.nt = nt;
+    DevGeom& dg = g->dg;
+    dg.kind = d->kind;
+    dg.nx = d->nx; dg.ny = d->ny; dg.nz = nz; dg.ns = d->ns; dg.nt = nt; dg.na = d->na;
+    dg.dx = (float)d->dx; dg.dy = (float)d->dy; dg.dz = is2d ? 1.0f : (float)d->dz;
+    dg.x0 = (float)(-(d->nx - 1) / 2.0 * d->dx + d->offx);
+    dg.y0 = (float)(-(d->ny - 1) / 2.0 * d->dy + d->offy);
+    double z0 = is2d ? 0.0 : (-(nz - 1) / 2.0 * d->dz + d->offz);
+    double zb0 = is2d ? -0.5 : z0 - 0.5 * d->dz;
+    dg.zb0 = (float)zb0;
+    dg.dso = (float)d->dso; dg.dsd = (float)d->dsd;
+    dg.dsd_ds = (float)(d->dsd / d->ds);
+    dg.cbase = (float)((d->ns - 1) / 2.0 + d->offs);
+    dg.rbase = (float)((nt - 1) / 2.0 + d->offt);
+    dg.dt = is2d ? 1.0f : (float)d->dt;
+
+    std::vector<float4> hv(d->na);
+    std::vector<double2> hvz(d->na);
+    double turns = d->orbit_deg / 360.0;
+    double h = d->kind == CT_CONE_HELICAL ? d->pitch * nt * d->dt * d->dso / d->dsd : 0.0;
+    for (int v = 0; v < d->na; v++) {
+        double beta = d->orbit_start_deg * M_PI / 180.0 + 2.0 * M_PI * turns * v / d->na;
+        double zs = d->kind == CT_CONE_HELICAL ? (v - (d->na - 1) / 2.0) * h / (d->na / turns) : 0.0;
+        double q = is2d ? 0.0 : (zs - zb0) / d->dz;
+        double qi = floor(q);
+        hv[v] = make_float4((float)sin(beta), (float)cos(beta), (float)qi, (float)(q - qi));
+        hvz[v] = make_double2(beta, zs);
+    }
+    DevGeomD& gd = g->dgd;
+    gd.kind = d->kind; gd.nx = d->nx; gd.ny = d->ny; gd.nz = nz; gd.ns = d->ns; gd.nt = nt;
+    gd.dx = d->dx; gd.dy = d->dy; gd.dz = is2d ? 1.0 : d->dz;
+    gd.x0 = -(d->nx - 1) / 2.0 * d->dx + d->offx;
+    gd.y0 = -(d->ny - 1) / 2.0 * d->dy + d->offy;
+    gd.z0 = z0;
+    gd.dso = d->dso; gd.dsd = d->dsd; gd.ds = d->ds; gd.dt = is2d ? 1.0 : d->dt; gd.offs = d->offs; gd.offt = d->offt;
+    gd.s_lo = (0 - (d->ns - 1) / 2.0 - d->offs) * d->ds - 0.5 * d->ds;
+    gd.s_hi = ((d->ns - 1) - (d->ns - 1) / 2.0 - d->offs) * d->ds + 0.5 * d->ds;
+    gd.t_lo = (0 - (nt - 1) / 2.0 - d->offt) * gd.dt - 0.5 * gd.dt;
+    gd.t_hi = ((nt - 1) - (nt - 1) / 2.0 - d->offt) * gd.dt + 0.5 * gd.dt;
+
+    cudaError_t e = cudaMalloc(&g->d_views, sizeof(float4) * d->na);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_vz, sizeof(double2) * d->na);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_views, hv.data(), sizeof(float4) * d->na, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_vz, hvz.data(), sizeof(double2) * d->na, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(g->d_views);
+        cudaFree(g->d_vz);
+        delete g;
+        return fail(e == cudaErrorMemoryAllocation ? CT_ENOMEM : CT_ECUDA, "geometry tables: %s", cudaGetErrorString(e));
+    }
+    dg.views = g->d_views;
+    gd.vz = g->d_vz;
+    *out = g;
+    return CT_OK;
+}
+
+extern "C" void ct_geom_destroy(ct_geom* g) {
+    if (!g) return;
+    DeviceGuard guard(g->d.device);
+    if (g->comm && g_nccl.ok) g_nccl.CommDestroy(g->comm);
+    cudaFree(g->d_views);
+    cudaFree(g->d_vz);
+    delete g;
+}
+
+static int check_views(const ct_geom* g, ct_views v) {
+    if (v.count < 0 || v.stride < 1 || v.first < 0) return fail(CT_EINVAL, "bad view list {%d,%d,%d}", v.first, v.stride, v.count);
+    if (v.count > 0 && (long long)v.first + (long long)(v.count - 1) * v.stride >= g->d.na)
+        return fail(CT_EINVAL, "view list {%d,%d,%d} exceeds na=%d", v.first, v.stride, v.count, g->d.na);
+    return CT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+template <bool RESID>
+static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, const float* yobs, const float* w,
+                      float scale, cudaStream_t st) {
+    if (v.count == 0) return CT_OK;
+    const DevGeom& dg = g->dg;
+    if (dg.kind == CT_FAN2D) {
+        constexpr int TC = 32;
+        dim3 grid((dg.ns + TC - 1) / TC, v.count);
+        fwd2d_kernel<TC, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+    } else {
+        constexpr int TC = 16;
+        dim3 grid((dg.ns + TC - 1) / TC, v.count);
+        if (dg.nt <= 32)
+            fwd3d_kernel<TC, 32, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+        else if (dg.nt <= 64)
+            fwd3d_kernel<TC, 64, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+        else
+            fwd3d_kernel<TC, 128, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+    }
+    CT_LAUNCHED(1);
+    return CT_OK;
+}
+
+static void back_grid(const ct_geom* g, dim3& grid) {
+    const DevGeom& dg = g->dg;
+    if (dg.kind == CT_FAN2D)
+        grid = dim3((dg.nx + 31) / 32, (dg.ny + 7) / 8, 1);
+    else
+        grid = dim3((dg.nx + 7) / 8, dg.ny, (dg.nz + 31) / 32);
+}
+
+static size_t back_nblocks(const ct_geom* g) {
+    dim3 gr;
+    back_grid(g, gr);
+    return (size_t)gr.x * gr.y * gr.z;
+}
+
+template <int EPI>
+static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, const GupdArgs& ga, cudaStream_t st) {
+    const DevGeom& dg = g->dg;
+    dim3 grid;
+    back_grid(g, grid);
+    if (dg.kind == CT_FAN2D)
+        back2d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+    else
+        back3d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+    CT_LAUNCHED(1);
+    return CT_OK;
+}
+
+static inline unsigned nblk(size_t n) { return (unsigned)((n + 255) / 256); }
+
+// ---------------------------------------------------------------------------
+// projections, D_L, regulariser, U
+// ---------------------------------------------------------------------------
+extern "C" int ct_fwd_proj(const ct_geom* g, ct_views v, const float* x, float* y, void* stream) {
+    if (!g || !x || !y) return fail(CT_EINVAL, "ct_fwd_proj: null argument");
+    if (int e = check_views(g, v)) return e;
+    DeviceGuard guard(g->d.device);
+    return launch_fwd<false>(g, v, x, y, nullptr, nullptr, 1.0f, (cudaStream_t)stream);
+}
+
+extern "C" int ct_back_proj(const ct_geom* g, ct_views v, const float* y, float* x, int accumulate, void* stream) {
+    if (!g || !x || (!y && v.count > 0)) return fail(CT_EINVAL, "ct_back_proj: null argument");
+    if (int e = check_views(g, v)) return e;
+    DeviceGuard guard(g->d.device);
+    GupdArgs ga{};
+    if (accumulate) return launch_back<EPI_ACCUM>(g, v, y, x, ga, (cudaStream_t)stream);
+    return launch_back<EPI_STORE>(g, v, y, x, ga, (cudaStream_t)stream);
+}
+
+extern "C" int ct_sqs_denom_scratch_bytes(const ct_geom* g, size_t* out) {
+    if (!g || !out) return fail(CT_EINVAL, "ct_sqs_denom_scratch_bytes: null argument");
+    *out = n_vox(g) * sizeof(float) + (size_t)g->d.na * n_cells_view(g) * sizeof(float) + 256;
+    return CT_OK;
+}
+
+extern "C" int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask, float* dl, void* scratch, void* stream) {
+    if (!g || !w || !mask || !dl || !scratch) return fail(CT_EINVAL, "ct_sqs_denom: null argument");
+    DeviceGuard guard(g->d.device);
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t N = n_vox(g);
+    float* one = (float*)scratch;
+    float* sino = (float*)(((uintptr_t)(one + N) + 255) & ~(uintptr_t)255);
+    ct_views all{0, 1, g->d.na};
+    mask_to_float_kernel<<<nblk(N), 256, 0, st>>>(mask, one, N);
+    CT_LAUNCHED(1);
+    if (int e = launch_fwd<true>(g, all, one, sino, nullptr, w, 1.0f, st)) return e;
+    GupdArgs ga{};
+    if (int e = launch_back<EPI_STORE>(g, all, sino, dl, ga, st)) return e;
+    mask_finalize_kernel<<<nblk(N), 256, 0, st>>>(mask, dl, N);
+    CT_LAUNCHED(1);
+    return CT_OK;
+}
+
+static int reg_launch(const ct_geom* g, const ct_reg* r, const uint8_t* mask, const float* x, float* grad, float* curv,
+                      cudaStream_t st) {
+    size_t N = n_vox(g);
+    float inv_d = (float)(1.0 / r->delta);
+    if (r->nbr == 8)
+        reg_grad_kernel<8><<<nblk(N), 256, 0, st>>>(g->dg, x, mask, grad, curv, (float)r->beta, inv_d, N);
+    else
+        reg_grad_kernel<26><<<nblk(N), 256, 0, st>>>(g->dg, x, mask, grad, curv, (float)r->beta, inv_d, N);
+    CT_LAUNCHED(1);
+    return CT_OK;
+}
+
+static int check_reg(const ct_geom* g, const ct_reg* r) {
+    if (!r) return fail(CT_EINVAL, "null regulariser");
+    if (!(r->nbr == 8 || r->nbr == 26)) return fail(CT_EINVAL, "nbr must be 8 or 26 (got %d)", r->nbr);
+    if (r->nbr == 26 && g->d.kind == CT_FAN2D) return fail(CT_EINVAL, "nbr = 26 needs a 3D geometry");
+    if (!(r->delta > 0) || !(r->beta >= 0)) return fail(CT_EINVAL, "need delta > 0 and beta >= 0");
+    return CT_OK;
+}
+
+extern "C" int ct_reg_grad(const ct_geom* g, const ct_reg* r, const uint8_t* mask, const float* x, float* grad,
+                           float* curv, void* stream) {
+    if (!g || !mask || !x || !grad) return fail(CT_EINVAL, "ct_reg_grad: null argument");
+    if (int e = check_reg(g, r)) return e;
+    DeviceGuard guard(g->d.device);
+    return reg_launch(g, r, mask, x, grad, curv, (cudaStream_t)stream);
+}
+
+extern "C" int ct_count_vv(const ct_geom* g, ct_views v, const uint8_t* mask, void* scratch, long long* out, void* stream) {
+    if (!g || !mask || !scratch || !out) return fail(CT_EINVAL, "ct_count_vv: null argument");
+    if (int e = check_views(g, v)) return e;
+    DeviceGuard guard(g->d.device);
+    cudaStream_t st = (cudaStream_t)stream;
+    CT_CUDA(cudaMemsetAsync(scratch, 0, 3 * sizeof(unsigned long long), st));
+    size_t n = (size_t)g->d.nx * g->d.ny * v.count;
+    if (n) {
+        count_vv_kernel<<<nblk(n), 256, 0, st>>>(g->dgd, v.first, v.stride, v.count, mask, (unsigned long long*)scratch);
+        CT_LAUNCHED(1);
+    }
+    unsigned long long h[3] = {0, 0, 0};
+    CT_CUDA(cudaMemcpyAsync(h, scratch, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CT_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < 3; i++) out[i] = (long long)h[i];
+    return CT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// OS-LALM state
+// ---------------------------------------------------------------------------
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    const void* key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int curG = -1;
+    size_t nodes = 0;
+};
+
+struct ct_oslalm_state {
+    const ct_geom* g;
+    ct_oslalm_cfg cfg;
+    std::vector<int> order;
+    size_t N, sino_elems, nparts;
+    float* gs;
+    float* Gbuf[2];
+    float* xalt;
+    float* Gtmp;
+    float* sino;
+    double* xi_part;
+    Scalars* sc;
+    double* dlog;        // M x 3 doubles (per iteration)
+    int curG = 0;
+    int initialised = 0;
+    cudaStream_t cap = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    GraphEntry graphs[2];
+    // diagnostic per-kernel timing
+    int timing = 0;
+    std::vector<cudaEvent_t> evpool;
+    std::vector<std::pair<int, int>> evmarks;   // (class, index of start event)
+    double tms[5] = {0, 0, 0, 0, 0};
+    long long tcnt[5] = {0, 0, 0, 0, 0};
+};
+
+static int tmark(ct_oslalm_state* s, cudaStream_t st) {
+    if (!s->timing) return -1;
+    size_t i = 0;
+    for (auto& m : s->evmarks) i = std::max(i, (size_t)m.second + 2);
+    if (s->evpool.size() < i + 2) {
+        while (s->evpool.size() < i + 2) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            s->evpool.push_back(e);
+        }
+    }
+    cudaEventRecord(s->evpool[i], st);
+    return (int)i;
+}
+
+static void tmark_end(ct_oslalm_state* s, cudaStream_t st, int cls, int i0) {
+    if (!s->timing || i0 < 0) return;
+    cudaEventRecord(s->evpool[i0 + 1], st);
+    s->evmarks.push_back({cls, i0});
+}
+
+static int tcollect(ct_oslalm_state* s) {
+    if (!s->timing || s->evmarks.empty()) return CT_OK;
+    CT_CUDA(cudaEventSynchronize(s->evpool[s->evmarks.back().second + 1]));
+    for (auto& m : s->evmarks) {
+        float ms = 0;
+        CT_CUDA(cudaEventElapsedTime(&ms, s->evpool[m.second], s->evpool[m.second + 1]));
+        s->tms[m.first] += ms;
+        s->tcnt[m.first] += 1;
+    }
+    s->evmarks.clear();
+    return CT_OK;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+static void bit_reversal(int M, std::vector<int>& order) {
+    int bits = 0;
+    while ((1 << bits) < M) bits++;
+    order.clear();
+    for (int i = 0; i < (1 << bits); i++) {
+        int r = 0;
+        for (int b = 0; b < bits; b++)
+            if (i & (1 << b)) r |= 1 << (bits - 1 - b);
+        if (r < M) order.push_back(r);
+    }
+}
+
+static int check_cfg(const ct_geom* g, const ct_oslalm_cfg* c) {
+    if (!c) return fail(CT_EINVAL, "null cfg");
+    if (c->M < 1 || c->M > g->d.na) return fail(CT_EINVAL, "M = %d must be in [1, na = %d]", c->M, g->d.na);
+    if (c->mode != CT_RHO_FIXED && c->mode != CT_RHO_CONTINUATION) return fail(CT_EINVAL, "bad rho mode %d", c->mode);
+    if (c->mode == CT_RHO_FIXED && !(c->rho_fixed > 0 && c->rho_fixed <= 1))
+        return fail(CT_EINVAL, "rho_fixed must be in (0, 1]");
+    if (c->mode == CT_RHO_CONTINUATION && !(c->rho_min > 0 && c->rho_min <= 1))
+        return fail(CT_EINVAL, "rho_min must be in (0, 1]");
+    if (c->n_inner != 1) return fail(CT_EUNSUPPORTED, "n_inner = %d: only one inner FISTA step is implemented", c->n_inner);
+    return check_reg(g, &c->reg);
+}
+
+static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[10], size_t* total) {
+    size_t N = n_vox(g);
+    int maxcount = (g->d.na + c->M - 1) / c->M;
+    size_t sino = (size_t)maxcount * n_cells_view(g);
+    size_t nparts = std::max(back_nblocks(g), (size_t)nblk(N));
+    size_t o = 0;
+    off[0] = o; o += align256(N * 4);       // g
+    off[1] = o; o += align256(N * 4);       // G0
+    off[2] = o; o += align256(N * 4);       // G1
+    off[3] = o; o += align256(N * 4);       // xalt
+    off[4] = o; o += align256(N * 4);       // Gtmp (multi-rank)
+    off[5] = o; o += align256(sino * 4);    // residual sinogram
+    off[6] = o; o += align256(nparts * 8);  // xi partials
+    off[7] = o; o += align256(sizeof(Scalars));
+    off[8] = o; o += align256((size_t)c->M * 3 * 8);  // device log
+    *total = o;
+}
+
+extern "C" int ct_oslalm_state_bytes(const ct_geom* g, const ct_oslalm_cfg* c, size_t* out) {
+    if (!g || !out) return fail(CT_EINVAL, "ct_oslalm_state_bytes: null argument");
+    if (int e = check_cfg(g, c)) return e;
+    size_t off[10];
+    state_layout(g, c, off, out);
+    return CT_OK;
+}
+
+extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, void* ws, size_t bytes,
+                                      ct_oslalm_state** out) {
+    if (!g || !ws || !out) return fail(CT_EINVAL, "ct_oslalm_state_create: null argument");
+    if (int e = check_cfg(g, c)) return e;
+    size_t off[10], total;
+    state_layout(g, c, off, &total);
+    if (bytes < total) return fail(CT_ENOMEM, "workspace of %zu bytes < required %zu", bytes, total);
+    if ((uintptr_t)ws & 255) return fail(CT_EINVAL, "workspace must be 256-byte aligned");
+    DeviceGuard guard(g->d.device);
+    ct_oslalm_state* s = new ct_oslalm_state();
+    s->g = g;
+    s->cfg = *c;
+    bit_reversal(c->M, s->order);
+    s->N = n_vox(g);
+    s->nparts = std::max(back_nblocks(g), (size_t)nblk(s->N));
+    char* b = (char*)ws;
+    s->gs = (float*)(b + off[0]);
+    s->Gbuf[0] = (float*)(b + off[1]);
+    s->Gbuf[1] = (float*)(b + off[2]);
+    s->xalt = (float*)(b + off[3]);
+    s->Gtmp = (float*)(b + off[4]);
+    s->sino = (float*)(b + off[5]);
+    s->xi_part = (double*)(b + off[6]);
+    s->sc = (Scalars*)(b + off[7]);
+    s->dlog = (double*)(b + off[8]);
+    cudaError_t e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        delete s;
+        return fail(CT_ECUDA, "state streams: %s", cudaGetErrorString(e));
+    }
+    *out = s;
+    return CT_OK;
+}
+
+extern "C" void ct_oslalm_state_destroy(ct_oslalm_state* s) {
+    if (!s) return;
+    DeviceGuard guard(s->g->d.device);
+    for (auto& ge : s->graphs)
+        if (ge.exec) cudaGraphExecDestroy(ge.exec);
+    for (auto e : s->evpool) cudaEventDestroy(e);
+    if (s->cap) cudaStreamDestroy(s->cap);
+    if (s->ev_in) cudaEventDestroy(s->ev_in);
+    if (s->ev_out) cudaEventDestroy(s->ev_out);
+    delete s;
+}
+
+extern "C" int ct_oslalm_state_reset(ct_oslalm_state* s) {
+    if (!s) return fail(CT_EINVAL, "ct_oslalm_state_reset: null argument");
+    s->initialised = 0;
+    return CT_OK;
+}
+
+extern "C" int ct_oslalm_set_timing(ct_oslalm_state* s, int enable) {
+    if (!s) return fail(CT_EINVAL, "ct_oslalm_set_timing: null argument");
+    s->timing = enable ? 1 : 0;
+    for (int i = 0; i < 5; i++) { s->tms[i] = 0; s->tcnt[i] = 0; }
+    s->evmarks.clear();
+    return CT_OK;
+}
+
+extern "C" int ct_oslalm_get_timing(const ct_oslalm_state* s, double* ms5, long long* cnt5) {
+    if (!s || !ms5 || !cnt5) return fail(CT_EINVAL, "ct_oslalm_get_timing: null argument");
+    for (int i = 0; i < 5; i++) { ms5[i] = s->tms[i]; cnt5[i] = s->tcnt[i]; }
+    return CT_OK;
+}
+
+extern "C" int ct_oslalm_state_get(const ct_oslalm_state* s, ct_oslalm_state_view* out) {
+    if (!s || !out) return fail(CT_EINVAL, "ct_oslalm_state_get: null argument");
+    out->g = s->gs;
+    out->G = s->Gbuf[s->curG];
+    out->rho = &s->sc->rho;
+    out->l = &s->sc->l;
+    out->step = &s->sc->step;
+    out->initialised = s->initialised;
+    return CT_OK;
+}
+
+// views of subset m owned by this rank (contiguous block)
+static ct_views rank_views(const ct_geom* g, int M, int m) {
+    int count = (g->d.na - m + M - 1) / M;
+    int base = count / g->nranks, extra = count % g->nranks;
+    int k0 = g->rank * base + std::min(g->rank, extra);
+    int n = base + (g->rank < extra ? 1 : 0);
+    return ct_views{m + k0 * M, M, n};
+}
+
+static int allreduce(const ct_geom* g, float* buf, size_t n, cudaStream_t st) {
+    ncclResult_t r = g_nccl.AllReduce(buf, buf, n, ncclFloat32, ncclSum, g->comm, st);
+    if (r != ncclSuccess)
+        return fail(CT_ENCCL, "ncclAllReduce: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error");
+    return CT_OK;
+}
+
+// G+ = M A_m'(W (A_m x - y)) for subset m with the requested epilogue.
+static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const float* x, int m, int epi, cudaStream_t st) {
+    const ct_geom* g = s->g;
+    int M = s->cfg.M;
+    ct_views v = rank_views(g, M, m);
+    int t0 = tmark(s, st);
+    if (int e = launch_fwd<true>(g, v, x, s->sino, d->y, d->w, (float)M, st)) return e;
+    tmark_end(s, st, 1, t0);
+    GupdArgs ga{};
+    ga.mask = d->mask;
+    ga.rho = &s->sc->rho;
+    ga.xi_part = s->xi_part;
+    ga.gs = s->gs;
+    if (g->nranks == 1) {
+        if (epi == EPI_INIT) {
+            ga.G_new = s->Gbuf[s->curG];
+            return launch_back<EPI_INIT>(g, v, s->sino, nullptr, ga, st);
+        }
+        ga.G_old = s->Gbuf[s->curG];
+        ga.G_new = s->Gbuf[s->curG ^ 1];
+        int t1 = tmark(s, st);
+        int e = launch_back<EPI_GUPD>(g, v, s->sino, nullptr, ga, st);
+        tmark_end(s, st, 2, t1);
+        return e;
+    }
+    // multi-rank: partial back-projection, NCCL sum, then the unfused epilogue
+    int t1 = tmark(s, st);
+    if (int e = launch_back<EPI_STORE>(g, v, s->sino, s->Gtmp, ga, st)) return e;
+    tmark_end(s, st, 2, t1);
+    int t2 = tmark(s, st);
+    if (int e = allreduce(g, s->Gtmp, s->N, st)) return e;
+    if (epi == EPI_INIT) {
+        CT_CUDA(cudaMemcpyAsync(s->Gbuf[s->curG], s->Gtmp, s->N * 4, cudaMemcpyDeviceToDevice, st));
+        CT_CUDA(cudaMemcpyAsync(s->gs, s->Gtmp, s->N * 4, cudaMemcpyDeviceToDevice, st));
+        return CT_OK;
+    }
+    ga.G_old = s->Gbuf[s->curG];
+    ga.G_new = s->Gbuf[s->curG ^ 1];
+    gupd_kernel<<<nblk(s->N), 256, 0, st>>>(s->Gtmp, ga, s->N);
+    CT_LAUNCHED(1);
+    tmark_end(s, st, 4, t2);
+    return CT_OK;
+}
+
+static int nparts_for_gupd(const ct_oslalm_state* s) {
+    return (int)(s->g->nranks == 1 ? back_nblocks(s->g) : nblk(s->N));
+}
+
+// Enqueue one outer iteration (M inner steps) on stream st.  x is updated in place.
+static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float* x, cudaStream_t st, int* nk) {
+    const ct_geom* g = s->g;
+    const ct_oslalm_cfg& c = s->cfg;
+    int M = c.M;
+    float* xa = x;
+    float* xb = s->xalt;
+    float inv_d = (float)(1.0 / c.reg.delta);
+    int kernels = 0;
+    for (int j = 0; j < M; j++) {
+        int t0 = tmark(s, st);
+        if (c.reg.nbr == 8)
+            sqs_update_kernel<8><<<nblk(s->N), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
+                                                              &s->sc->rho, (float)c.reg.beta, inv_d, s->N);
+        else
+            sqs_update_kernel<26><<<nblk(s->N), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
+                                                               &s->sc->rho, (float)c.reg.beta, inv_d, s->N);
+        CT_LAUNCHED(1);
+        tmark_end(s, st, 0, t0);
+        std::swap(xa, xb);
+        if (int e = subset_gradient(s, d, xa, s->order[(j + 1) % M], EPI_GUPD, st)) return e;
+        s->curG ^= 1;
+        int t3 = tmark(s, st);
+        xi_finalize_kernel<<<1, 256, 0, st>>>(s->xi_part, nparts_for_gupd(s), s->sc, c.mode, c.rho_fixed, c.rho_min,
+                                              s->dlog, j);
+        CT_LAUNCHED(1);
+        tmark_end(s, st, 3, t3);
+        kernels += 4 + (g->nranks > 1 ? 1 : 0);
+    }
+    if (xa != x) {
+        CT_CUDA(cudaMemcpyAsync(x, xa, s->N * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    if (nk) *nk = kernels;
+    return CT_OK;
+}
+
+static int ensure_initialised(ct_oslalm_state* s, const ct_oslalm_data* d, float* x, cudaStream_t st) {
+    if (s->initialised) return CT_OK;
+    const ct_oslalm_cfg& c = s->cfg;
+    init_scalars_kernel<<<1, 1, 0, st>>>(s->sc, c.mode == CT_RHO_FIXED ? c.rho_fixed : 1.0);
+    CT_LAUNCHED(1);
+    zero_offmask_kernel<<<nblk(s->N), 256, 0, st>>>(x, d->mask, s->N);
+    CT_LAUNCHED(1);
+    if (int e = subset_gradient(s, d, x, s->order[0], EPI_INIT, st)) return e;
+    s->initialised = 1;
+    return CT_OK;
+}
+
+static int check_data(const ct_geom* g, const ct_oslalm_data* d, const float* x) {
+    if (!d || !d->y || !d->w || !d->dl || !d->mask || !x) return fail(CT_EINVAL, "ct_oslalm: null data pointer");
+    return CT_OK;
+}
+
+static bool cfg_equal(const ct_oslalm_cfg& a, const ct_oslalm_cfg& b) {
+    return a.M == b.M && a.mode == b.mode && a.rho_fixed == b.rho_fixed && a.rho_min == b.rho_min &&
+           a.n_inner == b.n_inner && a.reg.beta == b.reg.beta && a.reg.delta == b.reg.delta && a.reg.nbr == b.reg.nbr;
+}
+
+extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_data* d, ct_oslalm_state* s,
+                              float* x, void* stream) {
+    if (!g || !s) return fail(CT_EINVAL, "ct_oslalm_iter: null argument");
+    if (s->g != g) return fail(CT_ESTATE, "state was created for another geometry");
+    if (cfg && !cfg_equal(*cfg, s->cfg)) {
+        if (int e = check_cfg(g, cfg)) return e;
+        if (cfg->M != s->cfg.M) return fail(CT_ESTATE, "M changed after state creation");
+        s->cfg = *cfg;
+        for (auto& ge : s->graphs)
+            if (ge.exec) { cudaGraphExecDestroy(ge.exec); ge.exec = nullptr; }
+    }
+    if (int e = check_data(g, d, x)) return e;
+    DeviceGuard guard(g->d.device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int e = ensure_initialised(s, d, x, st)) return e;
+    if (g->nranks > 1 || s->timing) {
+        if (int e = enqueue_iteration(s, d, x, st, nullptr)) return e;
+        return tcollect(s);
+    }
+
+    // single rank: capture the iteration once per (buffers, G parity) and replay it
+    const void* key[6] = {x, d->y, d->w, d->dl, d->mask, s->gs};
+    GraphEntry* ge = nullptr;
+    for (auto& e : s->graphs)
+        if (e.exec && e.curG == s->curG && memcmp(e.key, key, sizeof(key)) == 0) ge = &e;
+    int startG = s->curG;
+    if (!ge) {
+        ge = s->graphs[0].exec == nullptr || s->graphs[0].curG == s->curG ? &s->graphs[0] : &s->graphs[1];
+        if (ge->exec) { cudaGraphExecDestroy(ge->exec); ge->exec = nullptr; }
+        cudaGraph_t graph;
+        CT_CUDA(cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal));
+        unsigned long long before = g_launches.load();
+        int nk = 0;
+        int err = enqueue_iteration(s, d, x, s->cap, &nk);
+        g_launches = before;  // capture does not execute kernels
+        cudaError_t ce = cudaStreamEndCapture(s->cap, &graph);
+        s->curG = startG;     // capture did not run; restore the parity
+        if (err) return err;
+        if (ce != cudaSuccess) return fail(CT_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+        ce = cudaGraphInstantiate(&ge->exec, graph, 0);
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return fail(CT_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+        memcpy(ge->key, key, sizeof(key));
+        ge->curG = startG;
+        ge->nodes = (size_t)nk;
+    }
+    CT_CUDA(cudaEventRecord(s->ev_in, st));
+    CT_CUDA(cudaStreamWaitEvent(s->cap, s->ev_in, 0));
+    CT_CUDA(cudaGraphLaunch(ge->exec, s->cap));
+    CT_CUDA(cudaEventRecord(s->ev_out, s->cap));
+    CT_CUDA(cudaStreamWaitEvent(st, s->ev_out, 0));
+    g_launches += ge->nodes;
+    if (s->cfg.M & 1) s->curG ^= 1;
+    return CT_OK;
+}
+
+extern "C" int ct_oslalm_run(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_data* d, ct_oslalm_state* s,
+                             float* x, int n_iter, ct_oslalm_log* log, void* stream) {
+    if (n_iter < 0) return fail(CT_EINVAL, "n_iter < 0");
+    if (log) log->count = 0;
+    DeviceGuard guard(g ? g->d.device : 0);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<double> h;
+    for (int it = 0; it < n_iter; it++) {
+        if (int e = ct_oslalm_iter(g, cfg, d, s, x, stream)) return e;
+        if (log) {
+            int M = s->cfg.M;
+            h.resize((size_t)M * 3);
+            CT_CUDA(cudaMemcpyAsync(h.data(), s->dlog, sizeof(double) * M * 3, cudaMemcpyDeviceToHost, st));
+            CT_CUDA(cudaStreamSynchronize(st));
+            for (int j = 0; j < M && log->count < log->capacity; j++, log->count++) {
+                if (log->rho) log->rho[log->count] = h[3 * j];
+                if (log->xi) log->xi[log->count] = h[3 * j + 1];
+                if (log->restart) log->restart[log->count] = (int)h[3 * j + 2];
+            }
+        }
+    }
+    CT_CUDA(cudaStreamSynchronize(st));
+    CT_CUDA(cudaGetLastError());
+    return CT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU
+// ---------------------------------------------------------------------------
+extern "C" int ct_comm_get_unique_id(void* uid) {
+    if (!uid) return fail(CT_EINVAL, "null uid");
+    if (!load_nccl()) return fail(CT_ENCCL, "libnccl.so.2 not loadable: %s", dlerror());
+    ncclUniqueId id;
+    ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(CT_ENCCL, "ncclGetUniqueId failed (%d)", (int)r);
+    memcpy(uid, &id, sizeof(id));
+    return CT_OK;
+}
+
+extern "C" int ct_comm_init(ct_geom* g, int rank, int nranks, const void* uid) {
+    if (!g || !uid) return fail(CT_EINVAL, "ct_comm_init: null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CT_EINVAL, "bad rank %d of %d", rank, nranks);
+    if (nranks == 1) {
+        g->rank = 0;
+        g->nranks = 1;
+        return CT_OK;
+    }
+    if (!load_nccl()) return fail(CT_ENCCL, "libnccl.so.2 not loadable");
+    DeviceGuard guard(g->d.device);
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    ncclComm_t comm;
+    ncclResult_t r = g_nccl.CommInitRank(&comm, nranks, id, rank);
+    if (r != ncclSuccess) return fail(CT_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error");
+    g->comm = comm;
+    g->rank = rank;
+    g->nranks = nranks;
+    return CT_OK;
+}

@@ -1,0 +1,180 @@
+// ct_common.cuh — device-side scan geometry and the ONE separable-footprint
+// routine shared by the forward and back projectors (so a_ij is identical in
+// A and A').  sm_100a, fp32.
+//
+// SF-TR footprint with A1 amplitude (reading O2 / G1 of DESIGN.md; "A is
+// the system matrix of a CT scan"):
+//   a_ij = l_phi * l_theta * F_s(c) * F_t(r)
+//   F_s(c): bin average of the trapezoid whose breakpoints are the arc positions
+//           of the voxel's four in-plane corners;
+//   F_t(r): overlap of the magnified voxel z-extent with detector row r / dt;
+//   l_phi = dx / max(|cos phi0|, |sin phi0|), l_theta = sqrt(1 + ((z - z_s)/rho_h)^2).
+//
+// Precision: the corner breakpoints are evaluated relative to
+// the voxel-centre ray (one atan2f per (view, column) plus a small-angle series
+// for the corner offsets), in channel units, so fp32 keeps ~1e-5 relative accuracy.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ct {
+
+constexpr int kMaxFoot = 8;   // channel window of a voxel footprint (validated at create)
+
+struct DevGeom {
+    int kind;                 // 0 fan2d, 1 cone axial, 2 cone helical
+    int nx, ny, nz, ns, nt, na;
+    float dx, dy, dz;
+    float x0, y0;             // centre of voxel (ix=0, iy=0)
+    float zb0;                // lower boundary of voxel iz = 0
+    float dso, dsd;
+    float dsd_ds;             // dsd / ds  (radians -> channel units)
+    float cbase;              // channel coordinate of fan angle 0: (ns-1)/2 + offs
+    float rbase;              // row coordinate of t = 0: (nt-1)/2 + offt
+    float dt;
+    const float4* views;      // per view: (sin beta, cos beta, qi, qf) with
+                              // (z_s - zb0)/dz = qi + qf, qi integer (exact in fp32)
+};
+
+// Transaxial footprint of one voxel column for one view (channel units).
+struct Trans {
+    float cc;       // channel coordinate of the voxel-centre ray
+    float t0, t1, t2, t3;   // sorted breakpoints relative to cc (channel units)
+    float lphi;     // A1 in-plane amplitude (mm)
+    float rho;      // in-plane source-to-centre distance (mm)
+};
+
+__device__ __forceinline__ void sort2(float& a, float& b) {
+    float lo = fminf(a, b), hi = fmaxf(a, b);
+    a = lo;
+    b = hi;
+}
+
+__device__ __forceinline__ float small_atan(float u) {
+    // atan(u) = u - u^3/3 + u^5/5 - ...; |u| = corner half-diagonal / rho_h
+    // (< 2e-2 for every validated geometry) -> truncation u^7/7 < 2e-13
+    float u2 = u * u;
+    return u * (1.0f - u2 * (1.0f / 3.0f - u2 * 0.2f));
+}
+
+__device__ __forceinline__ void transaxial(const DevGeom& g, float sb, float cb, float xc, float yc, Trans& tr) {
+    float along = g.dso + xc * sb - yc * cb;     // (p - S) . e_c
+    float perp = xc * cb + yc * sb;              // (p - S) . e_perp
+    float rho2 = along * along + perp * perp;
+    float rho = sqrtf(rho2);
+    tr.rho = rho;
+    tr.cc = atan2f(perp, along) * g.dsd_ds + g.cbase;
+    // corner offsets (+-hx, +-hy): d_along = sx*ax + sy*ay, d_perp = sx*px + sy*py
+    float hx = 0.5f * g.dx, hy = 0.5f * g.dy;
+    float ax = hx * sb, ay = -hy * cb, px = hx * cb, py = hy * sb;
+    float t[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        float sx = (k & 1) ? 1.0f : -1.0f, sy = (k & 2) ? 1.0f : -1.0f;
+        float da = sx * ax + sy * ay, dp = sx * px + sy * py;
+        float cross = along * dp - perp * da;
+        float dot = rho2 + along * da + perp * dp;
+        t[k] = small_atan(__fdividef(cross, dot)) * g.dsd_ds;
+    }
+    // 5-comparator sorting network
+    sort2(t[0], t[1]);
+    sort2(t[2], t[3]);
+    sort2(t[0], t[2]);
+    sort2(t[1], t[3]);
+    sort2(t[1], t[2]);
+    tr.t0 = t[0]; tr.t1 = t[1]; tr.t2 = t[2]; tr.t3 = t[3];
+    float dirx = fabsf(xc + g.dso * sb), diry = fabsf(yc - g.dso * cb);
+    tr.lphi = g.dx * rho / fmaxf(dirx, diry);
+}
+
+// Antiderivative of the unit trapezoid (branch-free, degenerate widths safe).
+struct TrapCdf {
+    float t0, t1, t2, h0, h3;
+    __device__ __forceinline__ TrapCdf(const Trans& tr) {
+        t0 = tr.t0; t1 = tr.t1; t2 = tr.t2;
+        h0 = 0.5f / fmaxf(tr.t1 - tr.t0, 1e-20f);
+        h3 = 0.5f / fmaxf(tr.t3 - tr.t2, 1e-20f);
+        t3 = tr.t3;
+    }
+    float t3;
+    __device__ __forceinline__ float operator()(float s) const {
+        float a = fminf(fmaxf(s, t0), t1) - t0;
+        float f = fminf(fmaxf(s, t1), t2) - t1;
+        float b = fminf(fmaxf(s, t2), t3) - t2;
+        return a * a * h0 + f + b - b * b * h3;
+    }
+};
+
+// First channel of the footprint and number of channels (clamped to the detector).
+__device__ __forceinline__ void foot_range(const DevGeom& g, const Trans& tr, int& cA, int& n) {
+    int a = __float2int_rd(tr.cc + tr.t0 + 0.5f);
+    int b = __float2int_rd(tr.cc + tr.t3 + 0.5f);
+    a = max(a, 0);
+    b = min(b, g.ns - 1);
+    cA = a;
+    n = b - a + 1;   // may be <= 0 (footprint off the detector)
+}
+
+// Weight of channel c: lphi * F_s(c) (bin edges c -+ 0.5 relative to cc).
+__device__ __forceinline__ float chan_weight(const TrapCdf& F, float cc, float lphi, int c) {
+    float e0 = (float)c - 0.5f - cc;
+    return lphi * (F(e0 + 1.0f) - F(e0));
+}
+
+// Axial parameters of a column for one view, in voxel-index units q relative to
+// the integer qi of the source height (keeps fp32 precision on long helices):
+//   q(r) = qf + (r - rbase) * kz is the voxel coordinate (minus qi) of row r's
+//   centre; row r spans [q(r) - kz/2, q(r) + kz/2]; F_t = overlap_q / kz.
+struct Axial {
+    int qi;        // integer part of (z_s - zb0)/dz
+    float qf;      // fractional remainder
+    float kz;      // dt / (mag * dz),  mag = dsd / rho
+    float inv_kz;
+    float dz_rho;  // dz / rho  (for l_theta)
+};
+
+__device__ __forceinline__ void axial(const DevGeom& g, float4 view, float rho, Axial& ax) {
+    ax.qi = (int)view.z;
+    ax.qf = view.w;
+    ax.kz = g.dt * rho / (g.dsd * g.dz);
+    ax.inv_kz = 1.0f / ax.kz;
+    ax.dz_rho = g.dz / rho;
+}
+
+__device__ __forceinline__ float ltheta(const Axial& ax, int iz) {
+    float tz = ((float)(iz - ax.qi) + 0.5f - ax.qf) * ax.dz_rho;
+    return sqrtf(1.0f + tz * tz);
+}
+
+__device__ __forceinline__ float row_center_q(const Axial& ax, const DevGeom& g, int r) {
+    return ax.qf + ((float)r - g.rbase) * ax.kz;
+}
+
+// F_t(iz, r): overlap of voxel [iz, iz+1] with row r's q-interval, / kz.
+__device__ __forceinline__ float axial_weight(const Axial& ax, float qr, int iz) {
+    float lo = qr - 0.5f * ax.kz, hi = qr + 0.5f * ax.kz;
+    float zi = (float)(iz - ax.qi);
+    float ov = fminf(zi + 1.0f, hi) - fmaxf(zi, lo);
+    return fmaxf(ov, 0.0f) * ax.inv_kz;
+}
+
+// Voxel range [iz0, iz1] overlapping row r (unclamped).
+__device__ __forceinline__ void row_voxels(const Axial& ax, float qr, int& iz0, int& iz1) {
+    iz0 = __float2int_rd(qr - 0.5f * ax.kz) + ax.qi;
+    iz1 = __float2int_rd(qr + 0.5f * ax.kz) + ax.qi;
+}
+
+// Row range [r0, r1] overlapping voxel iz (unclamped).
+__device__ __forceinline__ void voxel_rows(const Axial& ax, const DevGeom& g, int iz, int& r0, int& r1) {
+    float zi = (float)(iz - ax.qi);
+    r0 = __float2int_rd((zi - ax.qf) * ax.inv_kz + g.rbase - 0.5f);
+    r1 = __float2int_rd((zi + 1.0f - ax.qf) * ax.inv_kz + g.rbase + 0.5f);
+}
+
+// Fair potential pieces (reading G3/G14)
+__device__ __forceinline__ void fair(float t, float inv_delta, float& dpsi, float& omega) {
+    omega = __frcp_rn(1.0f + fabsf(t) * inv_delta);
+    dpsi = t * omega;
+}
+
+}  // namespace ct

@@ -1,0 +1,721 @@
+// ct_kernels.cuh — sm_100a kernels of the OS-LALM hot path.
+//
+//   K1  fwd2d / fwd3d   : y_k = A_v x (+ fused weighted residual r = s W (A x - y))
+//   K2  back2d / back3d : x = A_v' y  (+ fused g-update / restart-indicator epilogue) P:391-395
+//   K3  sqs_update      : rho-scaled non-negative SQS step with the Fair stencil
+//   K4  xi_finalize     : fixed-order fp64 sum of xi, counter l and rho_l update
+//   K5  (setup)         : D_L = A'(W A 1_S) from K1/K2 + mask finalisation
+//   K6  reg_grad        : standalone Fair gradient / Huber curvature
+//
+// Every projection is a gather: no global or shared float atomics, so results are
+// deterministic run to run.  See DESIGN.md §Kernels for the tiling and rooflines.
+#pragma once
+#include "ct_common.cuh"
+
+namespace ct {
+
+// ---------------------------------------------------------------------------
+// Sweep-line wedge of a channel tile (shared by fwd2d / fwd3d)
+// ---------------------------------------------------------------------------
+// For one view and a tile of channels [c0, c0 + TC), the voxel columns whose
+// footprint can reach the tile lie, on each image row (or column), inside the
+// interval cut by the tile's two edge rays, widened by the footprint half-width.
+struct Wedge {
+    bool rows;        // true: lines are image rows (iy fixed, ix varies)
+    int nlines;       // ny or nx
+    float Sx, Sy;     // source position
+    float ka, kb;     // slopes (dx/dy for row lines, dy/dx for column lines) of the edge rays
+    float margin;     // in pixels
+    bool increasing;  // channel coordinate increases with the in-line index
+};
+
+__device__ __forceinline__ void ray_dir(float sb, float cb, float gam, float& dx, float& dy) {
+    float cg = __cosf(gam), sg = __sinf(gam);   // |gam| < pi/2; only bounds the wedge
+    // d = cos(g) e_c + sin(g) e_perp, e_c = (sb, -cb), e_perp = (cb, sb)
+    dx = cg * sb + sg * cb;
+    dy = -cg * cb + sg * sb;
+}
+
+__device__ __forceinline__ Wedge make_wedge(const DevGeom& g, float sb, float cb, int c0, int tc) {
+    Wedge w;
+    w.Sx = -g.dso * sb;
+    w.Sy = g.dso * cb;
+    float ga = ((float)c0 - 0.5f - g.cbase) / g.dsd_ds;
+    float gb = ((float)(c0 + tc) - 0.5f - g.cbase) / g.dsd_ds;
+    float ax, ay, bx, by, mx, my;
+    ray_dir(sb, cb, ga, ax, ay);
+    ray_dir(sb, cb, gb, bx, by);
+    ray_dir(sb, cb, 0.5f * (ga + gb), mx, my);
+    w.rows = fabsf(my) >= fabsf(mx);
+    if (w.rows) {
+        w.nlines = g.ny;
+        w.ka = ax / ay;
+        w.kb = bx / by;
+        // channel (fan angle) increases with x iff d gamma/dx = -dir.y/rho^2 > 0
+        w.increasing = my < 0.0f;
+    } else {
+        w.nlines = g.nx;
+        w.ka = ay / ax;
+        w.kb = by / bx;
+        // d gamma/dy = dir.x / rho^2
+        w.increasing = mx > 0.0f;
+    }
+    w.margin = 1.0f + 0.5f * fmaxf(fabsf(w.ka), fabsf(w.kb));
+    return w;
+}
+
+// In-line index range [lo, hi] of line L (clamped); empty if lo > hi.
+__device__ __forceinline__ void wedge_line(const DevGeom& g, const Wedge& w, int L, int& lo, int& hi) {
+    float a, b;
+    if (w.rows) {
+        float y = g.y0 + L * g.dy;
+        a = w.Sx + (y - w.Sy) * w.ka;
+        b = w.Sx + (y - w.Sy) * w.kb;
+        float u0 = (fminf(a, b) - g.x0) / g.dx - w.margin, u1 = (fmaxf(a, b) - g.x0) / g.dx + w.margin;
+        lo = max(0, __float2int_ru(u0));
+        hi = min(g.nx - 1, __float2int_rd(u1));
+    } else {
+        float x = g.x0 + L * g.dx;
+        a = w.Sy + (x - w.Sx) * w.ka;
+        b = w.Sy + (x - w.Sx) * w.kb;
+        float u0 = (fminf(a, b) - g.y0) / g.dy - w.margin, u1 = (fmaxf(a, b) - g.y0) / g.dy + w.margin;
+        lo = max(0, __float2int_ru(u0));
+        hi = min(g.ny - 1, __float2int_rd(u1));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Register sliding window of kMaxFoot channel accumulators.
+// Contributions arrive in non-decreasing first-channel order along a line.
+// ---------------------------------------------------------------------------
+struct Window {
+    float acc[kMaxFoot];
+    int base;
+    __device__ __forceinline__ void reset(int b) {
+        base = b;
+#pragma unroll
+        for (int k = 0; k < kMaxFoot; k++) acc[k] = 0.0f;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// K1 (2D fan): forward projection of one (view, channel tile)
+// ---------------------------------------------------------------------------
+// CTA = (tile of TC channels, view k).  Each thread owns whole sweep lines of
+// the tile's wedge, walks their pixels in channel order, computes each pixel's
+// footprint once and accumulates into a register window; window flushes go to
+// the thread's private smem column, which a fixed-order reduction sums.
+template <int TC, int NTHR, bool RESID>
+__global__ void __launch_bounds__(NTHR) fwd2d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
+                                                     float* __restrict__ out, const float* __restrict__ yobs,
+                                                     const float* __restrict__ wts, float scale) {
+    __shared__ float P[TC][NTHR + 1];
+    const int c0 = blockIdx.x * TC;
+    const int k = blockIdx.y;
+    const int v = first + k * stride;
+    const float4 vw = g.views[v];
+    const float sb = vw.x, cb = vw.y;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int c = 0; c < TC; c++) P[c][tid] = 0.0f;
+    Wedge w = make_wedge(g, sb, cb, c0, TC);
+    for (int L = tid; L < w.nlines; L += NTHR) {
+        int lo, hi;
+        wedge_line(g, w, L, lo, hi);
+        if (lo > hi) continue;
+        Window win;
+        win.reset(-1000000);
+        int n_in = hi - lo + 1;
+        for (int q = 0; q < n_in; q++) {
+            int u = w.increasing ? lo + q : hi - q;
+            int ix = w.rows ? u : L, iy = w.rows ? L : u;
+            float xv = __ldg(&x[iy * g.nx + ix]);
+            if (xv == 0.0f) continue;
+            Trans tr;
+            transaxial(g, sb, cb, g.x0 + ix * g.dx, g.y0 + iy * g.dy, tr);
+            int cA, n;
+            foot_range(g, tr, cA, n);
+            if (n <= 0 || cA + n <= c0 || cA >= c0 + TC) continue;
+            TrapCdf F(tr);
+            float lx = tr.lphi * xv;
+            if (cA >= win.base) {
+                // shift the window so that base == cA, flushing channels that are done
+                while (win.base < cA) {
+                    int cc = win.base - c0;
+                    if (cc >= 0 && cc < TC) P[cc][tid] += win.acc[0];
+#pragma unroll
+                    for (int j = 0; j < kMaxFoot - 1; j++) win.acc[j] = win.acc[j + 1];
+                    win.acc[kMaxFoot - 1] = 0.0f;
+                    win.base++;
+                    if (win.base < cA - kMaxFoot) {  // jump: everything left is zero
+                        int jmp = cA - win.base;
+#pragma unroll
+                        for (int j = 0; j < kMaxFoot; j++) {
+                            int c1 = win.base + j - c0;
+                            if (c1 >= 0 && c1 < TC && win.acc[j] != 0.0f) P[c1][tid] += win.acc[j];
+                        }
+                        win.reset(win.base + jmp);
+                    }
+                }
+                float e = (float)cA - 0.5f - tr.cc;
+                float Fp = F(e);
+#pragma unroll
+                for (int j = 0; j < kMaxFoot; j++) {
+                    if (j < n) {
+                        float Fn = F(e + (float)(j + 1));
+                        win.acc[j] += lx * (Fn - Fp);
+                        Fp = Fn;
+                    }
+                }
+            } else {
+                // out-of-order footprint (rounding at a line end): direct smem adds
+                for (int j = 0; j < n; j++) {
+                    int c = cA + j - c0;
+                    if (c >= 0 && c < TC) P[c][tid] += xv * chan_weight(F, tr.cc, tr.lphi, cA + j);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxFoot; j++) {
+            int c = win.base + j - c0;
+            if (c >= 0 && c < TC) P[c][tid] += win.acc[j];
+        }
+    }
+    __syncthreads();
+    // fixed-order reduction over threads: NTHR/TC threads per channel
+    constexpr int PER = NTHR / TC;
+    int c = tid / PER, part = tid % PER;
+    float s = 0.0f;
+    for (int t = part; t < NTHR; t += PER) s += P[c][t];
+#pragma unroll
+    for (int o = PER / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, PER);
+    if (part == 0 && c0 + c < g.ns) {
+        size_t oi = (size_t)k * g.ns + c0 + c;
+        if (RESID) {
+            size_t gi = (size_t)v * g.ns + c0 + c;
+            float yo = yobs ? __ldg(&yobs[gi]) : 0.0f;
+            out[oi] = scale * __ldg(&wts[gi]) * (s - yo);
+        } else {
+            out[oi] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1 (3D cone): forward projection of one (view, channel tile, all rows)
+// ---------------------------------------------------------------------------
+// CTA = (tile of TC channels, view k); NTHR threads = G groups of NTP row-threads.
+// Group gi walks sweep lines gi, gi+G, ...; for each wedge column all threads of
+// the group (one per detector row r) compute the column's axial sum
+//   A(r) = sum_iz x[iz] l_theta(iz) F_t(iz, r)      (z-fastest layout: coalesced)
+// and add lphi F_s(c) A(r) to a register window over the column's channels.
+template <int TC, int NTP, int NTHR, bool RESID>
+__global__ void __launch_bounds__(NTHR) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
+                                                     float* __restrict__ out, const float* __restrict__ yobs,
+                                                     const float* __restrict__ wts, float scale) {
+    constexpr int G = NTHR / NTP;
+    __shared__ float P[G][TC][NTP + 1];
+    const int c0 = blockIdx.x * TC;
+    const int k = blockIdx.y;
+    const int v = first + k * stride;
+    const float4 vw = g.views[v];
+    const float sb = vw.x, cb = vw.y;
+    const int gi = threadIdx.x / NTP, r = threadIdx.x % NTP;
+    const bool row_ok = r < g.nt;
+#pragma unroll
+    for (int c = 0; c < TC; c++) P[gi][c][r] = 0.0f;
+    Wedge w = make_wedge(g, sb, cb, c0, TC);
+    const int nz = g.nz;
+    for (int L = gi; L < w.nlines; L += G) {
+        int lo, hi;
+        wedge_line(g, w, L, lo, hi);
+        if (lo > hi) continue;
+        Window win;
+        win.reset(-1000000);
+        int n_in = hi - lo + 1;
+        for (int q = 0; q < n_in; q++) {
+            int u = w.increasing ? lo + q : hi - q;
+            int ix = w.rows ? u : L, iy = w.rows ? L : u;
+            Trans tr;
+            transaxial(g, sb, cb, g.x0 + ix * g.dx, g.y0 + iy * g.dy, tr);
+            int cA, n;
+            foot_range(g, tr, cA, n);
+            if (n <= 0 || cA + n <= c0 || cA >= c0 + TC) continue;
+            Axial ax;
+            axial(g, vw, tr.rho, ax);
+            // axial sum for this thread's row
+            float A = 0.0f;
+            if (row_ok) {
+                float qr = row_center_q(ax, g, r);
+                int iz0, iz1;
+                row_voxels(ax, qr, iz0, iz1);
+                iz0 = max(iz0, 0);
+                iz1 = min(iz1, nz - 1);
+                const float* xc = x + ((size_t)iy * g.nx + ix) * nz;
+                for (int iz = iz0; iz <= iz1; iz++) {
+                    float ft = axial_weight(ax, qr, iz);
+                    A += __ldg(&xc[iz]) * ltheta(ax, iz) * ft;
+                }
+            }
+            TrapCdf F(tr);
+            if (cA >= win.base) {
+                while (win.base < cA) {
+                    int cc = win.base - c0;
+                    if (cc >= 0 && cc < TC) P[gi][cc][r] += win.acc[0];
+#pragma unroll
+                    for (int j = 0; j < kMaxFoot - 1; j++) win.acc[j] = win.acc[j + 1];
+                    win.acc[kMaxFoot - 1] = 0.0f;
+                    win.base++;
+                    if (win.base < cA - kMaxFoot) {
+                        int jmp = cA - win.base;
+#pragma unroll
+                        for (int j = 0; j < kMaxFoot; j++) {
+                            int c1 = win.base + j - c0;
+                            if (c1 >= 0 && c1 < TC) P[gi][c1][r] += win.acc[j];
+                        }
+                        win.reset(win.base + jmp);
+                    }
+                }
+                float lA = tr.lphi * A;
+                float e = (float)cA - 0.5f - tr.cc;
+                float Fp = F(e);
+#pragma unroll
+                for (int j = 0; j < kMaxFoot; j++) {
+                    if (j < n) {
+                        float Fn = F(e + (float)(j + 1));
+                        win.acc[j] += lA * (Fn - Fp);
+                        Fp = Fn;
+                    }
+                }
+            } else {
+                for (int j = 0; j < n; j++) {
+                    int c = cA + j - c0;
+                    if (c >= 0 && c < TC) P[gi][c][r] += A * chan_weight(F, tr.cc, tr.lphi, cA + j);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxFoot; j++) {
+            int c = win.base + j - c0;
+            if (c >= 0 && c < TC) P[gi][c][r] += win.acc[j];
+        }
+    }
+    __syncthreads();
+    // fixed-order sum over groups; thread (c, r) pairs cover the tile, r fastest
+    for (int idx = threadIdx.x; idx < TC * NTP; idx += NTHR) {
+        int c = idx / NTP, rr = idx % NTP;
+        if (rr >= g.nt || c0 + c >= g.ns) continue;
+        float s = 0.0f;
+#pragma unroll
+        for (int q = 0; q < G; q++) s += P[q][c][rr];
+        size_t oi = ((size_t)k * g.ns + c0 + c) * g.nt + rr;
+        if (RESID) {
+            size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
+            float yo = yobs ? __ldg(&yobs[gidx]) : 0.0f;
+            out[oi] = scale * __ldg(&wts[gidx]) * (s - yo);
+        } else {
+            out[oi] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Back-projection epilogues
+// ---------------------------------------------------------------------------
+enum BackEpi { EPI_STORE = 0, EPI_ACCUM = 1, EPI_GUPD = 2, EPI_INIT = 3 };
+
+struct GupdArgs {
+    float* G_new;          // G+  (EPI_GUPD) / G (EPI_INIT)
+    const float* G_old;    // G   (EPI_GUPD)
+    float* gs;             // split gradient g, updated in place
+    const uint8_t* mask;   // support S
+    const double* rho;     // rho of this inner step (device scalar)
+    double* xi_part;       // per-block fp64 partials of xi
+};
+
+template <int NTHR>
+__device__ __forceinline__ void block_sum_store(double val, double* dst) {
+    __shared__ double red[NTHR / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) val += __shfl_down_sync(0xffffffffu, val, o);
+    int lane = threadIdx.x % 32, wid = threadIdx.x / 32;
+    if (lane == 0) red[wid] = val;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < NTHR / 32; i++) s += red[i];
+        *dst = s;
+    }
+}
+
+template <int EPI>
+__device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc, float* x, const GupdArgs& ga) {
+    if (!valid) return 0.0;
+    if (EPI == EPI_STORE) {
+        x[j] = acc;
+    } else if (EPI == EPI_ACCUM) {
+        x[j] += acc;
+    } else if (EPI == EPI_INIT) {
+        ga.G_new[j] = acc;
+        ga.gs[j] = acc;
+    } else {
+        float rho = (float)*ga.rho;
+        float Gp = acc, G = ga.G_old[j], gg = ga.gs[j];
+        ga.G_new[j] = Gp;
+        ga.gs[j] = (rho * Gp + gg) / (1.0f + rho);
+        if (ga.mask[j]) return (double)(gg - Gp) * (double)(Gp - G);
+    }
+    return 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// K2 (2D fan): voxel-driven back projection, one thread per pixel
+// ---------------------------------------------------------------------------
+template <int EPI>
+__global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int stride, int count,
+                                                    const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
+    const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int iy = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const bool valid = ix < g.nx && iy < g.ny;
+    float acc = 0.0f;
+    if (valid) {
+        const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
+        for (int k = 0; k < count; k++) {
+            const float4 vw = g.views[first + k * stride];
+            Trans tr;
+            transaxial(g, vw.x, vw.y, xc, yc, tr);
+            int cA, n;
+            foot_range(g, tr, cA, n);
+            if (n <= 0) continue;
+            TrapCdf F(tr);
+            const float* yk = y + (size_t)k * g.ns;
+            float e = (float)cA - 0.5f - tr.cc;
+            float Fp = F(e), s = 0.0f;
+#pragma unroll
+            for (int j = 0; j < kMaxFoot; j++) {
+                if (j < n) {
+                    float Fn = F(e + (float)(j + 1));
+                    s += (Fn - Fp) * __ldg(&yk[cA + j]);
+                    Fp = Fn;
+                }
+            }
+            acc += tr.lphi * s;
+        }
+    }
+    size_t j = (size_t)iy * g.nx + ix;
+    double xi = back_epilogue<EPI>(j, valid, acc, x, ga);
+    if (EPI == EPI_GUPD) block_sum_store<256>(xi, &ga.xi_part[blockIdx.y * gridDim.x + blockIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// K2 (3D cone): voxel-driven back projection; warp = one column x 32 slices
+// ---------------------------------------------------------------------------
+// The column's transaxial footprint is warp-uniform (computed once per view per
+// warp); lanes walk z, so sinogram reads y[k][c][r..] are unit-stride in r.
+template <int EPI>
+__global__ void __launch_bounds__(256) back3d_kernel(DevGeom g, int first, int stride, int count,
+                                                    const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int ix = blockIdx.x * 8 + wid;
+    const int iy = blockIdx.y;
+    const int iz = blockIdx.z * 32 + lane;
+    const bool colok = ix < g.nx;
+    const bool valid = colok && iz < g.nz;
+    const int nt = g.nt, ns = g.ns;
+    float acc = 0.0f;
+    if (colok) {
+        const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
+        const int zlo = blockIdx.z * 32, zhi = min(g.nz, zlo + 32) - 1;
+        for (int k = 0; k < count; k++) {
+            const float4 vw = g.views[first + k * stride];
+            Trans tr;
+            transaxial(g, vw.x, vw.y, xc, yc, tr);
+            Axial ax;
+            axial(g, vw, tr.rho, ax);
+            // warp-uniform skip when the chunk's rows miss the detector (helical)
+            int ra, rb, rc, rd;
+            voxel_rows(ax, g, zlo, ra, rb);
+            voxel_rows(ax, g, zhi, rc, rd);
+            if (rd < 0 || ra >= nt) continue;
+            int cA, n;
+            foot_range(g, tr, cA, n);
+            if (n <= 0) continue;
+            TrapCdf F(tr);
+            float wc[kMaxFoot];
+            {
+                float e = (float)cA - 0.5f - tr.cc;
+                float Fp = F(e);
+#pragma unroll
+                for (int j = 0; j < kMaxFoot; j++) {
+                    float Fn = F(e + (float)(j + 1));
+                    wc[j] = (j < n) ? tr.lphi * (Fn - Fp) : 0.0f;
+                    Fp = Fn;
+                }
+            }
+            if (!valid) continue;
+            int r0, r1;
+            voxel_rows(ax, g, iz, r0, r1);
+            r0 = max(r0, 0);
+            r1 = min(r1, nt - 1);
+            if (r0 > r1) continue;
+            const float* yk = y + ((size_t)k * ns + cA) * nt;
+            float s = 0.0f;
+            for (int r = r0; r <= r1; r++) {
+                float ft = axial_weight(ax, row_center_q(ax, g, r), iz);
+                float t = 0.0f;
+#pragma unroll
+                for (int j = 0; j < kMaxFoot; j++)
+                    if (j < n) t += wc[j] * __ldg(&yk[(size_t)j * nt + r]);
+                s += ft * t;
+            }
+            acc += ltheta(ax, iz) * s;
+        }
+    }
+    size_t j = ((size_t)iy * g.nx + (colok ? ix : 0)) * g.nz + iz;
+    double xi = back_epilogue<EPI>(j, valid, acc, x, ga);
+    if (EPI == EPI_GUPD)
+        block_sum_store<256>(xi, &ga.xi_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// K3: rho-scaled non-negative SQS update with the Fair stencil (one FISTA step)
+// ---------------------------------------------------------------------------
+// x_new = max(0, x - (rho G + (1-rho) g + grad R(x)) / (rho D_L + D_R(x)))  on S, 0 off S.
+// With `grad` != nullptr (K6 standalone) it writes grad R and D_R instead.
+template <int NBR>
+__device__ __forceinline__ void fair_stencil(const DevGeom& g, const float* __restrict__ x, const uint8_t* __restrict__ m,
+                                             int iy, int ix, int iz, float xj, float inv_delta, float& gr, float& cu) {
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    gr = 0.0f;
+    cu = 0.0f;
+#pragma unroll
+    for (int oy = -1; oy <= 1; oy++)
+#pragma unroll
+        for (int ox = -1; ox <= 1; ox++)
+#pragma unroll
+            for (int oz = (NBR == 26 ? -1 : 0); oz <= (NBR == 26 ? 1 : 0); oz++) {
+                if (oy == 0 && ox == 0 && oz == 0) continue;
+                int ky = iy + oy, kx = ix + ox, kz = iz + oz;
+                if (ky < 0 || ky >= ny || kx < 0 || kx >= nx || kz < 0 || kz >= nz) continue;
+                size_t kk = ((size_t)ky * nx + kx) * nz + kz;
+                if (!__ldg(&m[kk])) continue;
+                constexpr float r2 = 0.70710678118654752f, r3 = 0.57735026918962576f;
+                const int d2 = oy * oy + ox * ox + oz * oz;
+                const float wgt = d2 == 1 ? 1.0f : (d2 == 2 ? r2 : r3);
+                float dpsi, om;
+                fair(xj - __ldg(&x[kk]), inv_delta, dpsi, om);
+                gr += wgt * dpsi;
+                cu += wgt * om;
+            }
+}
+
+template <int NBR>
+__global__ void __launch_bounds__(256) sqs_update_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
+                                                        const float* __restrict__ G, const float* __restrict__ gs,
+                                                        const float* __restrict__ dl, const uint8_t* __restrict__ m,
+                                                        const double* __restrict__ rho_p, float beta, float inv_delta,
+                                                        size_t N) {
+    size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    if (!m[j]) {
+        xn[j] = 0.0f;
+        return;
+    }
+    const int nz = g.nz;
+    int iz = (int)(j % nz);
+    size_t c = j / nz;
+    int ix = (int)(c % g.nx), iy = (int)(c / g.nx);
+    float xj = x[j];
+    float gr, cu;
+    fair_stencil<NBR>(g, x, m, iy, ix, iz, xj, inv_delta, gr, cu);
+    float rho = (float)*rho_p;
+    float s = rho * G[j] + (1.0f - rho) * gs[j];
+    float den = rho * dl[j] + 2.0f * beta * cu;
+    float v = xj - (s + beta * gr) / den;
+    xn[j] = fmaxf(v, 0.0f);
+}
+
+template <int NBR>
+__global__ void __launch_bounds__(256) reg_grad_kernel(DevGeom g, const float* __restrict__ x, const uint8_t* __restrict__ m,
+                                                      float* __restrict__ grad, float* __restrict__ curv, float beta,
+                                                      float inv_delta, size_t N) {
+    size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    float gr = 0.0f, cu = 0.0f;
+    if (m[j]) {
+        const int nz = g.nz;
+        int iz = (int)(j % nz);
+        size_t c = j / nz;
+        int ix = (int)(c % g.nx), iy = (int)(c / g.nx);
+        fair_stencil<NBR>(g, x, m, iy, ix, iz, x[j], inv_delta, gr, cu);
+    }
+    grad[j] = beta * gr;
+    if (curv) curv[j] = 2.0f * beta * cu;
+}
+
+// ---------------------------------------------------------------------------
+// Unfused g-update (multi-rank path, after the NCCL all-reduce of G+)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gupd_kernel(const float* __restrict__ Gp, GupdArgs ga, size_t N) {
+    size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double xi = 0.0;
+    if (j < N) {
+        float rho = (float)*ga.rho;
+        float P = Gp[j], G = ga.G_old[j], gg = ga.gs[j];
+        ga.G_new[j] = P;
+        ga.gs[j] = (rho * P + gg) / (1.0f + rho);
+        if (ga.mask[j]) xi = (double)(gg - P) * (double)(P - G);
+    }
+    block_sum_store<256>(xi, &ga.xi_part[blockIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// K4: xi = fixed-order fp64 sum of block partials; restart rule; rho_l
+// ---------------------------------------------------------------------------
+struct Scalars {
+    double rho;        // rho for the next inner step
+    long long l;       // continuation counter
+    long long step;    // inner steps taken
+};
+
+__device__ __forceinline__ double rho_l(long long l, double rho_min) {
+    // rho_0 = 1; rho_l = max{ pi/(l+1) sqrt(1 - (pi/(2l+2))^2), rho_min }
+    if (l == 0) return 1.0;
+    const double pi = 3.14159265358979323846;
+    double a = pi / (double)(l + 1), b = pi / (2.0 * (double)l + 2.0);
+    double r = a * sqrt(1.0 - b * b);
+    return r > rho_min ? r : rho_min;
+}
+
+__global__ void __launch_bounds__(256) xi_finalize_kernel(const double* __restrict__ part, int nparts, Scalars* sc,
+                                                         int mode, double rho_fixed, double rho_min,
+                                                         double* __restrict__ log3, int log_slot) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += 256) s += part[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double xi = red[0];
+        int restart = xi > 0.0;
+        double rho_used = sc->rho;
+        if (mode == 1) {
+            sc->l = restart ? 0 : sc->l + 1;
+            sc->rho = rho_l(sc->l, rho_min);
+        } else {
+            sc->rho = rho_fixed;
+        }
+        sc->step += 1;
+        if (log3 && log_slot >= 0) {
+            log3[3 * log_slot + 0] = rho_used;
+            log3[3 * log_slot + 1] = xi;
+            log3[3 * log_slot + 2] = restart;
+        }
+    }
+}
+
+__global__ void init_scalars_kernel(Scalars* sc, double rho0) {
+    sc->rho = rho0;
+    sc->l = 0;
+    sc->step = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Setup helpers
+// ---------------------------------------------------------------------------
+__global__ void mask_to_float_kernel(const uint8_t* __restrict__ m, float* __restrict__ f, size_t N) {
+    size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < N) f[j] = m[j] ? 1.0f : 0.0f;
+}
+
+__global__ void mask_finalize_kernel(uint8_t* __restrict__ m, float* __restrict__ dl, size_t N) {
+    size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < N) {
+        bool in = m[j] && dl[j] > 0.0f;
+        m[j] = in ? 1 : 0;
+        if (!in) dl[j] = 0.0f;
+    }
+}
+
+__global__ void zero_offmask_kernel(float* __restrict__ x, const uint8_t* __restrict__ m, size_t N) {
+    size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < N && !m[j]) x[j] = 0.0f;
+}
+
+// U count (fp64 geometry): thread per (view, column), loop over z.
+struct DevGeomD {
+    int kind, nx, ny, nz, ns, nt;
+    double dx, dy, dz, x0, y0, z0, dso, dsd, ds, dt, offs, offt;
+    double s_lo, s_hi, t_lo, t_hi;
+    const double2* vz;  // per view: (beta, z_s)
+};
+
+__global__ void __launch_bounds__(256) count_vv_kernel(DevGeomD g, int first, int stride, int count,
+                                                      const uint8_t* __restrict__ m,
+                                                      unsigned long long* __restrict__ total) {
+    size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    size_t ncol = (size_t)g.nx * g.ny;
+    unsigned long long cu = 0, cn = 0, cc = 0;
+    if (idx < ncol * (size_t)count) {
+        int k = (int)(idx / ncol);
+        size_t col = idx % ncol;
+        int ix = (int)(col % g.nx), iy = (int)(col / g.nx);
+        double2 vz = g.vz[first + k * stride];
+        double sb = sin(vz.x), cb = cos(vz.x);
+        double xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
+        double tmin = 1e300, tmax = -1e300;
+        for (int q = 0; q < 4; q++) {
+            double px = xc + ((q & 1) ? 0.5 : -0.5) * g.dx, py = yc + ((q & 2) ? 0.5 : -0.5) * g.dy;
+            double along = g.dso + px * sb - py * cb, perp = px * cb + py * sb;
+            double t = g.dsd * atan2(perp, along);
+            tmin = fmin(tmin, t);
+            tmax = fmax(tmax, t);
+        }
+        double a = fmax(tmin, g.s_lo), b = fmin(tmax, g.s_hi);
+        if (b > a) {
+            // channels whose bin overlaps (a, b) with positive length
+            double cbase = -(g.ns - 1) / 2.0 - g.offs;
+            long long c0 = (long long)floor(a / g.ds - cbase + 0.5), c1 = (long long)ceil(b / g.ds - cbase - 0.5);
+            long long nch = c1 - c0 + 1;
+            double along = g.dso + xc * sb - yc * cb, perp = xc * cb + yc * sb;
+            double rho = sqrt(along * along + perp * perp), mag = g.dsd / rho;
+            bool any = false;
+            for (int iz = 0; iz < g.nz; iz++) {
+                if (!m[col * g.nz + iz]) continue;
+                long long nrow = 1;
+                if (g.kind != 0) {
+                    double zj = g.z0 + iz * g.dz;
+                    double tm = (zj - 0.5 * g.dz - vz.y) * mag, tp = (zj + 0.5 * g.dz - vz.y) * mag;
+                    double ta = fmax(tm, g.t_lo), tb = fmin(tp, g.t_hi);
+                    if (!(tb > ta)) continue;
+                    double rbase = -(g.nt - 1) / 2.0 - g.offt;
+                    long long r0 = (long long)floor(ta / g.dt - rbase + 0.5), r1 = (long long)ceil(tb / g.dt - rbase - 0.5);
+                    nrow = r1 - r0 + 1;
+                }
+                cu++;
+                cn += (unsigned long long)(nch * nrow);
+                any = true;
+            }
+            cc += any ? 1 : 0;
+        }
+    }
+    // warp reduce then integer atomics (exact, order-independent)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cu += __shfl_down_sync(0xffffffffu, cu, o);
+        cn += __shfl_down_sync(0xffffffffu, cn, o);
+        cc += __shfl_down_sync(0xffffffffu, cc, o);
+    }
+    if ((threadIdx.x & 31) == 0 && cu) {
+        atomicAdd(&total[0], cu);
+        atomicAdd(&total[1], cn);
+        atomicAdd(&total[2], cc);
+    }
+}
+
+}  // namespace ct

@@ -1,0 +1,298 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Tolerances (BASELINE.json north_star):
+  projection / back-projection: relative L2 <= 1e-4 (per view and overall);
+  regulariser gradient / curvature: elementwise, 1e-5 of the max + 1e-4 relative;
+  OS-LALM image: RMS over S <= 0.5 HU (1 HU = 2e-5 mm^-1) with identical restart decisions;
+  U counts (integer): exact.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1402_4381_b200 import inputs as I
+from tests import geomutil as GU
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ct():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1402_4381_b200 import build, ctlib
+    build.build()
+    ctlib.load()
+    return ctlib
+
+
+@pytest.fixture(scope="module")
+def O():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def geoms_small():
+    gs = GU.small_geoms()
+    # ragged tiles / offsets / non-square: extra cases
+    gs["fan_offsets"] = GU.geom("fan2d", nx=30, ny=22, dx=2.0, ns=77, ds=2.5, na=50, offx=3.1, offy=-2.2, offs=0.37,
+                                start=11.0)
+    gs["axial_offsets"] = GU.geom("cone_axial", nx=14, ny=11, nz=9, dx=1.5, dz=1.1, ns=37, ds=1.9, nt=13, dt=1.3,
+                                  na=30, offx=-0.7, offz=0.4, offs=-0.21, offt=0.33)
+    return gs
+
+
+def rand_image(g, seed, shape_abi):
+    rng = np.random.default_rng(seed)
+    return rng.random(shape_abi).astype(np.float32)
+
+
+# --------------------------------------------------------------------------- projector
+
+@pytest.mark.parametrize("name", list(geoms_small().keys()))
+def test_fwd_back_small(ct, O, name):
+    g = geoms_small()[name]
+    geo = ct.Geometry(g)
+    x = rand_image(g, 1, geo.img_shape)
+    xt = torch.from_numpy(x).cuda()
+    for views in ((0, 1, g["na"]), (1, 3, (g["na"] - 1 + 2) // 3), (2, 5, 1)):
+        yg = geo.fwd(xt, views).cpu().numpy()
+        yo = O.fwd(g, I.to_oracle_image(x), *views)
+        assert rel_l2(I.to_oracle_sino(yg), yo) <= 1e-4, name
+        p = np.random.default_rng(2).random(yg.shape).astype(np.float32)
+        bg = geo.back(torch.from_numpy(p).cuda(), views).cpu().numpy()
+        bo = O.back(g, I.to_oracle_sino(p), *views)
+        assert rel_l2(I.to_oracle_image(bg), bo) <= 1e-4, name
+
+
+@pytest.mark.parametrize("name", ["fan_c2", "axial_c3", "helical_c5"])
+def test_adjoint_gpu(ct, name):
+    g = geoms_small()[name]
+    geo = ct.Geometry(g)
+    x = torch.from_numpy(rand_image(g, 3, geo.img_shape)).cuda()
+    p = torch.rand(geo.sino_shape(g["na"]), device="cuda")
+    lhs = (geo.fwd(x).double() * p.double()).sum().item()
+    rhs = (x.double() * geo.back(p).double()).sum().item()
+    assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+
+
+def test_back_accumulate_and_empty_views(ct):
+    g = geoms_small()["axial_c3"]
+    geo = ct.Geometry(g)
+    p = torch.rand(geo.sino_shape(g["na"]), device="cuda")
+    full = geo.back(p)
+    acc = torch.zeros_like(full)
+    # virtual ranks: contiguous view blocks, partial back-projections summed
+    from paper_1402_4381_b200 import host
+    for r in range(3):
+        k0, n = host.rank_view_block(g["na"], r, 3)
+        geo.back(p[k0:k0 + n].contiguous(), (k0, 1, n), out=acc, accumulate=True)
+    assert rel_l2(acc.cpu().numpy(), full.cpu().numpy()) <= 1e-6
+    empty = geo.back(p[:0].contiguous(), (0, 1, 0))
+    assert torch.count_nonzero(empty).item() == 0
+    with pytest.raises(ct.CTError, match="CT_EINVAL"):
+        geo.back(p, (5, 1, g["na"]))
+
+
+def test_determinism(ct):
+    g = I.config("c1").geom
+    geo = ct.Geometry(g)
+    x = torch.rand(geo.img_shape, device="cuda")
+    a = geo.fwd(x); b = geo.fwd(x)
+    assert torch.equal(a, b)
+    p = torch.rand_like(a)
+    assert torch.equal(geo.back(p), geo.back(p))
+
+
+@pytest.mark.parametrize("cname,views", [
+    ("c1", None),
+    ("c2", (5, 24, 41)),          # one c2 subset (41 views) at full image/detector size
+    ("c3", (7, 24, 41)),          # one c3 subset
+    ("c4", (1000, 97, 6)),        # helical: sampled views
+    ("c5", (3000, 211, 5)),
+])
+def test_projector_full_size(ct, O, cname, views):
+    """Full BASELINE sizes in the bench's launch configuration, on sampled view lists."""
+    cfg = I.config(cname)
+    g = cfg.geom
+    geo = ct.Geometry(g)
+    views = views or (0, 1, g["na"])
+    rng = np.random.default_rng(4)
+    x = (rng.random(geo.img_shape).astype(np.float32) * 0.02) * I.support_mask(cfg).numpy()
+    xt = torch.from_numpy(x).cuda()
+    yg = geo.fwd(xt, views).cpu().numpy()
+    yo = O.fwd(g, I.to_oracle_image(x), *views)
+    assert rel_l2(I.to_oracle_sino(yg), yo) <= 1e-4
+    for k in range(views[2]):
+        assert rel_l2(I.to_oracle_sino(yg)[k], yo[k]) <= 1e-4
+    p = rng.random(yg.shape).astype(np.float32)
+    bg = geo.back(torch.from_numpy(p).cuda(), views).cpu().numpy()
+    bo = O.back(g, I.to_oracle_sino(p), *views)
+    assert rel_l2(I.to_oracle_image(bg), bo) <= 1e-4
+
+
+@pytest.mark.parametrize("name", ["fan_c1", "axial_c3", "helical_c4", "fan_offsets"])
+def test_count_vv_exact(ct, O, name):
+    g = geoms_small()[name]
+    geo = ct.Geometry(g)
+    rng = np.random.default_rng(5)
+    m = (rng.random(geo.img_shape) > 0.2).astype(np.uint8)
+    assert geo.count_vv(torch.from_numpy(m).cuda()) == O.count_vv(g, I.to_oracle_image(m).astype(np.uint8))
+    assert geo.count_vv(torch.from_numpy(m).cuda(), (1, 4, (g["na"] - 1 + 3) // 4)) == \
+        O.count_vv(g, I.to_oracle_image(m).astype(np.uint8), 1, 4)
+
+
+def test_count_vv_c2_exact(ct, O):
+    cfg = I.config("c2")
+    geo = ct.Geometry(cfg.geom)
+    m = I.support_mask(cfg)
+    assert geo.count_vv(m.cuda(), (3, 24, 41)) == O.count_vv(cfg.geom, I.to_oracle_image(m).astype(np.uint8), 3, 24)
+
+
+# --------------------------------------------------------------------------- D_L, regulariser
+
+@pytest.mark.parametrize("name", ["c1", "axial_c3", "helical_c4"])
+def test_sqs_denom(ct, O, name):
+    if name == "c1":
+        cfg = I.config("c1"); g = cfg.geom
+        m0 = I.support_mask(cfg).numpy()
+        w = I.synthesize(cfg)["w"].numpy()
+    else:
+        g = geoms_small()[name]
+        shape = (g["ny"], g["nx"], g["nz"])
+        m0 = np.ones(shape, np.uint8)
+        w = (np.random.default_rng(6).random((g["na"], g["ns"], g["nt"])) * 100 + 1).astype(np.float32)
+    geo = ct.Geometry(g)
+    dl, m = geo.sqs_denom(torch.from_numpy(w).cuda(), torch.from_numpy(m0).cuda())
+    dlo, mo = O.sqs_denom(g, I.to_oracle_sino(w), I.to_oracle_image(m0).astype(np.uint8))
+    assert np.array_equal(I.to_oracle_image(m.cpu().numpy()).astype(np.uint8), mo)
+    assert rel_l2(I.to_oracle_image(dl.cpu().numpy()), dlo) <= 1e-4
+
+
+@pytest.mark.parametrize("name,nbr", [("fan_c2", 8), ("axial_c3", 26), ("axial_offsets", 26), ("axial_c3", 8)])
+def test_reg_grad(ct, O, name, nbr):
+    g = geoms_small()[name]
+    geo = ct.Geometry(g)
+    rng = np.random.default_rng(7)
+    x = (rng.random(geo.img_shape) * 0.03).astype(np.float32)
+    m = (rng.random(geo.img_shape) > 0.1).astype(np.uint8)
+    beta, delta = 2.0 ** 10, 2e-4
+    gr, cu = geo.reg_grad(torch.from_numpy(x).cuda(), torch.from_numpy(m).cuda(), beta, delta, nbr)
+    gro, cuo = O.reg_grad(g, beta, delta, nbr, I.to_oracle_image(m).astype(np.uint8), I.to_oracle_image(x))
+    gr = I.to_oracle_image(gr.cpu().numpy()); cu = I.to_oracle_image(cu.cpu().numpy())
+    assert np.all(np.abs(gr - gro) <= 1e-5 * np.abs(gro).max() + 1e-4 * np.abs(gro))
+    assert np.all(np.abs(cu - cuo) <= 1e-5 * np.abs(cuo).max() + 1e-5 * np.abs(cuo))
+
+
+# --------------------------------------------------------------------------- OS-LALM
+
+def _run_pair(ct, O, cfg, n_iter, M=None, mode="continuation", rho_fixed=1.0, x0=None):
+    g = cfg.geom
+    M = M or cfg.M
+    d = I.synthesize(cfg)
+    y, w = d["y"], d["w"]
+    m0 = I.support_mask(cfg)
+    geo = ct.Geometry(g)
+    dl, S = geo.sqs_denom(w.cuda(), m0.cuda())
+    dlo, So = O.sqs_denom(g, I.to_oracle_sino(w), I.to_oracle_image(m0).astype(np.uint8))
+    assert np.array_equal(I.to_oracle_image(S.cpu().numpy()).astype(np.uint8), So)
+    sol = ct.OSLALM(geo, M, mode=mode, rho_fixed=rho_fixed, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr)
+    yc, wc = y.cuda(), w.cuda()
+    sol.set_data(yc, wc, dl, S)
+    x = torch.zeros(geo.img_shape, device="cuda") if x0 is None else x0.clone().cuda()
+    log = sol.run(x, n_iter, log=True)
+    xo, logo, _, _ = O.oslalm_run(g, I.to_oracle_sino(y), I.to_oracle_sino(w), dlo, So,
+                                  np.zeros(O.img_shape(g)) if x0 is None else I.to_oracle_image(x0),
+                                  M=M, mode=mode, rho_fixed=rho_fixed, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr,
+                                  n_iter=n_iter)
+    xg = I.to_oracle_image(x.cpu().numpy())
+    Sm = So > 0
+    rms_hu = math.sqrt(((xg - xo)[Sm] ** 2).mean()) / I.HU
+    return xg, xo, np.array(log), logo, rms_hu
+
+
+def test_oslalm_c1_full(ct, O):
+    """c1 (BASELINE configs[0]): 20 iterations, M = 4, continuation: <= 0.5 HU RMS on S."""
+    cfg = I.config("c1")
+    xg, xo, log, logo, rms = _run_pair(ct, O, cfg, cfg.n_iter)
+    assert rms <= 0.5, rms
+    assert np.array_equal(log[:, 2], logo[:, 2])          # identical restart decisions
+    assert np.allclose(log[:, 0], logo[:, 0], rtol=1e-12)  # identical rho trajectory
+    assert np.abs(xo).max() > 0.01                         # a non-trivial reconstruction
+
+
+@pytest.mark.parametrize("mode,rho", [("fixed", 1.0), ("fixed", 0.2), ("continuation", 1.0)])
+def test_oslalm_modes_small(ct, O, mode, rho):
+    cfg = I.scaled(I.config("c1"), "c1s", nx=48, ny=48, na=90)
+    xg, xo, log, logo, rms = _run_pair(ct, O, cfg, 6, M=5 if mode == "continuation" else 4, mode=mode, rho_fixed=rho)
+    assert rms <= 0.05, rms      # odd M exercises the graph's buffer-parity path
+    assert np.array_equal(log[:, 2], logo[:, 2])
+
+
+def test_oslalm_M1_restarts(ct, O):
+    """M = 1 with continuation fires restarts (V7); decisions must match the oracle."""
+    cfg = I.scaled(I.config("c1"), "c1m1", nx=32, ny=32, na=60)
+    xg, xo, log, logo, rms = _run_pair(ct, O, cfg, 60, M=1)
+    assert logo[:, 2].sum() >= 1
+    assert np.array_equal(log[:, 2], logo[:, 2])
+    assert rms <= 0.05, rms
+
+
+@pytest.mark.parametrize("name", ["axial_c3", "helical_c4"])
+def test_oslalm_3d_small(ct, O, name):
+    g = geoms_small()[name]
+    base = I.config("c3")
+    cfg = I.ScanConfig(name, g, 4, 8, base.beta, base.delta, 26, 1e5, 0.0, "body3d", body_z=2.0)
+    cfg.extra = {}
+    # phantom scaled into the small grid: a water cylinder + inserts
+    ell = [(0.0, 0.0, 0.0, 4.0, 3.5, 2.0, 0.0, 0.02), (1.0, -0.5, 0.3, 1.2, 0.8, 0.9, 0.4, 0.01)]
+    d = I.noisy_data(g, ell, 1e5, 0.0, 77)
+    geo = ct.Geometry(g)
+    m0 = torch.ones(geo.img_shape, dtype=torch.uint8)
+    dl, S = geo.sqs_denom(d["w"].cuda(), m0.cuda())
+    dlo, So = O.sqs_denom(g, I.to_oracle_sino(d["w"]), I.to_oracle_image(m0).astype(np.uint8))
+    sol = ct.OSLALM(geo, 4, beta=cfg.beta, delta=cfg.delta, nbr=26)
+    sol.set_data(d["y"].cuda(), d["w"].cuda(), dl, S)
+    x = torch.zeros(geo.img_shape, device="cuda")
+    log = np.array(sol.run(x, 8, log=True))
+    xo, logo, _, _ = O.oslalm_run(g, I.to_oracle_sino(d["y"]), I.to_oracle_sino(d["w"]), dlo, So,
+                                  np.zeros(O.img_shape(g)), M=4, beta=cfg.beta, delta=cfg.delta, nbr=26, n_iter=8)
+    xg = I.to_oracle_image(x.cpu().numpy())
+    rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
+    assert rms <= 0.5, rms
+    assert np.array_equal(log[:, 2], logo[:, 2])
+
+
+def test_oslalm_c2_full_size(ct, O):
+    """c2 (BASELINE configs[1]) at full size for 2 iterations (oracle cost bound): <= 0.5 HU."""
+    cfg = I.config("c2")
+    xg, xo, log, logo, rms = _run_pair(ct, O, cfg, 2)
+    assert rms <= 0.5, rms
+    assert np.array_equal(log[:, 2], logo[:, 2])
+
+
+def test_iter_equals_run_and_state(ct):
+    cfg = I.config("c1")
+    d = I.synthesize(cfg)
+    geo = ct.Geometry(cfg.geom)
+    dl, S = geo.sqs_denom(d["w"].cuda(), I.support_mask(cfg).cuda())
+    a = ct.OSLALM(geo, 4, beta=cfg.beta, delta=cfg.delta, nbr=8)
+    b = ct.OSLALM(geo, 4, beta=cfg.beta, delta=cfg.delta, nbr=8)
+    for s in (a, b):
+        s.set_data(d["y"].cuda(), d["w"].cuda(), dl, S)
+    xa = torch.zeros(geo.img_shape, device="cuda"); xb = xa.clone()
+    a.run(xa, 5)
+    for _ in range(5):
+        b.iterate(xb)
+    torch.cuda.synchronize()
+    assert torch.equal(xa, xb)
+    assert a.scalars() == b.scalars()
+    assert a.scalars()[2] == 20
+    assert torch.equal(a.split_gradient(), b.split_gradient())
