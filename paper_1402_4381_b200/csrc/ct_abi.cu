@@ -130,9 +130,10 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     double hx = 0.5 * (d->nx - 1) * d->dx + fabs(d->offx) + d->dx, hy = 0.5 * (d->ny - 1) * d->dy + fabs(d->offy) + d->dy;
     double rmax = sqrt(hx * hx + hy * hy);
     if (rmax >= d->dso) return fail(CT_EINVAL, "image (radius %.1f mm) reaches the source orbit (dso %.1f)", rmax, d->dso);
-    double wmax = d->dx * sqrt(2.0) * d->dsd / ((d->dso - rmax) * d->ds) + 1.0;
+    // a footprint of width w channels touches at most ceil(w) + 1 <= kMaxFoot bins
+    double wmax = d->dx * sqrt(2.0) * d->dsd / ((d->dso - rmax) * d->ds);
     if (wmax > kMaxFoot - 1)
-        return fail(CT_EUNSUPPORTED, "voxel footprint may span %.1f channels (> %d)", wmax, kMaxFoot - 1);
+        return fail(CT_EUNSUPPORTED, "voxel footprint may be %.2f channels wide (> %d)", wmax, kMaxFoot - 1);
 
     int dev = d->device;
     DeviceGuard guard(dev);
@@ -214,6 +215,18 @@ static int check_views(const ct_geom* g, ct_views v) {
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
+template <int TC, int NTP, bool RESID>
+static void launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const float* x, float* out, const float* yobs,
+                         const float* w, float scale, cudaStream_t st) {
+    constexpr size_t smem = fwd3d_smem<TC, NTP, 256>();
+    static bool configured = false;   // per template instance
+    if (!configured) {
+        cudaFuncSetAttribute(fwd3d_kernel<TC, NTP, 256, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    fwd3d_kernel<TC, NTP, 256, RESID><<<grid, 256, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+}
+
 template <bool RESID>
 static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, const float* yobs, const float* w,
                       float scale, cudaStream_t st) {
@@ -224,14 +237,14 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         fwd2d_kernel<TC, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
     } else {
-        constexpr int TC = 16;
+        constexpr int TC = 32;
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32)
-            fwd3d_kernel<TC, 32, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+            launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, st);
         else if (dg.nt <= 64)
-            fwd3d_kernel<TC, 64, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+            launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, st);
         else
-            fwd3d_kernel<TC, 128, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+            launch_fwd3d<TC, 128, RESID>(dg, grid, v, x, out, yobs, w, scale, st);
     }
     CT_LAUNCHED(1);
     return CT_OK;
@@ -242,7 +255,7 @@ static void back_grid(const ct_geom* g, dim3& grid) {
     if (dg.kind == CT_FAN2D)
         grid = dim3((dg.nx + 31) / 32, (dg.ny + 7) / 8, 1);
     else
-        grid = dim3((dg.nx + 7) / 8, dg.ny, (dg.nz + 31) / 32);
+        grid = dim3((dg.nx + 3) / 4, (dg.ny + 3) / 4, (dg.nz + 31) / 32);
 }
 
 static size_t back_nblocks(const ct_geom* g) {
@@ -259,7 +272,7 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
     if (dg.kind == CT_FAN2D)
         back2d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
     else
-        back3d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+        back3d_kernel<EPI><<<grid, 512, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
     CT_LAUNCHED(1);
     return CT_OK;
 }
@@ -303,6 +316,7 @@ extern "C" int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask, flo
     CT_LAUNCHED(1);
     if (int e = launch_fwd<true>(g, all, one, sino, nullptr, w, 1.0f, st)) return e;
     GupdArgs ga{};
+    ga.mask = mask;   // D_L is only needed on S (set to 0 elsewhere below)
     if (int e = launch_back<EPI_STORE>(g, all, sino, dl, ga, st)) return e;
     mask_finalize_kernel<<<nblk(N), 256, 0, st>>>(mask, dl, N);
     CT_LAUNCHED(1);
@@ -597,7 +611,7 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
         tmark_end(s, st, 2, t1);
         return e;
     }
-    // multi-rank: partial back-projection, NCCL sum, then the unfused epilogue
+    // multi-rank: partial back-projection (on S), NCCL sum, then the unfused epilogue
     int t1 = tmark(s, st);
     if (int e = launch_back<EPI_STORE>(g, v, s->sino, s->Gtmp, ga, st)) return e;
     tmark_end(s, st, 2, t1);

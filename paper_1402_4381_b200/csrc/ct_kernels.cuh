@@ -202,19 +202,60 @@ __global__ void __launch_bounds__(NTHR) fwd2d_kernel(DevGeom g, int first, int s
 }
 
 // ---------------------------------------------------------------------------
+// Footprint of one (voxel column, view), computed lane-parallel and broadcast
+// to the warp with shuffles (the column's transaxial part is shared by all its
+// voxels and, in the forward projector, by all detector rows).
+// ---------------------------------------------------------------------------
+struct __align__(16) Foot {
+    float w[kMaxFoot];      // lphi * F_s(cA + j)
+    int cA, n;              // first channel and channel count (n <= 0: misses the detector)
+    Axial ax;               // 5 words
+    int pad;
+};
+static_assert(sizeof(Foot) == 64, "Foot must be 64 bytes");
+
+__device__ __forceinline__ void load_foot(const Foot* src, Foot& d) {
+    const float4* p = reinterpret_cast<const float4*>(src);
+    float4 a = p[0], b = p[1], c = p[2], e = p[3];
+    d.w[0] = a.x; d.w[1] = a.y; d.w[2] = a.z; d.w[3] = a.w;
+    d.w[4] = b.x; d.w[5] = b.y; d.w[6] = b.z; d.w[7] = b.w;
+    d.cA = __float_as_int(c.x); d.n = __float_as_int(c.y); d.ax.qi = __float_as_int(c.z); d.ax.qf = c.w;
+    d.ax.kz = e.x; d.ax.inv_kz = e.y; d.ax.dz_rho = e.z;
+}
+
+__device__ __forceinline__ void column_footprint(const DevGeom& g, float4 vw, float xc, float yc, Foot& f) {
+    Trans tr;
+    transaxial(g, vw.x, vw.y, xc, yc, tr);
+    foot_range(g, tr, f.cA, f.n);
+    TrapCdf F(tr);
+    float e = (float)f.cA - 0.5f - tr.cc;
+    float Fp = F(e);
+#pragma unroll
+    for (int j = 0; j < kMaxFoot; j++) {
+        float Fn = F(e + (float)(j + 1));
+        f.w[j] = (j < f.n) ? tr.lphi * (Fn - Fp) : 0.0f;
+        Fp = Fn;
+    }
+    axial(g, vw, tr.rho, f.ax);
+}
+
+// ---------------------------------------------------------------------------
 // K1 (3D cone): forward projection of one (view, channel tile, all rows)
 // ---------------------------------------------------------------------------
 // CTA = (tile of TC channels, view k); NTHR threads = G groups of NTP row-threads.
-// Group gi walks sweep lines gi, gi+G, ...; for each wedge column all threads of
-// the group (one per detector row r) compute the column's axial sum
-//   A(r) = sum_iz x[iz] l_theta(iz) F_t(iz, r)      (z-fastest layout: coalesced)
-// and add lphi F_s(c) A(r) to a register window over the column's channels.
+// Group gi walks sweep lines gi, gi+G, ...; the footprints of a line's wedge
+// columns are computed group-parallel (one column per thread) into a shared
+// table; then, for each column in channel order, thread r computes the column's
+// axial sum  A(r) = sum_iz x[iz] l_theta(iz) F_t(iz, r)  (z-fastest layout:
+// coalesced) and adds lphi F_s(c) A(r) to a register window over the channels.
 template <int TC, int NTP, int NTHR, bool RESID>
-__global__ void __launch_bounds__(NTHR) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
-                                                     float* __restrict__ out, const float* __restrict__ yobs,
-                                                     const float* __restrict__ wts, float scale) {
+__global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
+                                                        float* __restrict__ out, const float* __restrict__ yobs,
+                                                        const float* __restrict__ wts, float scale) {
     constexpr int G = NTHR / NTP;
-    __shared__ float P[G][TC][NTP + 1];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float (*P)[TC][NTP + 1] = reinterpret_cast<float (*)[TC][NTP + 1]>(smem_raw);
+    Foot* table = reinterpret_cast<Foot*>(smem_raw + sizeof(float) * G * TC * (NTP + 1));
     const int c0 = blockIdx.x * TC;
     const int k = blockIdx.y;
     const int v = first + k * stride;
@@ -222,6 +263,8 @@ __global__ void __launch_bounds__(NTHR) fwd3d_kernel(DevGeom g, int first, int s
     const float sb = vw.x, cb = vw.y;
     const int gi = threadIdx.x / NTP, r = threadIdx.x % NTP;
     const bool row_ok = r < g.nt;
+    const float qr_off = ((float)r - g.rbase);
+    Foot* tab = table + gi * NTP;
 #pragma unroll
     for (int c = 0; c < TC; c++) P[gi][c][r] = 0.0f;
     Wedge w = make_wedge(g, sb, cb, c0, TC);
@@ -232,72 +275,78 @@ __global__ void __launch_bounds__(NTHR) fwd3d_kernel(DevGeom g, int first, int s
         if (lo > hi) continue;
         Window win;
         win.reset(-1000000);
-        int n_in = hi - lo + 1;
-        for (int q = 0; q < n_in; q++) {
-            int u = w.increasing ? lo + q : hi - q;
-            int ix = w.rows ? u : L, iy = w.rows ? L : u;
-            Trans tr;
-            transaxial(g, sb, cb, g.x0 + ix * g.dx, g.y0 + iy * g.dy, tr);
-            int cA, n;
-            foot_range(g, tr, cA, n);
-            if (n <= 0 || cA + n <= c0 || cA >= c0 + TC) continue;
-            Axial ax;
-            axial(g, vw, tr.rho, ax);
-            // axial sum for this thread's row
-            float A = 0.0f;
-            if (row_ok) {
-                float qr = row_center_q(ax, g, r);
-                int iz0, iz1;
-                row_voxels(ax, qr, iz0, iz1);
-                iz0 = max(iz0, 0);
-                iz1 = min(iz1, nz - 1);
-                const float* xc = x + ((size_t)iy * g.nx + ix) * nz;
-                for (int iz = iz0; iz <= iz1; iz++) {
-                    float ft = axial_weight(ax, qr, iz);
-                    A += __ldg(&xc[iz]) * ltheta(ax, iz) * ft;
-                }
+        const int n_in = hi - lo + 1;
+        for (int cb0 = 0; cb0 < n_in; cb0 += NTP) {
+            // group-parallel footprints of up to NTP columns of this line (channel order)
+            int q = cb0 + r;
+            if (q < n_in) {
+                int u = w.increasing ? lo + q : hi - q;
+                int ix = w.rows ? u : L, iy = w.rows ? L : u;
+                Foot f;
+                column_footprint(g, vw, g.x0 + ix * g.dx, g.y0 + iy * g.dy, f);
+                if (!(f.n > 0 && f.cA + f.n > c0 && f.cA < c0 + TC)) f.n = 0;   // misses the tile
+                tab[r] = f;
             }
-            TrapCdf F(tr);
-            if (cA >= win.base) {
-                while (win.base < cA) {
-                    int cc = win.base - c0;
-                    if (cc >= 0 && cc < TC) P[gi][cc][r] += win.acc[0];
+            asm volatile("bar.sync %0, %1;" ::"r"(gi + 1), "r"(NTP) : "memory");
+            const int nq = min(NTP, n_in - cb0);
+            for (int j = 0; j < nq; j++) {
+                Foot f;
+                load_foot(&tab[j], f);
+                if (f.n <= 0) continue;
+                const int qj = cb0 + j;
+                const int u = w.increasing ? lo + qj : hi - qj;
+                const int ix = w.rows ? u : L, iy = w.rows ? L : u;
+                float A = 0.0f;
+                if (row_ok) {
+                    float qr = f.ax.qf + qr_off * f.ax.kz;
+                    int iz0, iz1;
+                    row_voxels(f.ax, qr, iz0, iz1);
+                    iz0 = max(iz0, 0);
+                    iz1 = min(iz1, nz - 1);
+                    const float* xc = x + ((size_t)iy * g.nx + ix) * nz;
+                    for (int iz = iz0; iz <= iz1; iz++)
+                        A += __ldg(&xc[iz]) * ltheta(f.ax, iz) * axial_weight(f.ax, qr, iz);
+                }
+                const int cA = f.cA;
+                if (cA >= win.base) {
+                    while (win.base < cA) {
+                        int cc = win.base - c0;
+                        if (cc >= 0 && cc < TC) P[gi][cc][r] += win.acc[0];
 #pragma unroll
-                    for (int j = 0; j < kMaxFoot - 1; j++) win.acc[j] = win.acc[j + 1];
-                    win.acc[kMaxFoot - 1] = 0.0f;
-                    win.base++;
-                    if (win.base < cA - kMaxFoot) {
-                        int jmp = cA - win.base;
+                        for (int jj = 0; jj < kMaxFoot - 1; jj++) win.acc[jj] = win.acc[jj + 1];
+                        win.acc[kMaxFoot - 1] = 0.0f;
+                        win.base++;
+                        if (win.base < cA - kMaxFoot) {
+                            int jmp = cA - win.base;
 #pragma unroll
-                        for (int j = 0; j < kMaxFoot; j++) {
-                            int c1 = win.base + j - c0;
-                            if (c1 >= 0 && c1 < TC) P[gi][c1][r] += win.acc[j];
+                            for (int jj = 0; jj < kMaxFoot; jj++) {
+                                int c1 = win.base + jj - c0;
+                                if (c1 >= 0 && c1 < TC) P[gi][c1][r] += win.acc[jj];
+                            }
+                            win.reset(win.base + jmp);
                         }
-                        win.reset(win.base + jmp);
                     }
-                }
-                float lA = tr.lphi * A;
-                float e = (float)cA - 0.5f - tr.cc;
-                float Fp = F(e);
+                    if (f.n <= 4) {
 #pragma unroll
-                for (int j = 0; j < kMaxFoot; j++) {
-                    if (j < n) {
-                        float Fn = F(e + (float)(j + 1));
-                        win.acc[j] += lA * (Fn - Fp);
-                        Fp = Fn;
+                        for (int jj = 0; jj < 4; jj++) win.acc[jj] += f.w[jj] * A;
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < kMaxFoot; jj++) win.acc[jj] += f.w[jj] * A;
                     }
-                }
-            } else {
-                for (int j = 0; j < n; j++) {
-                    int c = cA + j - c0;
-                    if (c >= 0 && c < TC) P[gi][c][r] += A * chan_weight(F, tr.cc, tr.lphi, cA + j);
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < kMaxFoot; jj++) {
+                        int c = cA + jj - c0;
+                        if (jj < f.n && c >= 0 && c < TC) P[gi][c][r] += f.w[jj] * A;
+                    }
                 }
             }
+            asm volatile("bar.sync %0, %1;" ::"r"(gi + 1), "r"(NTP) : "memory");
         }
 #pragma unroll
-        for (int j = 0; j < kMaxFoot; j++) {
-            int c = win.base + j - c0;
-            if (c >= 0 && c < TC) P[gi][c][r] += win.acc[j];
+        for (int jj = 0; jj < kMaxFoot; jj++) {
+            int c = win.base + jj - c0;
+            if (c >= 0 && c < TC) P[gi][c][r] += win.acc[jj];
         }
     }
     __syncthreads();
@@ -317,6 +366,11 @@ __global__ void __launch_bounds__(NTHR) fwd3d_kernel(DevGeom g, int first, int s
             out[oi] = s;
         }
     }
+}
+
+template <int TC, int NTP, int NTHR>
+constexpr size_t fwd3d_smem() {
+    return sizeof(float) * (NTHR / NTP) * TC * (NTP + 1) + sizeof(Foot) * NTHR;
 }
 
 // ---------------------------------------------------------------------------
@@ -378,8 +432,11 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
     const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
     const int iy = blockIdx.y * 8 + (threadIdx.x >> 5);
     const bool valid = ix < g.nx && iy < g.ny;
+    const size_t jv = (size_t)(valid ? iy : 0) * g.nx + (valid ? ix : 0);
+    // voxels outside the support S are not needed by OS-LALM / D_L: skip their views
+    const bool act = valid && (ga.mask == nullptr || ga.mask[jv]);
     float acc = 0.0f;
-    if (valid) {
+    if (act) {
         const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
         for (int k = 0; k < count; k++) {
             const float4 vw = g.views[first + k * stride];
@@ -411,71 +468,72 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
 // ---------------------------------------------------------------------------
 // K2 (3D cone): voxel-driven back projection; warp = one column x 32 slices
 // ---------------------------------------------------------------------------
-// The column's transaxial footprint is warp-uniform (computed once per view per
-// warp); lanes walk z, so sinogram reads y[k][c][r..] are unit-stride in r.
+// Block = 4x4 columns (16 warps); lanes walk z, so sinogram reads y[k][c][r..]
+// are unit-stride in r.  Views are processed in batches of 32: lane l computes
+// the column's footprint for view vb + l into the warp's shared table, then the
+// warp walks the batch reading each footprint by broadcast (no recomputation).
 template <int EPI>
-__global__ void __launch_bounds__(256) back3d_kernel(DevGeom g, int first, int stride, int count,
-                                                    const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
+__global__ void __launch_bounds__(512, 2) back3d_kernel(DevGeom g, int first, int stride, int count,
+                                                       const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
+    __shared__ Foot table[16][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ix = blockIdx.x * 8 + wid;
-    const int iy = blockIdx.y;
-    const int iz = blockIdx.z * 32 + lane;
-    const bool colok = ix < g.nx;
+    const int ix = blockIdx.x * 4 + (wid & 3);
+    const int iy = blockIdx.y * 4 + (wid >> 2);
+    const int zlo = blockIdx.z * 32;
+    const int iz = zlo + lane;
+    const bool colok = ix < g.nx && iy < g.ny;
     const bool valid = colok && iz < g.nz;
     const int nt = g.nt, ns = g.ns;
+    const size_t jv = ((size_t)(colok ? iy : 0) * g.nx + (colok ? ix : 0)) * g.nz + (valid ? iz : 0);
+    // voxels outside the support S are not needed by OS-LALM / D_L: skip them (warp-uniformly)
+    const bool act = valid && (ga.mask == nullptr || ga.mask[jv]);
+    const bool warp_act = __ballot_sync(0xffffffffu, act) != 0u;
+    Foot* tab = table[wid];
     float acc = 0.0f;
-    if (colok) {
+    if (warp_act) {
         const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
-        const int zlo = blockIdx.z * 32, zhi = min(g.nz, zlo + 32) - 1;
-        for (int k = 0; k < count; k++) {
-            const float4 vw = g.views[first + k * stride];
-            Trans tr;
-            transaxial(g, vw.x, vw.y, xc, yc, tr);
-            Axial ax;
-            axial(g, vw, tr.rho, ax);
-            // warp-uniform skip when the chunk's rows miss the detector (helical)
-            int ra, rb, rc, rd;
-            voxel_rows(ax, g, zlo, ra, rb);
-            voxel_rows(ax, g, zhi, rc, rd);
-            if (rd < 0 || ra >= nt) continue;
-            int cA, n;
-            foot_range(g, tr, cA, n);
-            if (n <= 0) continue;
-            TrapCdf F(tr);
-            float wc[kMaxFoot];
-            {
-                float e = (float)cA - 0.5f - tr.cc;
-                float Fp = F(e);
+        const int zhi = min(g.nz, zlo + 32) - 1;
+        for (int vb = 0; vb < count; vb += 32) {
+            const int kk = vb + lane;
+            if (kk < count) {
+                Foot f;
+                column_footprint(g, g.views[first + kk * stride], xc, yc, f);
+                int ra, rb, rc, rd;
+                voxel_rows(f.ax, g, zlo, ra, rb);
+                voxel_rows(f.ax, g, zhi, rc, rd);
+                if (!(rd >= 0 && ra < nt)) f.n = 0;   // the chunk's rows miss the detector
+                tab[lane] = f;
+            }
+            __syncwarp();
+            const int nb = min(32, count - vb);
+            if (act) {
+                for (int j = 0; j < nb; j++) {
+                    Foot f;
+                    load_foot(&tab[j], f);
+                    if (f.n <= 0) continue;
+                    int r0, r1;
+                    voxel_rows(f.ax, g, iz, r0, r1);
+                    r0 = max(r0, 0);
+                    r1 = min(r1, nt - 1);
+                    const float* yk = y + ((size_t)(vb + j) * ns + f.cA) * nt;
+                    float s = 0.0f;
+                    for (int r = r0; r <= r1; r++) {
+                        float ft = axial_weight(f.ax, row_center_q(f.ax, g, r), iz);
+                        float t = 0.0f;
 #pragma unroll
-                for (int j = 0; j < kMaxFoot; j++) {
-                    float Fn = F(e + (float)(j + 1));
-                    wc[j] = (j < n) ? tr.lphi * (Fn - Fp) : 0.0f;
-                    Fp = Fn;
+                        for (int c = 0; c < kMaxFoot; c++)
+                            if (c < f.n) t += f.w[c] * __ldg(&yk[(size_t)c * nt + r]);
+                        s += ft * t;
+                    }
+                    acc += ltheta(f.ax, iz) * s;
                 }
             }
-            if (!valid) continue;
-            int r0, r1;
-            voxel_rows(ax, g, iz, r0, r1);
-            r0 = max(r0, 0);
-            r1 = min(r1, nt - 1);
-            if (r0 > r1) continue;
-            const float* yk = y + ((size_t)k * ns + cA) * nt;
-            float s = 0.0f;
-            for (int r = r0; r <= r1; r++) {
-                float ft = axial_weight(ax, row_center_q(ax, g, r), iz);
-                float t = 0.0f;
-#pragma unroll
-                for (int j = 0; j < kMaxFoot; j++)
-                    if (j < n) t += wc[j] * __ldg(&yk[(size_t)j * nt + r]);
-                s += ft * t;
-            }
-            acc += ltheta(ax, iz) * s;
+            __syncwarp();
         }
     }
-    size_t j = ((size_t)iy * g.nx + (colok ? ix : 0)) * g.nz + iz;
-    double xi = back_epilogue<EPI>(j, valid, acc, x, ga);
+    double xi = back_epilogue<EPI>(jv, valid, acc, x, ga);
     if (EPI == EPI_GUPD)
-        block_sum_store<256>(xi, &ga.xi_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]);
+        block_sum_store<512>(xi, &ga.xi_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
