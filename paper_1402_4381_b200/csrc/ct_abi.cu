@@ -255,7 +255,7 @@ static void back_grid(const ct_geom* g, dim3& grid) {
     if (dg.kind == CT_FAN2D)
         grid = dim3((dg.nx + 31) / 32, (dg.ny + 7) / 8, 1);
     else
-        grid = dim3((dg.nx + 3) / 4, (dg.ny + 3) / 4, (dg.nz + 31) / 32);
+        grid = dim3((dg.nx + 3) / 4, (dg.ny + 1) / 2, (dg.nz + 63) / 64);
 }
 
 static size_t back_nblocks(const ct_geom* g) {
@@ -272,7 +272,7 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
     if (dg.kind == CT_FAN2D)
         back2d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
     else
-        back3d_kernel<EPI><<<grid, 512, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+        back3d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
     CT_LAUNCHED(1);
     return CT_OK;
 }

@@ -57,24 +57,48 @@ __device__ __forceinline__ float small_atan(float u) {
     return u * (1.0f - u2 * (1.0f / 3.0f - u2 * 0.2f));
 }
 
+// atan(u) for any u: odd minimax polynomial on [-1, 1] (max error 1.0e-7 in fp32,
+// comparable to atan2f) with the reduction atan(u) = sign(u) pi/2 - atan(1/u).
+__device__ __forceinline__ float fast_atan(float u) {
+    const float au = fabsf(u);
+    const bool big = au > 1.0f;
+    const float t = big ? __fdividef(1.0f, au) : au;
+    const float t2 = t * t;
+    float p = 2.456723016e-03f;
+    p = fmaf(p, t2, -1.440135344e-02f);
+    p = fmaf(p, t2, 3.978122036e-02f);
+    p = fmaf(p, t2, -7.234857604e-02f);
+    p = fmaf(p, t2, 1.049894656e-01f);
+    p = fmaf(p, t2, -1.416122948e-01f);
+    p = fmaf(p, t2, 1.998590685e-01f);
+    p = fmaf(p, t2, -3.333259704e-01f);
+    p = fmaf(p, t2, 9.999998864e-01f);
+    float r = p * t;
+    r = big ? 1.57079632679489662f - r : r;
+    return copysignf(r, u);
+}
+
 __device__ __forceinline__ void transaxial(const DevGeom& g, float sb, float cb, float xc, float yc, Trans& tr) {
-    float along = g.dso + xc * sb - yc * cb;     // (p - S) . e_c
+    float along = g.dso + xc * sb - yc * cb;     // (p - S) . e_c  (> 0: the image is inside the orbit)
     float perp = xc * cb + yc * sb;              // (p - S) . e_perp
     float rho2 = along * along + perp * perp;
     float rho = sqrtf(rho2);
     tr.rho = rho;
-    tr.cc = atan2f(perp, along) * g.dsd_ds + g.cbase;
-    // corner offsets (+-hx, +-hy): d_along = sx*ax + sy*ay, d_perp = sx*px + sy*py
+    tr.cc = fast_atan(__fdividef(perp, along)) * g.dsd_ds + g.cbase;
+    // corner offsets (+-hx, +-hy).  Opposite corners are negatives of each other,
+    // so two "diagonals" (sx, sy) = (+,+) and (+,-) give all four breakpoints:
+    //   corner = +-(d_along, d_perp); Delta gamma = atan(cross / dot) relative to the centre ray.
     float hx = 0.5f * g.dx, hy = 0.5f * g.dy;
     float ax = hx * sb, ay = -hy * cb, px = hx * cb, py = hy * sb;
     float t[4];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-        float sx = (k & 1) ? 1.0f : -1.0f, sy = (k & 2) ? 1.0f : -1.0f;
-        float da = sx * ax + sy * ay, dp = sx * px + sy * py;
-        float cross = along * dp - perp * da;
-        float dot = rho2 + along * da + perp * dp;
-        t[k] = small_atan(__fdividef(cross, dot)) * g.dsd_ds;
+    for (int k = 0; k < 2; k++) {
+        float sy = k ? -1.0f : 1.0f;
+        float da = ax + sy * ay, dp = px + sy * py;
+        float cross = along * dp - perp * da;      // odd in the corner offset
+        float lin = along * da + perp * dp;        // odd in the corner offset
+        t[2 * k] = small_atan(__fdividef(cross, rho2 + lin)) * g.dsd_ds;
+        t[2 * k + 1] = small_atan(__fdividef(-cross, rho2 - lin)) * g.dsd_ds;
     }
     // 5-comparator sorting network
     sort2(t[0], t[1]);
@@ -84,7 +108,7 @@ __device__ __forceinline__ void transaxial(const DevGeom& g, float sb, float cb,
     sort2(t[1], t[2]);
     tr.t0 = t[0]; tr.t1 = t[1]; tr.t2 = t[2]; tr.t3 = t[3];
     float dirx = fabsf(xc + g.dso * sb), diry = fabsf(yc - g.dso * cb);
-    tr.lphi = g.dx * rho / fmaxf(dirx, diry);
+    tr.lphi = __fdividef(g.dx * rho, fmaxf(dirx, diry));
 }
 
 // Antiderivative of the unit trapezoid (branch-free, degenerate widths safe).
@@ -92,8 +116,8 @@ struct TrapCdf {
     float t0, t1, t2, h0, h3;
     __device__ __forceinline__ TrapCdf(const Trans& tr) {
         t0 = tr.t0; t1 = tr.t1; t2 = tr.t2;
-        h0 = 0.5f / fmaxf(tr.t1 - tr.t0, 1e-20f);
-        h3 = 0.5f / fmaxf(tr.t3 - tr.t2, 1e-20f);
+        h0 = __fdividef(0.5f, fmaxf(tr.t1 - tr.t0, 1e-20f));
+        h3 = __fdividef(0.5f, fmaxf(tr.t3 - tr.t2, 1e-20f));
         t3 = tr.t3;
     }
     float t3;
@@ -141,9 +165,16 @@ __device__ __forceinline__ void axial(const DevGeom& g, float4 view, float rho, 
     ax.dz_rho = g.dz / rho;
 }
 
+__device__ __forceinline__ float sqrt_approx(float v) {
+    // MUFU square root (rel. error ~2^-22), ample for l_theta in [1, 1.01]
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+
 __device__ __forceinline__ float ltheta(const Axial& ax, int iz) {
     float tz = ((float)(iz - ax.qi) + 0.5f - ax.qf) * ax.dz_rho;
-    return sqrtf(1.0f + tz * tz);
+    return sqrt_approx(fmaf(tz, tz, 1.0f));
 }
 
 __device__ __forceinline__ float row_center_q(const Axial& ax, const DevGeom& g, int r) {

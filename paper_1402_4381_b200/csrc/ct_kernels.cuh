@@ -161,11 +161,10 @@ __global__ void __launch_bounds__(NTHR) fwd2d_kernel(DevGeom g, int first, int s
                 float Fp = F(e);
 #pragma unroll
                 for (int j = 0; j < kMaxFoot; j++) {
-                    if (j < n) {
-                        float Fn = F(e + (float)(j + 1));
-                        win.acc[j] += lx * (Fn - Fp);
-                        Fp = Fn;
-                    }
+                    if (j >= n) break;
+                    float Fn = F(e + (float)(j + 1));
+                    win.acc[j] += lx * (Fn - Fp);
+                    Fp = Fn;
                 }
             } else {
                 // out-of-order footprint (rounding at a line end): direct smem adds
@@ -210,7 +209,7 @@ struct __align__(16) Foot {
     float w[kMaxFoot];      // lphi * F_s(cA + j)
     int cA, n;              // first channel and channel count (n <= 0: misses the detector)
     Axial ax;               // 5 words
-    int pad;
+    int rows;               // back3d: first row | (row count << 16) of the warp's z-chunk
 };
 static_assert(sizeof(Foot) == 64, "Foot must be 64 bytes");
 
@@ -220,7 +219,7 @@ __device__ __forceinline__ void load_foot(const Foot* src, Foot& d) {
     d.w[0] = a.x; d.w[1] = a.y; d.w[2] = a.z; d.w[3] = a.w;
     d.w[4] = b.x; d.w[5] = b.y; d.w[6] = b.z; d.w[7] = b.w;
     d.cA = __float_as_int(c.x); d.n = __float_as_int(c.y); d.ax.qi = __float_as_int(c.z); d.ax.qf = c.w;
-    d.ax.kz = e.x; d.ax.inv_kz = e.y; d.ax.dz_rho = e.z;
+    d.ax.kz = e.x; d.ax.inv_kz = e.y; d.ax.dz_rho = e.z; d.rows = __float_as_int(e.w);
 }
 
 __device__ __forceinline__ void column_footprint(const DevGeom& g, float4 vw, float xc, float yc, Foot& f) {
@@ -245,9 +244,65 @@ __device__ __forceinline__ void column_footprint(const DevGeom& g, float4 vw, fl
 // CTA = (tile of TC channels, view k); NTHR threads = G groups of NTP row-threads.
 // Group gi walks sweep lines gi, gi+G, ...; the footprints of a line's wedge
 // columns are computed group-parallel (one column per thread) into a shared
-// table; then, for each column in channel order, thread r computes the column's
-// axial sum  A(r) = sum_iz x[iz] l_theta(iz) F_t(iz, r)  (z-fastest layout:
-// coalesced) and adds lphi F_s(c) A(r) to a register window over the channels.
+// table; then, for each column, thread r computes the column's axial sum
+//   A(r) = sum_iz x[iz] l_theta(iz) F_t(iz, r)      (z-fastest layout: coalesced)
+// and adds lphi F_s(c) A(r) to its register accumulators of the tile's channels.
+// The column's channel offset is warp-uniform, so a jump table selects a fully
+// static (register-indexed) 8-channel update: no atomics, no shared-memory RMW.
+template <int TC>
+__device__ __forceinline__ void tile_add(float (&acc)[TC], int o, const float (&w)[kMaxFoot], float A) {
+    static_assert(TC <= 32, "offset table covers TC <= 32");
+#define CT_ADD(O)                                                                   \
+    case O:                                                                         \
+        _Pragma("unroll") for (int j = 0; j < kMaxFoot; j++) {                     \
+            if ((O) + j >= 0 && (O) + j < TC) acc[((O) + j >= 0 && (O) + j < TC) ? (O) + j : 0] += w[j] * A; \
+        }                                                                           \
+        break;
+    switch (o) {
+        CT_ADD(-7)
+        CT_ADD(-6)
+        CT_ADD(-5)
+        CT_ADD(-4)
+        CT_ADD(-3)
+        CT_ADD(-2)
+        CT_ADD(-1)
+        CT_ADD(0)
+        CT_ADD(1)
+        CT_ADD(2)
+        CT_ADD(3)
+        CT_ADD(4)
+        CT_ADD(5)
+        CT_ADD(6)
+        CT_ADD(7)
+        CT_ADD(8)
+        CT_ADD(9)
+        CT_ADD(10)
+        CT_ADD(11)
+        CT_ADD(12)
+        CT_ADD(13)
+        CT_ADD(14)
+        CT_ADD(15)
+        CT_ADD(16)
+        CT_ADD(17)
+        CT_ADD(18)
+        CT_ADD(19)
+        CT_ADD(20)
+        CT_ADD(21)
+        CT_ADD(22)
+        CT_ADD(23)
+        CT_ADD(24)
+        CT_ADD(25)
+        CT_ADD(26)
+        CT_ADD(27)
+        CT_ADD(28)
+        CT_ADD(29)
+        CT_ADD(30)
+        CT_ADD(31)
+        default: break;
+    }
+#undef CT_ADD
+}
+
 template <int TC, int NTP, int NTHR, bool RESID>
 __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
                                                         float* __restrict__ out, const float* __restrict__ yobs,
@@ -265,22 +320,21 @@ __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, in
     const bool row_ok = r < g.nt;
     const float qr_off = ((float)r - g.rbase);
     Foot* tab = table + gi * NTP;
+    float acc[TC];
 #pragma unroll
-    for (int c = 0; c < TC; c++) P[gi][c][r] = 0.0f;
+    for (int c = 0; c < TC; c++) acc[c] = 0.0f;
     Wedge w = make_wedge(g, sb, cb, c0, TC);
     const int nz = g.nz;
     for (int L = gi; L < w.nlines; L += G) {
         int lo, hi;
         wedge_line(g, w, L, lo, hi);
         if (lo > hi) continue;
-        Window win;
-        win.reset(-1000000);
         const int n_in = hi - lo + 1;
         for (int cb0 = 0; cb0 < n_in; cb0 += NTP) {
-            // group-parallel footprints of up to NTP columns of this line (channel order)
+            // group-parallel footprints of up to NTP columns of this line
             int q = cb0 + r;
             if (q < n_in) {
-                int u = w.increasing ? lo + q : hi - q;
+                int u = lo + q;
                 int ix = w.rows ? u : L, iy = w.rows ? L : u;
                 Foot f;
                 column_footprint(g, vw, g.x0 + ix * g.dx, g.y0 + iy * g.dy, f);
@@ -293,62 +347,33 @@ __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, in
                 Foot f;
                 load_foot(&tab[j], f);
                 if (f.n <= 0) continue;
-                const int qj = cb0 + j;
-                const int u = w.increasing ? lo + qj : hi - qj;
+                const int u = lo + cb0 + j;
                 const int ix = w.rows ? u : L, iy = w.rows ? L : u;
                 float A = 0.0f;
                 if (row_ok) {
-                    float qr = f.ax.qf + qr_off * f.ax.kz;
+                    const float qr = f.ax.qf + qr_off * f.ax.kz;
                     int iz0, iz1;
                     row_voxels(f.ax, qr, iz0, iz1);
-                    iz0 = max(iz0, 0);
-                    iz1 = min(iz1, nz - 1);
                     const float* xc = x + ((size_t)iy * g.nx + ix) * nz;
-                    for (int iz = iz0; iz <= iz1; iz++)
-                        A += __ldg(&xc[iz]) * ltheta(f.ax, iz) * axial_weight(f.ax, qr, iz);
-                }
-                const int cA = f.cA;
-                if (cA >= win.base) {
-                    while (win.base < cA) {
-                        int cc = win.base - c0;
-                        if (cc >= 0 && cc < TC) P[gi][cc][r] += win.acc[0];
+                    if (iz1 - iz0 <= 2) {
 #pragma unroll
-                        for (int jj = 0; jj < kMaxFoot - 1; jj++) win.acc[jj] = win.acc[jj + 1];
-                        win.acc[kMaxFoot - 1] = 0.0f;
-                        win.base++;
-                        if (win.base < cA - kMaxFoot) {
-                            int jmp = cA - win.base;
-#pragma unroll
-                            for (int jj = 0; jj < kMaxFoot; jj++) {
-                                int c1 = win.base + jj - c0;
-                                if (c1 >= 0 && c1 < TC) P[gi][c1][r] += win.acc[jj];
-                            }
-                            win.reset(win.base + jmp);
+                        for (int t = 0; t < 3; t++) {
+                            const int iz = iz0 + t;
+                            if (iz <= iz1 && iz >= 0 && iz < nz)
+                                A += __ldg(&xc[iz]) * ltheta(f.ax, iz) * axial_weight(f.ax, qr, iz);
                         }
-                    }
-                    if (f.n <= 4) {
-#pragma unroll
-                        for (int jj = 0; jj < 4; jj++) win.acc[jj] += f.w[jj] * A;
                     } else {
-#pragma unroll
-                        for (int jj = 0; jj < kMaxFoot; jj++) win.acc[jj] += f.w[jj] * A;
-                    }
-                } else {
-#pragma unroll
-                    for (int jj = 0; jj < kMaxFoot; jj++) {
-                        int c = cA + jj - c0;
-                        if (jj < f.n && c >= 0 && c < TC) P[gi][c][r] += f.w[jj] * A;
+                        for (int iz = max(iz0, 0); iz <= min(iz1, nz - 1); iz++)
+                            A += __ldg(&xc[iz]) * ltheta(f.ax, iz) * axial_weight(f.ax, qr, iz);
                     }
                 }
+                tile_add<TC>(acc, f.cA - c0, f.w, A);
             }
             asm volatile("bar.sync %0, %1;" ::"r"(gi + 1), "r"(NTP) : "memory");
         }
-#pragma unroll
-        for (int jj = 0; jj < kMaxFoot; jj++) {
-            int c = win.base + jj - c0;
-            if (c >= 0 && c < TC) P[gi][c][r] += win.acc[jj];
-        }
     }
+#pragma unroll
+    for (int c = 0; c < TC; c++) P[gi][c][r] = acc[c];
     __syncthreads();
     // fixed-order sum over groups; thread (c, r) pairs cover the tile, r fastest
     for (int idx = threadIdx.x; idx < TC * NTP; idx += NTHR) {
@@ -446,16 +471,15 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
             foot_range(g, tr, cA, n);
             if (n <= 0) continue;
             TrapCdf F(tr);
-            const float* yk = y + (size_t)k * g.ns;
+            const float* yk = y + (size_t)k * g.ns + cA;
             float e = (float)cA - 0.5f - tr.cc;
             float Fp = F(e), s = 0.0f;
 #pragma unroll
             for (int j = 0; j < kMaxFoot; j++) {
-                if (j < n) {
-                    float Fn = F(e + (float)(j + 1));
-                    s += (Fn - Fp) * __ldg(&yk[cA + j]);
-                    Fp = Fn;
-                }
+                if (j >= n) break;
+                float Fn = F(e + (float)(j + 1));
+                s += (Fn - Fp) * __ldg(&yk[j]);
+                Fp = Fn;
             }
             acc += tr.lphi * s;
         }
@@ -466,33 +490,50 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
 }
 
 // ---------------------------------------------------------------------------
-// K2 (3D cone): voxel-driven back projection; warp = one column x 32 slices
+// K2 (3D cone): voxel-driven back projection; warp = one column x 64 slices
 // ---------------------------------------------------------------------------
-// Block = 4x4 columns (16 warps); lanes walk z, so sinogram reads y[k][c][r..]
-// are unit-stride in r.  Views are processed in batches of 32: lane l computes
-// the column's footprint for view vb + l into the warp's shared table, then the
-// warp walks the batch reading each footprint by broadcast (no recomputation).
+// Block = 4x2 columns (8 warps); lane l owns slices zlo + l and zlo + 32 + l.
+// Views are processed in batches of 32: lane l computes the column's footprint
+// for view vb + l into the warp's shared table.  For each view the warp then
+//  (1) forms the transaxially filtered detector rows of its z-chunk
+//        Q(r) = sum_c lphi F_s(c) y[k][c][r]
+//      (lanes = rows: unit-stride loads, warp-uniform loop over the channels)
+//      and their prefix sums (warp scan), and
+//  (2) for each slice, sum_r F_t(iz, r) Q(r) is the integral of the row-wise
+//      constant Q over the slice's extent on the detector (in row units):
+//      PF(u1) - PF(u0) with PF the piecewise-linear cumulative sum.
 template <int EPI>
-__global__ void __launch_bounds__(512, 2) back3d_kernel(DevGeom g, int first, int stride, int count,
+__global__ void __launch_bounds__(256, 4) back3d_kernel(DevGeom g, int first, int stride, int count,
                                                        const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
-    __shared__ Foot table[16][32];
+    constexpr int kRows = 128;                 // >= nt (validated)
+    __shared__ Foot table[8][32];
+    __shared__ float Qs[8][kRows];
+    __shared__ float Pf[8][kRows + 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ix = blockIdx.x * 4 + (wid & 3);
-    const int iy = blockIdx.y * 4 + (wid >> 2);
-    const int zlo = blockIdx.z * 32;
-    const int iz = zlo + lane;
+    const int iy = blockIdx.y * 2 + (wid >> 2);
+    const int zlo = blockIdx.z * 64;
     const bool colok = ix < g.nx && iy < g.ny;
-    const bool valid = colok && iz < g.nz;
-    const int nt = g.nt, ns = g.ns;
-    const size_t jv = ((size_t)(colok ? iy : 0) * g.nx + (colok ? ix : 0)) * g.nz + (valid ? iz : 0);
-    // voxels outside the support S are not needed by OS-LALM / D_L: skip them (warp-uniformly)
-    const bool act = valid && (ga.mask == nullptr || ga.mask[jv]);
-    const bool warp_act = __ballot_sync(0xffffffffu, act) != 0u;
+    const int nt = g.nt, ns = g.ns, nz = g.nz;
+    const size_t col = (size_t)(colok ? iy : 0) * g.nx + (colok ? ix : 0);
+    bool valid[2], act[2];
+    size_t jv[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int iz = zlo + 32 * h + lane;
+        valid[h] = colok && iz < nz;
+        jv[h] = col * nz + (valid[h] ? iz : 0);
+        // voxels outside the support S are not needed by OS-LALM / D_L
+        act[h] = valid[h] && (ga.mask == nullptr || ga.mask[jv[h]]);
+    }
+    const bool warp_act = __ballot_sync(0xffffffffu, act[0] || act[1]) != 0u;
     Foot* tab = table[wid];
-    float acc = 0.0f;
+    float* Q = Qs[wid];
+    float* PF = Pf[wid];
+    float acc[2] = {0.0f, 0.0f};
     if (warp_act) {
         const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
-        const int zhi = min(g.nz, zlo + 32) - 1;
+        const int zhi = min(nz, zlo + 64) - 1;
         for (int vb = 0; vb < count; vb += 32) {
             const int kk = vb + lane;
             if (kk < count) {
@@ -501,39 +542,63 @@ __global__ void __launch_bounds__(512, 2) back3d_kernel(DevGeom g, int first, in
                 int ra, rb, rc, rd;
                 voxel_rows(f.ax, g, zlo, ra, rb);
                 voxel_rows(f.ax, g, zhi, rc, rd);
-                if (!(rd >= 0 && ra < nt)) f.n = 0;   // the chunk's rows miss the detector
+                ra = max(ra, 0);
+                rd = min(rd, nt - 1);
+                if (!(f.n > 0 && rd >= ra)) f.n = 0;   // the chunk's rows miss the detector
+                f.rows = ra | ((rd - ra + 1) << 16);
                 tab[lane] = f;
             }
             __syncwarp();
             const int nb = min(32, count - vb);
-            if (act) {
-                for (int j = 0; j < nb; j++) {
-                    Foot f;
-                    load_foot(&tab[j], f);
-                    if (f.n <= 0) continue;
-                    int r0, r1;
-                    voxel_rows(f.ax, g, iz, r0, r1);
-                    r0 = max(r0, 0);
-                    r1 = min(r1, nt - 1);
-                    const float* yk = y + ((size_t)(vb + j) * ns + f.cA) * nt;
-                    float s = 0.0f;
-                    for (int r = r0; r <= r1; r++) {
-                        float ft = axial_weight(f.ax, row_center_q(f.ax, g, r), iz);
-                        float t = 0.0f;
-#pragma unroll
-                        for (int c = 0; c < kMaxFoot; c++)
-                            if (c < f.n) t += f.w[c] * __ldg(&yk[(size_t)c * nt + r]);
-                        s += ft * t;
+            for (int j = 0; j < nb; j++) {
+                Foot f;
+                load_foot(&tab[j], f);
+                if (f.n <= 0) continue;
+                const int ra = f.rows & 0xffff, nr = f.rows >> 16;
+                const float* yk = y + ((size_t)(vb + j) * ns + f.cA) * nt + ra;
+                const float* wj = tab[j].w;
+                // (1) filtered rows and their prefix sums (lanes = rows)
+                float carry = 0.0f;
+                for (int p0 = 0; p0 < nr; p0 += 32) {
+                    const int p = p0 + lane;
+                    float q = 0.0f;
+                    if (p < nr) {
+                        for (int c = 0; c < f.n; c++) q += wj[c] * __ldg(&yk[(size_t)c * nt + p]);
+                        Q[p] = q;
                     }
-                    acc += ltheta(f.ax, iz) * s;
+                    float inc = q;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        float t = __shfl_up_sync(0xffffffffu, inc, o);
+                        if (lane >= o) inc += t;
+                    }
+                    if (p < nr) PF[p + 1] = carry + inc;
+                    carry += __shfl_sync(0xffffffffu, inc, 31);
                 }
+                if (lane == 0) PF[0] = 0.0f;
+                __syncwarp();
+                // (2) lanes = slices: integral of the row-wise constant Q over each slice
+                const float fnr = (float)nr;
+                const float ubase = g.rbase + 0.5f - (float)ra;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    if (!act[h]) continue;
+                    const int iz = zlo + 32 * h + lane;
+                    const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
+                    float u0 = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubase), 0.0f), fnr);
+                    float u1 = fminf(fmaxf(fmaf(zi + 1.0f, f.ax.inv_kz, ubase), 0.0f), fnr);
+                    int p0 = min(__float2int_rd(u0), nr - 1), p1 = min(__float2int_rd(u1), nr - 1);
+                    float s0 = PF[p0] + (u0 - (float)p0) * Q[p0];
+                    float s1 = PF[p1] + (u1 - (float)p1) * Q[p1];
+                    acc[h] += ltheta(f.ax, iz) * (s1 - s0);
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
-    double xi = back_epilogue<EPI>(jv, valid, acc, x, ga);
+    double xi = back_epilogue<EPI>(jv[0], valid[0], acc[0], x, ga) + back_epilogue<EPI>(jv[1], valid[1], acc[1], x, ga);
     if (EPI == EPI_GUPD)
-        block_sum_store<512>(xi, &ga.xi_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]);
+        block_sum_store<256>(xi, &ga.xi_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
