@@ -351,18 +351,27 @@ __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, in
                 const int ix = w.rows ? u : L, iy = w.rows ? L : u;
                 float A = 0.0f;
                 if (row_ok) {
-                    const float qr = f.ax.qf + qr_off * f.ax.kz;
-                    int iz0, iz1;
-                    row_voxels(f.ax, qr, iz0, iz1);
                     const float* xc = x + ((size_t)iy * g.nx + ix) * nz;
-                    if (iz1 - iz0 <= 2) {
-#pragma unroll
-                        for (int t = 0; t < 3; t++) {
-                            const int iz = iz0 + t;
-                            if (iz <= iz1 && iz >= 0 && iz < nz)
-                                A += __ldg(&xc[iz]) * ltheta(f.ax, iz) * axial_weight(f.ax, qr, iz);
-                        }
+                    const float qr = f.ax.qf + qr_off * f.ax.kz;   // row centre, voxel units rel. to qi
+                    if (f.ax.kz < 2.0f) {
+                        // the row's extent [lo, hi] meets at most three slices i0, i0+1, i0+2
+                        const float lo = qr - 0.5f * f.ax.kz, hi = qr + 0.5f * f.ax.kz;
+                        const int i0 = __float2int_rd(lo);
+                        const float z0 = (float)i0;
+                        const float o0 = fminf(z0 + 1.0f, hi) - lo;
+                        const float o1 = fminf(fmaxf(hi - (z0 + 1.0f), 0.0f), 1.0f);
+                        const float o2 = fmaxf(hi - (z0 + 2.0f), 0.0f);
+                        const float tz0 = (z0 + 0.5f - f.ax.qf) * f.ax.dz_rho;
+                        const float tz1 = tz0 + f.ax.dz_rho, tz2 = tz1 + f.ax.dz_rho;
+                        const int iz = i0 + f.ax.qi;
+                        const float v0 = (iz >= 0 && iz < nz) ? __ldg(&xc[iz]) : 0.0f;
+                        const float v1 = (iz + 1 >= 0 && iz + 1 < nz && o1 > 0.0f) ? __ldg(&xc[iz + 1]) : 0.0f;
+                        const float v2 = (iz + 2 >= 0 && iz + 2 < nz && o2 > 0.0f) ? __ldg(&xc[iz + 2]) : 0.0f;
+                        A = (v0 * sqrt_approx(fmaf(tz0, tz0, 1.0f)) * o0 + v1 * sqrt_approx(fmaf(tz1, tz1, 1.0f)) * o1 +
+                             v2 * sqrt_approx(fmaf(tz2, tz2, 1.0f)) * o2) * f.ax.inv_kz;
                     } else {
+                        int iz0, iz1;
+                        row_voxels(f.ax, qr, iz0, iz1);
                         for (int iz = max(iz0, 0); iz <= min(iz1, nz - 1); iz++)
                             A += __ldg(&xc[iz]) * ltheta(f.ax, iz) * axial_weight(f.ax, qr, iz);
                     }
@@ -503,7 +512,7 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
 //      constant Q over the slice's extent on the detector (in row units):
 //      PF(u1) - PF(u0) with PF the piecewise-linear cumulative sum.
 template <int EPI>
-__global__ void __launch_bounds__(256, 4) back3d_kernel(DevGeom g, int first, int stride, int count,
+__global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, int stride, int count,
                                                        const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     constexpr int kRows = 128;                 // >= nt (validated)
     __shared__ Foot table[8][32];
@@ -555,17 +564,29 @@ __global__ void __launch_bounds__(256, 4) back3d_kernel(DevGeom g, int first, in
                 load_foot(&tab[j], f);
                 if (f.n <= 0) continue;
                 const int ra = f.rows & 0xffff, nr = f.rows >> 16;
-                const float* yk = y + ((size_t)(vb + j) * ns + f.cA) * nt + ra;
-                const float* wj = tab[j].w;
+                const float* yv = y + (size_t)(vb + j) * ns * nt;     // this view's sinogram
+                const int off0 = f.cA * nt + ra;                        // 32-bit offsets below
                 // (1) filtered rows and their prefix sums (lanes = rows)
                 float carry = 0.0f;
                 for (int p0 = 0; p0 < nr; p0 += 32) {
                     const int p = p0 + lane;
-                    float q = 0.0f;
-                    if (p < nr) {
-                        for (int c = 0; c < f.n; c++) q += wj[c] * __ldg(&yk[(size_t)c * nt + p]);
-                        Q[p] = q;
+                    const bool inr = p < nr;
+                    const float* yr = yv + (off0 + (inr ? p : 0));
+                    float q;
+                    if (f.n <= 4) {   // warp-uniform: issue all loads first, then the FMAs
+                        float v[4];
+#pragma unroll
+                        for (int c = 0; c < 4; c++) v[c] = (inr && c < f.n) ? __ldg(yr + c * nt) : 0.0f;
+                        q = f.w[0] * v[0] + f.w[1] * v[1] + f.w[2] * v[2] + f.w[3] * v[3];
+                    } else {
+                        float v[kMaxFoot];
+#pragma unroll
+                        for (int c = 0; c < kMaxFoot; c++) v[c] = (inr && c < f.n) ? __ldg(yr + c * nt) : 0.0f;
+                        q = 0.0f;
+#pragma unroll
+                        for (int c = 0; c < kMaxFoot; c++) q += f.w[c] * v[c];
                     }
+                    if (inr) Q[p] = q;
                     float inc = q;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
