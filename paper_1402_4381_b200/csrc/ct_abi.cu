@@ -49,7 +49,7 @@ static int fail(int code, const char* fmt, ...) {
 extern "C" const char* ct_last_error(void) { return g_err; }
 extern "C" unsigned long long ct_kernel_launches(void) { return g_launches.load(); }
 extern "C" const char* ct_build_info(void) {
-    return "ct_oslalm sm_100a: fwd2d fwd3d back2d back3d sqs_update reg_grad gupd xi_finalize count_vv";
+    return "ct_oslalm sm_100a: fwd2d fwd3d back2d back3d (fused g-update + xi/rho finalize) sqs_update reg_grad gupd count_vv";
 }
 
 // ---------------------------------------------------------------------------
@@ -126,6 +126,8 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     if (fabs(d->dx - d->dy) > 1e-9 * d->dx) return fail(CT_EINVAL, "dx must equal dy (square voxels)");
     if (!is2d && nt > 128) return fail(CT_EUNSUPPORTED, "nt = %d > 128 detector rows", nt);
     if (d->kind == CT_CONE_HELICAL && !(d->pitch > 0)) return fail(CT_EINVAL, "helical geometry needs pitch > 0");
+    if ((double)d->nx * d->ny * nz >= 2147483647.0 || (double)d->na * d->ns * nt >= 2147483647.0)
+        return fail(CT_EUNSUPPORTED, "image or sinogram has >= 2^31 elements (32-bit kernel indexing)");
     // footprint width bound: voxel half-diagonal magnified at the closest approach
     double hx = 0.5 * (d->nx - 1) * d->dx + fabs(d->offx) + d->dx, hy = 0.5 * (d->ny - 1) * d->dy + fabs(d->offy) + d->dy;
     double rmax = sqrt(hx * hx + hy * hy);
@@ -394,6 +396,7 @@ struct ct_oslalm_state {
     double* dlog;        // M x 3 doubles (per iteration)
     int curG = 0;
     int initialised = 0;
+    int log_slot = -1;
     cudaStream_t cap = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     GraphEntry graphs[2];
@@ -588,6 +591,7 @@ static int allreduce(const ct_geom* g, float* buf, size_t n, cudaStream_t st) {
 
 // G+ = M A_m'(W (A_m x - y)) for subset m with the requested epilogue.
 static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const float* x, int m, int epi, cudaStream_t st) {
+    // the fused K4 logs into slot s->log_slot (set by the caller)
     const ct_geom* g = s->g;
     int M = s->cfg.M;
     ct_views v = rank_views(g, M, m);
@@ -599,6 +603,12 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
     ga.rho = &s->sc->rho;
     ga.xi_part = s->xi_part;
     ga.gs = s->gs;
+    ga.sc = s->sc;
+    ga.mode = s->cfg.mode;
+    ga.rho_fixed = s->cfg.rho_fixed;
+    ga.rho_min = s->cfg.rho_min;
+    ga.log3 = s->dlog;
+    ga.log_slot = s->log_slot;
     if (g->nranks == 1) {
         if (epi == EPI_INIT) {
             ga.G_new = s->Gbuf[s->curG];
@@ -630,10 +640,6 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
     return CT_OK;
 }
 
-static int nparts_for_gupd(const ct_oslalm_state* s) {
-    return (int)(s->g->nranks == 1 ? back_nblocks(s->g) : nblk(s->N));
-}
-
 // Enqueue one outer iteration (M inner steps) on stream st.  x is updated in place.
 static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float* x, cudaStream_t st, int* nk) {
     const ct_geom* g = s->g;
@@ -649,19 +655,16 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
             sqs_update_kernel<8><<<nblk(s->N), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
                                                               &s->sc->rho, (float)c.reg.beta, inv_d, s->N);
         else
-            sqs_update_kernel<26><<<nblk(s->N), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
-                                                               &s->sc->rho, (float)c.reg.beta, inv_d, s->N);
+            sqs_update3d_kernel<<<dim3((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (g->dg.ny + kK3Y - 1) / kK3Y), 256, 0, st>>>(
+                g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask, &s->sc->rho, (float)c.reg.beta, inv_d);
         CT_LAUNCHED(1);
         tmark_end(s, st, 0, t0);
         std::swap(xa, xb);
+        s->log_slot = j;
         if (int e = subset_gradient(s, d, xa, s->order[(j + 1) % M], EPI_GUPD, st)) return e;
+        s->log_slot = -1;
         s->curG ^= 1;
-        int t3 = tmark(s, st);
-        xi_finalize_kernel<<<1, 256, 0, st>>>(s->xi_part, nparts_for_gupd(s), s->sc, c.mode, c.rho_fixed, c.rho_min,
-                                              s->dlog, j);
-        CT_LAUNCHED(1);
-        tmark_end(s, st, 3, t3);
-        kernels += 4 + (g->nranks > 1 ? 1 : 0);
+        kernels += 3 + (g->nranks > 1 ? 1 : 0);
     }
     if (xa != x) {
         CT_CUDA(cudaMemcpyAsync(x, xa, s->N * 4, cudaMemcpyDeviceToDevice, st));

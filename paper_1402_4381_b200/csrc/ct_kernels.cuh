@@ -412,6 +412,23 @@ constexpr size_t fwd3d_smem() {
 // ---------------------------------------------------------------------------
 enum BackEpi { EPI_STORE = 0, EPI_ACCUM = 1, EPI_GUPD = 2, EPI_INIT = 3 };
 
+struct Scalars {
+    double rho;        // rho for the next inner step
+    long long l;       // continuation counter
+    long long step;    // inner steps taken
+    unsigned int arrive;   // blocks of the current back-projection that have stored their xi partial
+    int pad;
+};
+
+__device__ __forceinline__ double rho_l(long long l, double rho_min) {
+    // P:507-515: rho_0 = 1; rho_l = max{ pi/(l+1) sqrt(1 - (pi/(2l+2))^2), rho_min }
+    if (l == 0) return 1.0;
+    const double pi = 3.14159265358979323846;
+    double a = pi / (double)(l + 1), b = pi / (2.0 * (double)l + 2.0);
+    double r = a * sqrt(1.0 - b * b);
+    return r > rho_min ? r : rho_min;
+}
+
 struct GupdArgs {
     float* G_new;          // G+  (EPI_GUPD) / G (EPI_INIT)
     const float* G_old;    // G   (EPI_GUPD)
@@ -419,7 +436,63 @@ struct GupdArgs {
     const uint8_t* mask;   // support S
     const double* rho;     // rho of this inner step (device scalar)
     double* xi_part;       // per-block fp64 partials of xi
+    // K4 fused: the last block to finish sums the partials in fixed order and
+    // applies the restart rule / rho_l update
+    Scalars* sc;
+    int mode;
+    double rho_fixed, rho_min;
+    double* log3;
+    int log_slot;
 };
+
+// xi = fixed-order fp64 sum of the partials; l <- (xi > 0) ? 0 : l + 1; rho <- rho_l.
+template <int NTHR>
+__device__ void xi_finalize_block(const double* part, int nparts, const GupdArgs& ga) {
+    __shared__ double red[NTHR];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += NTHR) s += __ldcg(&part[i]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = NTHR / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        Scalars* sc = ga.sc;
+        double xi = red[0];
+        int restart = xi > 0.0;
+        double rho_used = sc->rho;
+        if (ga.mode == 1) {
+            sc->l = restart ? 0 : sc->l + 1;
+            sc->rho = rho_l(sc->l, ga.rho_min);
+        } else {
+            sc->rho = ga.rho_fixed;
+        }
+        sc->step += 1;
+        if (ga.log3 && ga.log_slot >= 0) {
+            ga.log3[3 * ga.log_slot + 0] = rho_used;
+            ga.log3[3 * ga.log_slot + 1] = xi;
+            ga.log3[3 * ga.log_slot + 2] = restart;
+        }
+        sc->arrive = 0;   // ready for the next launch (stream order)
+    }
+}
+
+// Called by every block after its partial is stored: the last arriving block finalises.
+template <int NTHR>
+__device__ __forceinline__ void xi_arrive(const GupdArgs& ga, int nblocks) {
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned prev = atomicAdd(&ga.sc->arrive, 1u);
+        last = (prev == (unsigned)nblocks - 1u);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        xi_finalize_block<NTHR>(ga.xi_part, nblocks, ga);
+    }
+}
 
 template <int NTHR>
 __device__ __forceinline__ void block_sum_store(double val, double* dst) {
@@ -495,7 +568,10 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
     }
     size_t j = (size_t)iy * g.nx + ix;
     double xi = back_epilogue<EPI>(j, valid, acc, x, ga);
-    if (EPI == EPI_GUPD) block_sum_store<256>(xi, &ga.xi_part[blockIdx.y * gridDim.x + blockIdx.x]);
+    if (EPI == EPI_GUPD) {
+        block_sum_store<256>(xi, &ga.xi_part[blockIdx.y * gridDim.x + blockIdx.x]);
+        xi_arrive<256>(ga, gridDim.x * gridDim.y);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -618,8 +694,10 @@ __global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, in
         }
     }
     double xi = back_epilogue<EPI>(jv[0], valid[0], acc[0], x, ga) + back_epilogue<EPI>(jv[1], valid[1], acc[1], x, ga);
-    if (EPI == EPI_GUPD)
+    if (EPI == EPI_GUPD) {
         block_sum_store<256>(xi, &ga.xi_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]);
+        xi_arrive<256>(ga, gridDim.x * gridDim.y * gridDim.z);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -680,6 +758,79 @@ __global__ void __launch_bounds__(256) sqs_update_kernel(DevGeom g, const float*
     xn[j] = fmaxf(v, 0.0f);
 }
 
+// 3D (26-neighbour) K3 with shared-memory planes: block = 8 (ix) x 32 (z) voxels
+// marching along iy; three planes of x (with a one-voxel halo) rotate through
+// shared memory, voxels outside S (or outside the grid) are stored as NaN so the
+// "both voxels in S" pair rule is one comparison and the stencil needs no bounds
+// checks.  Streams G, g, D_L once and writes x' once (21 B/voxel of HBM).
+constexpr int kK3Y = 8;
+
+__global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
+                                                          const float* __restrict__ G, const float* __restrict__ gs,
+                                                          const float* __restrict__ dl, const uint8_t* __restrict__ m,
+                                                          const double* __restrict__ rho_p, float beta, float inv_delta) {
+    __shared__ float Pl[3][10][34];
+    const int tz = threadIdx.x & 31, tx = threadIdx.x >> 5;
+    const int ix0 = blockIdx.x * 8, z0 = blockIdx.y * 32, iy0 = blockIdx.z * kK3Y;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    const float rho = (float)*rho_p;
+    auto load_plane = [&](int slot, int iy) {
+        for (int e = threadIdx.x; e < 340; e += 256) {
+            const int a = e / 34, b = e - a * 34;
+            const int ix = ix0 - 1 + a, iz = z0 - 1 + b;
+            float v = __int_as_float(0x7fc00000);   // NaN: not in S
+            if (iy >= 0 && iy < ny && ix >= 0 && ix < nx && iz >= 0 && iz < nz) {
+                const int j = (iy * nx + ix) * nz + iz;
+                if (__ldg(&m[j])) v = __ldg(&x[j]);
+            }
+            Pl[slot][a][b] = v;
+        }
+    };
+    load_plane(0, iy0 - 1);
+    load_plane(1, iy0);
+    const int ix = ix0 + tx, iz = z0 + tz;
+    const bool inb = ix < nx && iz < nz;
+    constexpr float r2 = 0.70710678118654752f, r3 = 0.57735026918962576f;
+    for (int t = 0; t < kK3Y; t++) {
+        const int iy = iy0 + t;
+        if (iy >= ny) break;
+        load_plane((t + 2) % 3, iy + 1);
+        __syncthreads();
+        if (inb) {
+            const int j = (iy * nx + ix) * nz + iz;
+            const float xj = Pl[(t + 1) % 3][tx + 1][tz + 1];
+            if (xj != xj) {
+                xn[j] = 0.0f;   // off S
+            } else {
+                float gr = 0.0f, cu = 0.0f;
+#pragma unroll
+                for (int oy = -1; oy <= 1; oy++) {
+                    const int sl = (t + 1 + oy + 3) % 3;
+#pragma unroll
+                    for (int ox = -1; ox <= 1; ox++)
+#pragma unroll
+                        for (int oz = -1; oz <= 1; oz++) {
+                            if (oy == 0 && ox == 0 && oz == 0) continue;
+                            const int d2 = oy * oy + ox * ox + oz * oz;
+                            const float wgt = d2 == 1 ? 1.0f : (d2 == 2 ? r2 : r3);
+                            const float xk = Pl[sl][tx + 1 + ox][tz + 1 + oz];
+                            if (xk == xk) {
+                                float dpsi, om;
+                                fair(xj - xk, inv_delta, dpsi, om);
+                                gr += wgt * dpsi;
+                                cu += wgt * om;
+                            }
+                        }
+                }
+                const float sdir = rho * __ldg(&G[j]) + (1.0f - rho) * __ldg(&gs[j]);
+                const float den = rho * __ldg(&dl[j]) + 2.0f * beta * cu;
+                xn[j] = fmaxf(xj - (sdir + beta * gr) / den, 0.0f);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 template <int NBR>
 __global__ void __launch_bounds__(256) reg_grad_kernel(DevGeom g, const float* __restrict__ x, const uint8_t* __restrict__ m,
                                                       float* __restrict__ grad, float* __restrict__ curv, float beta,
@@ -712,61 +863,17 @@ __global__ void __launch_bounds__(256) gupd_kernel(const float* __restrict__ Gp,
         if (ga.mask[j]) xi = (double)(gg - P) * (double)(P - G);
     }
     block_sum_store<256>(xi, &ga.xi_part[blockIdx.x]);
+    xi_arrive<256>(ga, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
 // K4: xi = fixed-order fp64 sum of block partials; restart rule; rho_l
 // ---------------------------------------------------------------------------
-struct Scalars {
-    double rho;        // rho for the next inner step
-    long long l;       // continuation counter
-    long long step;    // inner steps taken
-};
-
-__device__ __forceinline__ double rho_l(long long l, double rho_min) {
-    // P:507-515: rho_0 = 1; rho_l = max{ pi/(l+1) sqrt(1 - (pi/(2l+2))^2), rho_min }
-    if (l == 0) return 1.0;
-    const double pi = 3.14159265358979323846;
-    double a = pi / (double)(l + 1), b = pi / (2.0 * (double)l + 2.0);
-    double r = a * sqrt(1.0 - b * b);
-    return r > rho_min ? r : rho_min;
-}
-
-__global__ void __launch_bounds__(256) xi_finalize_kernel(const double* __restrict__ part, int nparts, Scalars* sc,
-                                                         int mode, double rho_fixed, double rho_min,
-                                                         double* __restrict__ log3, int log_slot) {
-    __shared__ double red[256];
-    double s = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += 256) s += part[i];
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        double xi = red[0];
-        int restart = xi > 0.0;
-        double rho_used = sc->rho;
-        if (mode == 1) {
-            sc->l = restart ? 0 : sc->l + 1;
-            sc->rho = rho_l(sc->l, rho_min);
-        } else {
-            sc->rho = rho_fixed;
-        }
-        sc->step += 1;
-        if (log3 && log_slot >= 0) {
-            log3[3 * log_slot + 0] = rho_used;
-            log3[3 * log_slot + 1] = xi;
-            log3[3 * log_slot + 2] = restart;
-        }
-    }
-}
-
 __global__ void init_scalars_kernel(Scalars* sc, double rho0) {
     sc->rho = rho0;
     sc->l = 0;
     sc->step = 0;
+    sc->arrive = 0;
 }
 
 // ---------------------------------------------------------------------------
