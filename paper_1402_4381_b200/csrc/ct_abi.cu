@@ -157,6 +157,17 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     dg.cbase = (float)((d->ns - 1) / 2.0 + d->offs);
     dg.rbase = (float)((nt - 1) / 2.0 + d->offt);
     dg.dt = is2d ? 1.0f : (float)d->dt;
+    {
+        // helical: z_s(v) = zs0 + v * dzs; the largest z half-coverage of the detector
+        // (at the smallest magnification, rho_max = dso + rmax) bounds the views a z-chunk needs
+        double turns_ = d->orbit_deg / 360.0;
+        double h_ = d->kind == CT_CONE_HELICAL ? d->pitch * nt * d->dt * d->dso / d->dsd : 0.0;
+        double dzs = d->kind == CT_CONE_HELICAL ? h_ / (d->na / turns_) : 0.0;
+        dg.zs0 = (float)(-(d->na - 1) / 2.0 * dzs);
+        dg.dzs = (float)dzs;
+        dg.zhalf = (float)((0.5 * nt * (is2d ? 1.0 : d->dt) + 0.5 * fabs(d->offt) * (is2d ? 1.0 : d->dt)) *
+                           (d->dso + rmax) / d->dsd + (is2d ? 0.0 : d->dz));
+    }
 
     std::vector<float4> hv(d->na);
     std::vector<double2> hvz(d->na);
@@ -239,7 +250,7 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         fwd2d_kernel<TC, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
     } else {
-        constexpr int TC = 32;
+        constexpr int TC = 16;
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32)
             launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, st);

@@ -32,6 +32,8 @@ struct DevGeom {
     float cbase;              // channel coordinate of fan angle 0: (ns-1)/2 + offs
     float rbase;              // row coordinate of t = 0: (nt-1)/2 + offt
     float dt;
+    float zs0, dzs;           // helical source height z_s(v) = zs0 + v dzs (dzs = 0: axial)
+    float zhalf;              // bound on |z - z_s| of any voxel a view can see (mm)
     const float4* views;      // per view: (sin beta, cos beta, qi, qf) with
                               // (z_s - zb0)/dz = qi + qf, qi integer (exact in fp32)
 };

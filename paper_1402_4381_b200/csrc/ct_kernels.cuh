@@ -303,6 +303,45 @@ __device__ __forceinline__ void tile_add(float (&acc)[TC], int o, const float (&
 #undef CT_ADD
 }
 
+// Axial sum of one column for detector row r (forward projector):
+//   A(r) = sum_iz x[iz] l_theta(iz) F_t(iz, r),  F_t = overlap / kz.
+// Table fields (set in the footprint phase): ax.qf = lower edge of row 0's extent
+// (voxel units relative to qi), rows = 32-bit index of (column, iz = qi).
+// Fast form for kz < 2 (a row meets at most three slices), predicated loads only.
+__device__ __forceinline__ float fwd_axial3(const Foot& f, const float* __restrict__ x, int r, int nz, float rbase) {
+    if (f.n <= 0) return 0.0f;
+    const float lo = fmaf((float)r, f.ax.kz, f.ax.qf);
+    const float hi = lo + f.ax.kz;
+    const int i0 = __float2int_rd(lo);
+    const float z0 = (float)i0;
+    const float o0 = fminf(z0 + 1.0f, hi) - lo;
+    const float o1 = fminf(fmaxf(hi - (z0 + 1.0f), 0.0f), 1.0f);
+    const float o2 = fmaxf(hi - (z0 + 2.0f), 0.0f);
+    const float qf = f.ax.qf + (0.5f + rbase) * f.ax.kz;
+    const float tz0 = (z0 + 0.5f - qf) * f.ax.dz_rho;
+    const float tz1 = tz0 + f.ax.dz_rho, tz2 = tz1 + f.ax.dz_rho;
+    const int iz = i0 + f.ax.qi;
+    const int idx = f.rows + i0;
+    const float v0 = ((unsigned)iz < (unsigned)nz) ? __ldg(x + idx) : 0.0f;
+    const float v1 = ((unsigned)(iz + 1) < (unsigned)nz && o1 > 0.0f) ? __ldg(x + idx + 1) : 0.0f;
+    const float v2 = ((unsigned)(iz + 2) < (unsigned)nz && o2 > 0.0f) ? __ldg(x + idx + 2) : 0.0f;
+    return (v0 * sqrt_approx(fmaf(tz0, tz0, 1.0f)) * o0 + v1 * sqrt_approx(fmaf(tz1, tz1, 1.0f)) * o1 +
+            v2 * sqrt_approx(fmaf(tz2, tz2, 1.0f)) * o2) * f.ax.inv_kz;
+}
+
+__device__ __forceinline__ float fwd_axial_any(const Foot& f, const float* __restrict__ x, int r, int nz, float rbase) {
+    if (f.n <= 0) return 0.0f;
+    Axial ax = f.ax;
+    ax.qf = f.ax.qf + (0.5f + rbase) * f.ax.kz;
+    const float qr = fmaf((float)r, f.ax.kz, f.ax.qf) + 0.5f * f.ax.kz;
+    int iz0, iz1;
+    row_voxels(ax, qr, iz0, iz1);
+    const float* xc = x + (f.rows - f.ax.qi);
+    float A = 0.0f;
+    for (int iz = max(iz0, 0); iz <= min(iz1, nz - 1); iz++) A += __ldg(&xc[iz]) * ltheta(ax, iz) * axial_weight(ax, qr, iz);
+    return A;
+}
+
 template <int TC, int NTP, int NTHR, bool RESID>
 __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
                                                         float* __restrict__ out, const float* __restrict__ yobs,
@@ -339,44 +378,31 @@ __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, in
                 Foot f;
                 column_footprint(g, vw, g.x0 + ix * g.dx, g.y0 + iy * g.dy, f);
                 if (!(f.n > 0 && f.cA + f.n > c0 && f.cA < c0 + TC)) f.n = 0;   // misses the tile
+                // forward-projector table: qf -> lower edge of row 0's extent; rows -> 32-bit column base
+                f.ax.qf = f.ax.qf - 0.5f * f.ax.kz - g.rbase * f.ax.kz;
+                f.rows = (iy * g.nx + ix) * nz + f.ax.qi;
                 tab[r] = f;
             }
             asm volatile("bar.sync %0, %1;" ::"r"(gi + 1), "r"(NTP) : "memory");
             const int nq = min(NTP, n_in - cb0);
-            for (int j = 0; j < nq; j++) {
-                Foot f;
-                load_foot(&tab[j], f);
-                if (f.n <= 0) continue;
-                const int u = lo + cb0 + j;
-                const int ix = w.rows ? u : L, iy = w.rows ? L : u;
-                float A = 0.0f;
+            // two columns per step: both columns' loads are in flight before either's FMAs
+            for (int j = 0; j < nq; j += 2) {
+                Foot f0, f1;
+                load_foot(&tab[j], f0);
+                if (j + 1 < nq) load_foot(&tab[j + 1], f1); else f1.n = 0;
+                if (f0.n <= 0 && f1.n <= 0) continue;
+                float A0 = 0.0f, A1 = 0.0f;
                 if (row_ok) {
-                    const float* xc = x + ((size_t)iy * g.nx + ix) * nz;
-                    const float qr = f.ax.qf + qr_off * f.ax.kz;   // row centre, voxel units rel. to qi
-                    if (f.ax.kz < 2.0f) {
-                        // the row's extent [lo, hi] meets at most three slices i0, i0+1, i0+2
-                        const float lo = qr - 0.5f * f.ax.kz, hi = qr + 0.5f * f.ax.kz;
-                        const int i0 = __float2int_rd(lo);
-                        const float z0 = (float)i0;
-                        const float o0 = fminf(z0 + 1.0f, hi) - lo;
-                        const float o1 = fminf(fmaxf(hi - (z0 + 1.0f), 0.0f), 1.0f);
-                        const float o2 = fmaxf(hi - (z0 + 2.0f), 0.0f);
-                        const float tz0 = (z0 + 0.5f - f.ax.qf) * f.ax.dz_rho;
-                        const float tz1 = tz0 + f.ax.dz_rho, tz2 = tz1 + f.ax.dz_rho;
-                        const int iz = i0 + f.ax.qi;
-                        const float v0 = (iz >= 0 && iz < nz) ? __ldg(&xc[iz]) : 0.0f;
-                        const float v1 = (iz + 1 >= 0 && iz + 1 < nz && o1 > 0.0f) ? __ldg(&xc[iz + 1]) : 0.0f;
-                        const float v2 = (iz + 2 >= 0 && iz + 2 < nz && o2 > 0.0f) ? __ldg(&xc[iz + 2]) : 0.0f;
-                        A = (v0 * sqrt_approx(fmaf(tz0, tz0, 1.0f)) * o0 + v1 * sqrt_approx(fmaf(tz1, tz1, 1.0f)) * o1 +
-                             v2 * sqrt_approx(fmaf(tz2, tz2, 1.0f)) * o2) * f.ax.inv_kz;
+                    if (f0.ax.kz < 2.0f && f1.ax.kz < 2.0f) {
+                        A0 = fwd_axial3(f0, x, r, nz, g.rbase);
+                        A1 = fwd_axial3(f1, x, r, nz, g.rbase);
                     } else {
-                        int iz0, iz1;
-                        row_voxels(f.ax, qr, iz0, iz1);
-                        for (int iz = max(iz0, 0); iz <= min(iz1, nz - 1); iz++)
-                            A += __ldg(&xc[iz]) * ltheta(f.ax, iz) * axial_weight(f.ax, qr, iz);
+                        A0 = fwd_axial_any(f0, x, r, nz, g.rbase);
+                        A1 = fwd_axial_any(f1, x, r, nz, g.rbase);
                     }
                 }
-                tile_add<TC>(acc, f.cA - c0, f.w, A);
+                if (f0.n > 0) tile_add<TC>(acc, f0.cA - c0, f0.w, A0);
+                if (f1.n > 0) tile_add<TC>(acc, f1.cA - c0, f1.w, A1);
             }
             asm volatile("bar.sync %0, %1;" ::"r"(gi + 1), "r"(NTP) : "memory");
         }
@@ -619,9 +645,18 @@ __global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, in
     if (warp_act) {
         const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
         const int zhi = min(nz, zlo + 64) - 1;
-        for (int vb = 0; vb < count; vb += 32) {
+        // helical: only the views whose source is within zhalf of the chunk can reach it
+        int k_lo = 0, k_hi = count - 1;
+        if (g.dzs != 0.0f) {
+            const float za = g.zb0 + zlo * g.dz - g.zhalf, zb = g.zb0 + (zhi + 1) * g.dz + g.zhalf;
+            float va = (za - g.zs0) / g.dzs, vbnd = (zb - g.zs0) / g.dzs;
+            if (va > vbnd) { float t = va; va = vbnd; vbnd = t; }
+            k_lo = max(0, (int)floorf((va - first) / stride) - 1);
+            k_hi = min(count - 1, (int)ceilf((vbnd - first) / stride) + 1);
+        }
+        for (int vb = k_lo; vb <= k_hi; vb += 32) {
             const int kk = vb + lane;
-            if (kk < count) {
+            if (kk <= k_hi) {
                 Foot f;
                 column_footprint(g, g.views[first + kk * stride], xc, yc, f);
                 int ra, rb, rc, rd;
@@ -634,7 +669,7 @@ __global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, in
                 tab[lane] = f;
             }
             __syncwarp();
-            const int nb = min(32, count - vb);
+            const int nb = min(32, k_hi + 1 - vb);
             for (int j = 0; j < nb; j++) {
                 Foot f;
                 load_foot(&tab[j], f);

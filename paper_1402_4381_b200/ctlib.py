@@ -17,7 +17,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libct_oslalm.so")
+LIB_PATH = os.environ.get("CT_OSLALM_LIB", os.path.join(_HERE, "libct_oslalm.so"))   # override: tuning experiments only
 
 CT_FAN2D, CT_CONE_AXIAL, CT_CONE_HELICAL = 0, 1, 2
 KIND = {"fan2d": CT_FAN2D, "cone_axial": CT_CONE_AXIAL, "cone_helical": CT_CONE_HELICAL}
