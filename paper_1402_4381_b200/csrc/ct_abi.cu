@@ -620,7 +620,7 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
     ga.rho_min = s->cfg.rho_min;
     ga.log3 = s->dlog;
     ga.log_slot = s->log_slot;
-    if (g->nranks == 1) {
+    if (g->comm == nullptr) {   // single GPU: fused epilogue
         if (epi == EPI_INIT) {
             ga.G_new = s->Gbuf[s->curG];
             return launch_back<EPI_INIT>(g, v, s->sino, nullptr, ga, st);
@@ -675,7 +675,7 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
         if (int e = subset_gradient(s, d, xa, s->order[(j + 1) % M], EPI_GUPD, st)) return e;
         s->log_slot = -1;
         s->curG ^= 1;
-        kernels += 3 + (g->nranks > 1 ? 1 : 0);
+        kernels += 3 + (g->comm ? 1 : 0);
     }
     if (xa != x) {
         CT_CUDA(cudaMemcpyAsync(x, xa, s->N * 4, cudaMemcpyDeviceToDevice, st));
@@ -721,7 +721,7 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
     DeviceGuard guard(g->d.device);
     cudaStream_t st = (cudaStream_t)stream;
     if (int e = ensure_initialised(s, d, x, st)) return e;
-    if (g->nranks > 1 || s->timing) {
+    if (g->comm || s->timing) {
         if (int e = enqueue_iteration(s, d, x, st, nullptr)) return e;
         return tcollect(s);
     }
@@ -806,12 +806,14 @@ extern "C" int ct_comm_get_unique_id(void* uid) {
 extern "C" int ct_comm_init(ct_geom* g, int rank, int nranks, const void* uid) {
     if (!g || !uid) return fail(CT_EINVAL, "ct_comm_init: null argument");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CT_EINVAL, "bad rank %d of %d", rank, nranks);
-    if (nranks == 1) {
-        g->rank = 0;
-        g->nranks = 1;
-        return CT_OK;
-    }
+    // nranks == 1 still creates a (trivial) communicator: the exchange path (partial
+    // back-projection, all-reduce, unfused g-update) then runs on one GPU, which is
+    // how the multi-GPU code path is exercised when only one GPU is available.
     if (!load_nccl()) return fail(CT_ENCCL, "libnccl.so.2 not loadable");
+    if (g->comm) {
+        g_nccl.CommDestroy(g->comm);
+        g->comm = nullptr;
+    }
     DeviceGuard guard(g->d.device);
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));

@@ -131,6 +131,21 @@ struct TrapCdf {
     }
 };
 
+// Footprint bins with end information: if the first (last) bin is not clamped by
+// the detector edge, its left (right) edge lies outside (t0, t3), so F there is
+// exactly 0 (total) and needs no evaluation.
+__device__ __forceinline__ void foot_range_ends(const DevGeom& g, const Trans& tr, int& cA, int& n, bool& clampL,
+                                                bool& clampR) {
+    int a = __float2int_rd(tr.cc + tr.t0 + 0.5f);
+    int b = __float2int_rd(tr.cc + tr.t3 + 0.5f);
+    clampL = a < 0;
+    clampR = b > g.ns - 1;
+    a = max(a, 0);
+    b = min(b, g.ns - 1);
+    cA = a;
+    n = b - a + 1;
+}
+
 // First channel of the footprint and number of channels (clamped to the detector).
 __device__ __forceinline__ void foot_range(const DevGeom& g, const Trans& tr, int& cA, int& n) {
     int a = __float2int_rd(tr.cc + tr.t0 + 0.5f);

@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(NTHR) fwd2d_kernel(DevGeom g, int first, int s
             Trans tr;
             transaxial(g, sb, cb, g.x0 + ix * g.dx, g.y0 + iy * g.dy, tr);
             int cA, n;
-            foot_range(g, tr, cA, n);
+            bool clL, clR;
+            foot_range_ends(g, tr, cA, n, clL, clR);
             if (n <= 0 || cA + n <= c0 || cA >= c0 + TC) continue;
             TrapCdf F(tr);
             float lx = tr.lphi * xv;
@@ -157,12 +158,14 @@ __global__ void __launch_bounds__(NTHR) fwd2d_kernel(DevGeom g, int first, int s
                         win.reset(win.base + jmp);
                     }
                 }
-                float e = (float)cA - 0.5f - tr.cc;
-                float Fp = F(e);
+                const float e = (float)cA - 0.5f - tr.cc;
+                // interior bin edges only: F = 0 left of t0 and F = total right of t3
+                float Fp = clL ? F(e) : 0.0f;
+                const float Fend = clR ? F(e + (float)n) : 0.5f * (tr.t3 + tr.t2 - tr.t1 - tr.t0);
 #pragma unroll
                 for (int j = 0; j < kMaxFoot; j++) {
                     if (j >= n) break;
-                    float Fn = F(e + (float)(j + 1));
+                    const float Fn = (j + 1 < n) ? F(e + (float)(j + 1)) : Fend;
                     win.acc[j] += lx * (Fn - Fp);
                     Fp = Fn;
                 }
@@ -576,19 +579,23 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
             Trans tr;
             transaxial(g, vw.x, vw.y, xc, yc, tr);
             int cA, n;
-            foot_range(g, tr, cA, n);
+            bool clL, clR;
+            foot_range_ends(g, tr, cA, n, clL, clR);
             if (n <= 0) continue;
             TrapCdf F(tr);
-            const float* yk = y + (size_t)k * g.ns + cA;
-            float e = (float)cA - 0.5f - tr.cc;
-            float Fp = F(e), s = 0.0f;
+            const float* yk = y + k * g.ns + cA;
+            const float e = (float)cA - 0.5f - tr.cc;
+            // interior bin edges only: F = 0 left of t0 and F = total right of t3
+            float Fp = clL ? F(e) : 0.0f, s = 0.0f;
 #pragma unroll
-            for (int j = 0; j < kMaxFoot; j++) {
-                if (j >= n) break;
-                float Fn = F(e + (float)(j + 1));
+            for (int j = 0; j < kMaxFoot - 1; j++) {
+                if (j + 1 >= n) break;
+                const float Fn = F(e + (float)(j + 1));
                 s += (Fn - Fp) * __ldg(&yk[j]);
                 Fp = Fn;
             }
+            const float Fend = clR ? F(e + (float)n) : 0.5f * (tr.t3 + tr.t2 - tr.t1 - tr.t0);
+            s += (Fend - Fp) * __ldg(&yk[n - 1]);
             acc += tr.lphi * s;
         }
     }
