@@ -83,7 +83,9 @@ def lib():
         L.or_bit_reversal.argtypes = [i, ip]; L.or_bit_reversal.restype = None
         L.or_rho_l.argtypes = [ctypes.c_long, d]; L.or_rho_l.restype = d
         L.or_subset_grad.argtypes = [G, i, i, dp, dp, dp, dp]; L.or_subset_grad.restype = None
-        L.or_oslalm_run.argtypes = [G, dp, dp, dp, u8, i, i, d, d, d, d, i, i, i, dp, dp, dp, dp]
+        L.or_oslalm_run.argtypes = [G, dp, dp, dp, u8, i, i, d, d, d, d, i, i, i, dp, dp, dp, dp, i, i]
+        L.or_inner_fista.argtypes = [G, d, d, i, u8, dp, d, dp, dp, i, dp]
+        L.or_inner_fista.restype = None
         L.or_oslalm_run.restype = None
         _lib = L
     return _lib
@@ -225,9 +227,22 @@ def subset_grad(g, M, m, y, w, x):
     return G
 
 
+def inner_fista(g, beta, delta, nbr, mask, dl, rho, xk, s, n):
+    """n warm-started FISTA iterations on the inner denoising problem (NEXT-1)."""
+    m, mp = _u8(np.reshape(mask, img_shape(g)))
+    dl, dp = _d(np.reshape(dl, img_shape(g)))
+    xk, xp = _d(np.reshape(xk, img_shape(g)))
+    s, sp = _d(np.reshape(s, img_shape(g)))
+    out = np.zeros(img_shape(g))
+    _, op = _d(out)
+    lib().or_inner_fista(geom(g), beta, delta, nbr, mp, dp, rho, xp, sp, n, op)
+    return out
+
+
 def oslalm_run(g, y, w, dl, mask, x0, *, M, mode="continuation", rho_fixed=1.0, rho_min=1e-3,
-               beta, delta, nbr, n_iter, trailing=False):
-    """Run O7; returns (x, log[n_steps,3] = (rho, xi, restart), g, G)."""
+               beta, delta, nbr, n_iter, trailing=False, inner="sqs", n_inner=1):
+    """Run O7; returns (x, log[n_steps,3] = (rho, xi, restart), g, G).
+    inner = "sqs" (one Huber-curvature SQS step, G14) or "fista" (n_inner FISTA iterations, NEXT-1)."""
     y, yp = _d(np.reshape(y, sino_shape(g, g["na"])))
     w, wp = _d(np.reshape(w, sino_shape(g, g["na"])))
     dl, dp = _d(np.reshape(dl, img_shape(g)))
@@ -239,5 +254,6 @@ def oslalm_run(g, y, w, dl, mask, x0, *, M, mode="continuation", rho_fixed=1.0, 
     gs = np.zeros(img_shape(g)); Gs = np.zeros(img_shape(g))
     _, gp = _d(gs); _, Gp = _d(Gs)
     lib().or_oslalm_run(geom(g), yp, wp, dp, mp, M, 0 if mode == "fixed" else 1, rho_fixed, rho_min,
-                        beta, delta, nbr, n_iter, 1 if trailing else 0, xp, lp, gp, Gp)
+                        beta, delta, nbr, n_iter, 1 if trailing else 0, xp, lp, gp, Gp,
+                        0 if inner == "sqs" else 1, int(n_inner))
     return x, log, gs, Gs

@@ -436,6 +436,68 @@ void or_subset_grad(const or_geom* g, int M, int m, const double* y, const doubl
 }
 
 /*
+ * Inner constrained denoising by n warm-started FISTA iterations ("we solve this
+ * inner constrained denoising problem using n iterations of ... FISTA ... starting from
+ * the previous update as a warm start"; NEXT-1 reading in DESIGN.md):
+ *   minimise  phi(x) = R(x) + (rho/2) ||x - z||^2_{D_L}  over x >= 0 (x = 0 off S),
+ *   z = xk - s / (rho D_L),  grad f(v) = grad R(v) + rho D_L (v - xk) + s,
+ * with the fixed diagonal Lipschitz metric P = rho D_L + 2 beta sum_{k in N(j) & S} w_jk
+ * (Fair: psi'' <= 1) and Beck-Teboulle momentum:
+ *   v0 = x0 = xk, t0 = 1;  x_i = max(0, v_{i-1} - P^-1 grad f(v_{i-1}));
+ *   t_i = (1 + sqrt(1 + 4 t_{i-1}^2)) / 2;  v_i = x_i + ((t_{i-1} - 1)/t_i)(x_i - x_{i-1}).
+ * s is the search direction rho G + (1 - rho) g.  Writes x_n to x_out.
+ */
+void or_inner_fista(const or_geom* g, double beta, double delta, int nbr, const uint8_t* mask, const double* dl,
+                    double rho, const double* xk, const double* s, int n, double* x_out) {
+    size_t N = (size_t)nzv(g) * g->ny * g->nx;
+    int NZ = nzv(g);
+    double* v = (double*)malloc(N * sizeof(double));
+    double* xp = (double*)malloc(N * sizeof(double));
+    double* xn = (double*)malloc(N * sizeof(double));
+    double* gr = (double*)malloc(N * sizeof(double));
+    double* P = (double*)malloc(N * sizeof(double));
+    /* Lipschitz metric: rho D_L + 2 beta sum of neighbour weights inside S */
+    for (int iz = 0; iz < NZ; iz++)
+        for (int iy = 0; iy < g->ny; iy++)
+            for (int ix = 0; ix < g->nx; ix++) {
+                size_t j = ((size_t)iz * g->ny + iy) * g->nx + ix;
+                double sw = 0.0;
+                if (mask[j])
+                    for (int oz = -1; oz <= 1; oz++)
+                        for (int oy = -1; oy <= 1; oy++)
+                            for (int ox = -1; ox <= 1; ox++) {
+                                if (!nbr_ok(g, nbr, oz) || (ox == 0 && oy == 0 && oz == 0)) continue;
+                                int kx = ix + ox, ky = iy + oy, kz = iz + oz;
+                                if (kx < 0 || ky < 0 || kz < 0 || kx >= g->nx || ky >= g->ny || kz >= NZ) continue;
+                                size_t k = ((size_t)kz * g->ny + ky) * g->nx + kx;
+                                if (mask[k]) sw += 1.0 / sqrt((double)(ox * ox + oy * oy + oz * oz));
+                            }
+                P[j] = rho * dl[j] + 2.0 * beta * sw;
+            }
+    memcpy(v, xk, N * sizeof(double));
+    memcpy(xp, xk, N * sizeof(double));
+    double t = 1.0;
+    for (int i = 1; i <= n; i++) {
+        or_reg_grad(g, beta, delta, nbr, mask, v, gr, NULL);
+        for (size_t j = 0; j < N; j++) {
+            if (!mask[j]) { xn[j] = 0.0; continue; }
+            double grad = gr[j] + rho * dl[j] * (v[j] - xk[j]) + s[j];
+            double val = v[j] - grad / P[j];
+            xn[j] = val > 0.0 ? val : 0.0;
+        }
+        double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+        double mom = (t - 1.0) / tn;
+        for (size_t j = 0; j < N; j++) {
+            v[j] = xn[j] + mom * (xn[j] - xp[j]);
+            xp[j] = xn[j];
+        }
+        t = tn;
+    }
+    memcpy(x_out, xp, N * sizeof(double));
+    free(v); free(xp); free(xn); free(gr); free(P);
+}
+
+/*
  * OS-LALM run:
  *   x <- x0 (caller, 0 on S); G <- M A_{pi0}'(W(A x - y)); g <- G; l <- 0
  *   for k = 1..K, j = 0..M-1:
@@ -452,7 +514,8 @@ void or_subset_grad(const or_geom* g, int M, int m, const double* y, const doubl
  */
 void or_oslalm_run(const or_geom* g, const double* y, const double* w, const double* dl, const uint8_t* mask,
                    int M, int mode, double rho_fixed, double rho_min, double beta, double delta, int nbr,
-                   int n_iter, int trailing, double* x, double* log, double* g_out, double* G_out) {
+                   int n_iter, int trailing, double* x, double* log, double* g_out, double* G_out, int inner,
+                   int n_inner) {
     size_t N = (size_t)nzv(g) * g->ny * g->nx;
     size_t cells = (size_t)ntv(g) * g->ns;
     int maxcount = (g->na + M - 1) / M;
@@ -473,12 +536,20 @@ void or_oslalm_run(const or_geom* g, const double* y, const double* w, const dou
     for (int k = 1; k <= n_iter; k++)
         for (int j = 0; j < M; j++, step++) {
             double rho = mode == 0 ? rho_fixed : or_rho_l(l, rho_min);
-            or_reg_grad(g, beta, delta, nbr, mask, x, gr, cu);
-            for (size_t q = 0; q < N; q++) {
-                if (!mask[q]) { x[q] = 0.0; continue; }
-                double s = rho * G[q] + (1.0 - rho) * sg[q];
-                double xn = x[q] - (s + gr[q]) / (rho * dl[q] + cu[q]);
-                x[q] = xn > 0.0 ? xn : 0.0;
+            if (inner == 0) {
+                /* n = 1 SQS step with the Huber curvature of R at x (reading G14) */
+                or_reg_grad(g, beta, delta, nbr, mask, x, gr, cu);
+                for (size_t q = 0; q < N; q++) {
+                    if (!mask[q]) { x[q] = 0.0; continue; }
+                    double s = rho * G[q] + (1.0 - rho) * sg[q];
+                    double xn = x[q] - (s + gr[q]) / (rho * dl[q] + cu[q]);
+                    x[q] = xn > 0.0 ? xn : 0.0;
+                }
+            } else {
+                /* n warm-started FISTA iterations on the inner problem (NEXT-1) */
+                for (size_t q = 0; q < N; q++) cu[q] = rho * G[q] + (1.0 - rho) * sg[q];   /* s */
+                memcpy(gr, x, N * sizeof(double));                                         /* x_k */
+                or_inner_fista(g, beta, delta, nbr, mask, dl, rho, gr, cu, n_inner, x);
             }
             if (log) { log[3 * step] = rho; log[3 * step + 1] = 0.0; log[3 * step + 2] = 0.0; }
             if (!trailing && k == n_iter && j == M - 1) break;

@@ -394,3 +394,89 @@ def test_converges_to_bruteforce_minimiser_16x16():
     assert err <= 1e-8, (err, kkt)
     assert (xhat == 0).sum() > 20          # the box constraint is active on part of S
     assert log[:, 2].sum() >= 1            # continuation restarted at least once
+
+
+# ---------------------------------------------------------------- inner FISTA (NEXT-1)
+
+def _inner_case(seed=21, beta=2.0 ** 10, nbr=8):
+    g, y, w, mask = _small_problem()
+    dl, S = O.sqs_denom(g, w, mask)
+    rng = np.random.default_rng(seed)
+    shape = O.img_shape(g)
+    xk = rng.random(shape) * 0.02 * (S > 0)
+    s = (rng.standard_normal(shape) * 0.5 * dl.max() * 1e-3) * (S > 0)
+    return g, dl, S, xk, s, beta, 2e-4, nbr
+
+
+def test_inner_fista_beta0_is_box_projection():
+    """beta = 0: the inner problem is a D_L-weighted projection, solved exactly by one step:
+    x = max(0, z), z = x_k - s / (rho D_L); further iterations stay there."""
+    g, dl, S, xk, s, _, delta, nbr = _inner_case()
+    rho = 0.3
+    Sm = S > 0
+    z = np.where(Sm, xk - s / np.where(Sm, rho * dl, 1.0), 0.0)
+    for n in (1, 3):
+        x = O.inner_fista(g, 0.0, delta, nbr, S, dl, rho, xk, s, n)
+        assert np.abs(x - np.maximum(z, 0.0)).max() <= 1e-15 * max(1.0, np.abs(z).max())
+
+
+def _inner_reference(g, dl, S, xk, s, beta, delta, rho):
+    """High-accuracy solve of min_{x >= 0 on S} R(x) + rho/2 ||x - z||^2_{D_L} (L-BFGS-B, independent R)."""
+    Sm = S.reshape(-1) > 0
+    z = (xk - s / np.where(S > 0, rho * dl, 1.0)).reshape(-1)[Sm]
+    D = dl.reshape(-1)[Sm]
+    j, k, wt = _pairs(O.img_shape(g), 8)
+    both = Sm[j] & Sm[k]
+    pos = -np.ones(Sm.size, int); pos[Sm] = np.arange(Sm.sum())
+    j, k, wt = pos[j[both]], pos[k[both]], wt[both]
+
+    def f(xs):
+        t = xs[j] - xs[k]
+        a = np.abs(t) / delta
+        val = beta * (wt * delta * delta * (a - np.log1p(a))).sum() + 0.5 * rho * (D * (xs - z) ** 2).sum()
+        ps = beta * wt * t / (1 + a)
+        gd = np.bincount(j, ps, Sm.sum()) - np.bincount(k, ps, Sm.sum()) + rho * D * (xs - z)
+        return val, gd
+
+    res = scipy.optimize.minimize(f, np.maximum(z, 0), jac=True, method="L-BFGS-B", bounds=[(0, None)] * Sm.sum(),
+                                  options=dict(maxiter=100000, maxfun=200000, ftol=0, gtol=1e-16, maxcor=50))
+    out = np.zeros(Sm.size); out[Sm] = res.x
+    return out.reshape(O.img_shape(g))
+
+
+def test_inner_fista_converges_to_inner_minimiser():
+    """n -> large: FISTA reaches the exact inner minimiser."""
+    g, dl, S, xk, s, beta, delta, nbr = _inner_case()
+    rho = 0.5
+    ref = _inner_reference(g, dl, S, xk, s, beta, delta, rho)
+    x = O.inner_fista(g, beta, delta, nbr, S, dl, rho, xk, s, 3000)
+    assert np.linalg.norm(x - ref) <= 1e-7 * np.linalg.norm(ref)
+    # more iterations never hurt much, few iterations are already close (warm start)
+    x5 = O.inner_fista(g, beta, delta, nbr, S, dl, rho, xk, s, 5)
+    assert np.linalg.norm(x5 - ref) < np.linalg.norm(xk - ref)
+
+
+def test_inner_fista_warm_start_at_solution_is_fixed():
+    """Warm start at the inner solution (same z) is a fixed point."""
+    g, dl, S, xk, s, beta, delta, nbr = _inner_case()
+    rho = 0.5
+    xs = O.inner_fista(g, beta, delta, nbr, S, dl, rho, xk, s, 4000)
+    Sm = S > 0
+    z = np.where(Sm, xk - s / np.where(Sm, rho * dl, 1.0), 0.0)
+    s2 = np.where(Sm, rho * dl * (xs - z), 0.0)          # keeps z unchanged for x_k = xs
+    x = O.inner_fista(g, beta, delta, nbr, S, dl, rho, xs, s2, 5)
+    assert np.abs(x - xs).max() <= 1e-10 * np.abs(xs).max()
+
+
+def test_oslalm_fista_inner_converges_to_bruteforce():
+    """OS-LALM with n = 3 inner FISTA iterations (M = 1, continuation) has the same fixed point:
+    the brute-force minimiser of the 16x16 problem."""
+    g, y, w, mask = _small_problem()
+    dl, S = O.sqs_denom(g, w, mask)
+    beta, delta = 2.0 ** 16, 2e-4
+    xhat, kkt, f = _bruteforce_solution(g, y, w, S, beta, delta)
+    x = np.zeros(O.img_shape(g))
+    x, log, _, _ = O.oslalm_run(g, y, w, dl, S, x, M=1, mode="continuation", beta=beta, delta=delta,
+                                nbr=8, n_iter=3000, inner="fista", n_inner=3)
+    err = np.linalg.norm(x - xhat) / np.linalg.norm(xhat)
+    assert err <= 1e-6, err
