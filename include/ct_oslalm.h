@@ -156,12 +156,19 @@ int ct_count_vv(const ct_geom* g, ct_views v, const uint8_t* mask, void* scratch
 
 typedef enum { CT_RHO_FIXED = 0, CT_RHO_CONTINUATION = 1 } ct_rho_mode;
 
+typedef enum {
+    CT_INNER_SQS = 0,   /* one SQS step with the Huber curvature of R at x (n_inner = 1; reading G14) */
+    CT_INNER_FISTA = 1  /* n_inner warm-started FISTA iterations with the fixed Lipschitz metric
+                           rho D_L + 2 beta sum_k w_jk ("n iterations of FISTA"; NEXT-1)   */
+} ct_inner_mode;
+
 typedef struct {
-    int M;            /* number of ordered subsets, 1 <= M <= na            */
-    int mode;         /* ct_rho_mode                                        */
-    double rho_fixed; /* FIXED mode: AL penalty rho in (0, 1]               */
-    double rho_min;   /* CONTINUATION floor, P:516 uses 1e-3                */
-    int n_inner;      /* FISTA steps for the inner problem; only 1 supported */
+    int M;            /* number of ordered subsets, 1 <= M <= na                 */
+    int mode;         /* ct_rho_mode                                             */
+    double rho_fixed; /* FIXED mode: AL penalty rho in (0, 1]                    */
+    double rho_min;   /* CONTINUATION floor, P:516 uses 1e-3                     */
+    int n_inner;      /* inner iterations: 1 for CT_INNER_SQS, 1..64 for FISTA   */
+    int inner;        /* ct_inner_mode                                           */
     ct_reg reg;
 } ct_oslalm_cfg;
 
@@ -224,6 +231,8 @@ int ct_oslalm_get_timing(const ct_oslalm_state* s, double* ms5, long long* count
  * One outer iteration = M inner steps in bit-reversal order (reading O7):
  *   rho <- FIXED ? rho_fixed : rho_l(l)
  *   x   <- max(0, x - (rho G + (1-rho) g + grad R(x)) / (rho D_L + D_R(x)))   on S, 0 off S
+ *          (CT_INNER_SQS; with CT_INNER_FISTA: n_inner FISTA iterations on
+ *           min_{x>=0} R(x) + rho/2 ||x - (x_k - s/(rho D_L))||^2_{D_L}, s = rho G + (1-rho) g)
  *   G+  <- M A_m'(W (A_m x - y)),  m = next subset    (fused residual in the projection)
  *   xi  <- sum_S (g - G+)(G+ - G);  g <- (rho G+ + g)/(1 + rho);  G <- G+   
  *   CONTINUATION: l <- (xi > 0) ? 0 : l + 1

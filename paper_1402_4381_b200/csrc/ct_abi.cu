@@ -402,6 +402,7 @@ struct ct_oslalm_state {
     float* xalt;
     float* Gtmp;
     float* sino;
+    float* vbuf[2] = {nullptr, nullptr};
     double* xi_part;
     Scalars* sc;
     double* dlog;        // M x 3 doubles (per iteration)
@@ -475,11 +476,15 @@ static int check_cfg(const ct_geom* g, const ct_oslalm_cfg* c) {
         return fail(CT_EINVAL, "rho_fixed must be in (0, 1]");
     if (c->mode == CT_RHO_CONTINUATION && !(c->rho_min > 0 && c->rho_min <= 1))
         return fail(CT_EINVAL, "rho_min must be in (0, 1]");
-    if (c->n_inner != 1) return fail(CT_EUNSUPPORTED, "n_inner = %d: only one inner FISTA step is implemented", c->n_inner);
+    if (c->inner != CT_INNER_SQS && c->inner != CT_INNER_FISTA) return fail(CT_EINVAL, "bad inner mode %d", c->inner);
+    if (c->inner == CT_INNER_SQS && c->n_inner != 1)
+        return fail(CT_EINVAL, "CT_INNER_SQS takes exactly one step (n_inner = %d); use CT_INNER_FISTA", c->n_inner);
+    if (c->inner == CT_INNER_FISTA && (c->n_inner < 1 || c->n_inner > 64))
+        return fail(CT_EINVAL, "n_inner = %d outside [1, 64]", c->n_inner);
     return check_reg(g, &c->reg);
 }
 
-static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[10], size_t* total) {
+static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[12], size_t* total) {
     size_t N = n_vox(g);
     int maxcount = (g->d.na + c->M - 1) / c->M;
     size_t sino = (size_t)maxcount * n_cells_view(g);
@@ -494,13 +499,15 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[10
     off[6] = o; o += align256(nparts * 8);  // xi partials
     off[7] = o; o += align256(sizeof(Scalars));
     off[8] = o; o += align256((size_t)c->M * 3 * 8);  // device log
+    const bool two_v = c->inner == CT_INNER_FISTA && c->n_inner > 1;
+    off[9] = o; o += two_v ? 2 * align256(N * 4) : 0;  // FISTA extrapolation points v (ping-pong)
     *total = o;
 }
 
 extern "C" int ct_oslalm_state_bytes(const ct_geom* g, const ct_oslalm_cfg* c, size_t* out) {
     if (!g || !out) return fail(CT_EINVAL, "ct_oslalm_state_bytes: null argument");
     if (int e = check_cfg(g, c)) return e;
-    size_t off[10];
+    size_t off[12];
     state_layout(g, c, off, out);
     return CT_OK;
 }
@@ -509,7 +516,7 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
                                       ct_oslalm_state** out) {
     if (!g || !ws || !out) return fail(CT_EINVAL, "ct_oslalm_state_create: null argument");
     if (int e = check_cfg(g, c)) return e;
-    size_t off[10], total;
+    size_t off[12], total;
     state_layout(g, c, off, &total);
     if (bytes < total) return fail(CT_ENOMEM, "workspace of %zu bytes < required %zu", bytes, total);
     if ((uintptr_t)ws & 255) return fail(CT_EINVAL, "workspace must be 256-byte aligned");
@@ -530,6 +537,10 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
     s->xi_part = (double*)(b + off[6]);
     s->sc = (Scalars*)(b + off[7]);
     s->dlog = (double*)(b + off[8]);
+    if (c->inner == CT_INNER_FISTA && c->n_inner > 1) {
+        s->vbuf[0] = (float*)(b + off[9]);
+        s->vbuf[1] = (float*)(b + off[9] + align256(s->N * 4));
+    }
     cudaError_t e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming);
@@ -662,20 +673,47 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
     int kernels = 0;
     for (int j = 0; j < M; j++) {
         int t0 = tmark(s, st);
-        if (c.reg.nbr == 8)
-            sqs_update_kernel<8><<<nblk(s->N), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
-                                                              &s->sc->rho, (float)c.reg.beta, inv_d, s->N);
-        else
-            sqs_update3d_kernel<<<dim3((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (g->dg.ny + kK3Y - 1) / kK3Y), 256, 0, st>>>(
-                g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask, &s->sc->rho, (float)c.reg.beta, inv_d);
-        CT_LAUNCHED(1);
+        if (c.inner == CT_INNER_SQS) {
+            if (c.reg.nbr == 8)
+                sqs_update_kernel<8><<<nblk(s->N), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
+                                                                  &s->sc->rho, (float)c.reg.beta, inv_d, s->N);
+            else
+                sqs_update3d_kernel<<<dim3((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (g->dg.ny + kK3Y - 1) / kK3Y), 256,
+                                      0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask, &s->sc->rho,
+                                               (float)c.reg.beta, inv_d);
+            CT_LAUNCHED(1);
+        } else {
+            // n warm-started FISTA iterations: v_0 = x_0 = x_k (= xa), result in xb
+            double t = 1.0;
+            const float* v = xa;
+            const float* xprev = xa;
+            for (int i = 1; i <= c.n_inner; i++) {
+                double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+                float mom = (float)((t - 1.0) / tn);
+                bool last = i == c.n_inner;
+                float* vout = last ? nullptr : s->vbuf[i & 1];
+#define CT_FISTA(NB, LAST)                                                                                         \
+    fista_step_kernel<NB, LAST><<<nblk(s->N), 256, 0, st>>>(g->dg, v, xprev, xa, xb, vout, s->Gbuf[s->curG], s->gs, \
+                                                            d->dl, d->mask, &s->sc->rho, (float)c.reg.beta, inv_d, mom, s->N)
+                if (c.reg.nbr == 8) {
+                    if (last) CT_FISTA(8, true); else CT_FISTA(8, false);
+                } else {
+                    if (last) CT_FISTA(26, true); else CT_FISTA(26, false);
+                }
+#undef CT_FISTA
+                CT_LAUNCHED(1);
+                v = vout;
+                xprev = xb;
+                t = tn;
+            }
+        }
         tmark_end(s, st, 0, t0);
         std::swap(xa, xb);
         s->log_slot = j;
         if (int e = subset_gradient(s, d, xa, s->order[(j + 1) % M], EPI_GUPD, st)) return e;
         s->log_slot = -1;
         s->curG ^= 1;
-        kernels += 3 + (g->comm ? 1 : 0);
+        kernels += 2 + (c.inner == CT_INNER_FISTA ? c.n_inner : 1) + (g->comm ? 1 : 0);
     }
     if (xa != x) {
         CT_CUDA(cudaMemcpyAsync(x, xa, s->N * 4, cudaMemcpyDeviceToDevice, st));
@@ -703,7 +741,8 @@ static int check_data(const ct_geom* g, const ct_oslalm_data* d, const float* x)
 
 static bool cfg_equal(const ct_oslalm_cfg& a, const ct_oslalm_cfg& b) {
     return a.M == b.M && a.mode == b.mode && a.rho_fixed == b.rho_fixed && a.rho_min == b.rho_min &&
-           a.n_inner == b.n_inner && a.reg.beta == b.reg.beta && a.reg.delta == b.reg.delta && a.reg.nbr == b.reg.nbr;
+           a.n_inner == b.n_inner && a.inner == b.inner && a.reg.beta == b.reg.beta && a.reg.delta == b.reg.delta &&
+           a.reg.nbr == b.reg.nbr;
 }
 
 extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_data* d, ct_oslalm_state* s,
@@ -713,6 +752,8 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
     if (cfg && !cfg_equal(*cfg, s->cfg)) {
         if (int e = check_cfg(g, cfg)) return e;
         if (cfg->M != s->cfg.M) return fail(CT_ESTATE, "M changed after state creation");
+        if (cfg->inner != s->cfg.inner || cfg->n_inner != s->cfg.n_inner)
+            return fail(CT_ESTATE, "inner solver changed after state creation (workspace layout)");
         s->cfg = *cfg;
         for (auto& ge : s->graphs)
             if (ge.exec) { cudaGraphExecDestroy(ge.exec); ge.exec = nullptr; }

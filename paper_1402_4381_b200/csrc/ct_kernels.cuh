@@ -873,6 +873,59 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
     }
 }
 
+// One FISTA iteration of the inner denoising problem (NEXT-1):
+//   x_i = max(0, v - (grad R(v) + rho D_L (v - x_k) + s) / (rho D_L + 2 beta sum w)),  s = rho G + (1-rho) g
+//   v_i = x_i + mom (x_i - x_{i-1})            (skipped on the last iteration)
+// x_prev may alias x_out (element-wise, read before write).
+template <int NBR, bool LAST>
+__global__ void __launch_bounds__(256) fista_step_kernel(DevGeom g, const float* __restrict__ v, const float* xprev,
+                                                        const float* __restrict__ xk, float* xout, float* __restrict__ vout,
+                                                        const float* __restrict__ G, const float* __restrict__ gs,
+                                                        const float* __restrict__ dl, const uint8_t* __restrict__ m,
+                                                        const double* __restrict__ rho_p, float beta, float inv_delta,
+                                                        float mom, size_t N) {
+    size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    if (!m[j]) {
+        xout[j] = 0.0f;
+        if (!LAST) vout[j] = 0.0f;
+        return;
+    }
+    const int nz = g.nz;
+    const int iz = (int)(j % nz);
+    const size_t c = j / nz;
+    const int ix = (int)(c % g.nx), iy = (int)(c / g.nx);
+    const float vj = v[j];
+    float gr = 0.0f, sw = 0.0f;
+#pragma unroll
+    for (int oy = -1; oy <= 1; oy++)
+#pragma unroll
+        for (int ox = -1; ox <= 1; ox++)
+#pragma unroll
+            for (int oz = (NBR == 26 ? -1 : 0); oz <= (NBR == 26 ? 1 : 0); oz++) {
+                if (oy == 0 && ox == 0 && oz == 0) continue;
+                const int ky = iy + oy, kx = ix + ox, kz = iz + oz;
+                if (ky < 0 || ky >= g.ny || kx < 0 || kx >= g.nx || kz < 0 || kz >= nz) continue;
+                const size_t kk = ((size_t)ky * g.nx + kx) * nz + kz;
+                if (!__ldg(&m[kk])) continue;
+                constexpr float r2 = 0.70710678118654752f, r3 = 0.57735026918962576f;
+                const int d2 = oy * oy + ox * ox + oz * oz;
+                const float wgt = d2 == 1 ? 1.0f : (d2 == 2 ? r2 : r3);
+                float dpsi, om;
+                fair(vj - __ldg(&v[kk]), inv_delta, dpsi, om);
+                gr += wgt * dpsi;
+                sw += wgt;
+            }
+    const float rho = (float)*rho_p;
+    const float rdl = rho * dl[j];
+    const float s = rho * G[j] + (1.0f - rho) * gs[j];
+    const float grad = beta * gr + rdl * (vj - xk[j]) + s;
+    const float xp = xprev[j];
+    const float xn = fmaxf(vj - grad / (rdl + 2.0f * beta * sw), 0.0f);
+    xout[j] = xn;
+    if (!LAST) vout[j] = xn + mom * (xn - xp);
+}
+
 template <int NBR>
 __global__ void __launch_bounds__(256) reg_grad_kernel(DevGeom g, const float* __restrict__ x, const uint8_t* __restrict__ m,
                                                       float* __restrict__ grad, float* __restrict__ curv, float beta,

@@ -56,7 +56,7 @@ class ct_reg(ctypes.Structure):
 
 class ct_oslalm_cfg(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int), ("mode", ctypes.c_int), ("rho_fixed", ctypes.c_double),
-                ("rho_min", ctypes.c_double), ("n_inner", ctypes.c_int), ("reg", ct_reg)]
+                ("rho_min", ctypes.c_double), ("n_inner", ctypes.c_int), ("inner", ctypes.c_int), ("reg", ct_reg)]
 
 
 class ct_oslalm_data(ctypes.Structure):
@@ -290,10 +290,10 @@ class OSLALM:
     """OS-LALM solver state over a caller-owned (torch) device workspace."""
 
     def __init__(self, geo: Geometry, M, *, mode="continuation", rho_fixed=1.0, rho_min=1e-3, beta, delta, nbr,
-                 n_inner=1):
+                 n_inner=1, inner="sqs"):
         self.geo = geo
         self.cfg = ct_oslalm_cfg(int(M), 1 if mode == "continuation" else 0, float(rho_fixed), float(rho_min),
-                                 int(n_inner), ct_reg(float(beta), float(delta), int(nbr)))
+                                 int(n_inner), 0 if inner == "sqs" else 1, ct_reg(float(beta), float(delta), int(nbr)))
         L = load()
         n = ctypes.c_size_t()
         _check(L.ct_oslalm_state_bytes(geo.h, ctypes.byref(self.cfg), ctypes.byref(n)))

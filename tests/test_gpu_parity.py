@@ -211,7 +211,7 @@ def test_reg_grad(ct, O, name, nbr):
 
 # --------------------------------------------------------------------------- OS-LALM
 
-def _run_pair(ct, O, cfg, n_iter, M=None, mode="continuation", rho_fixed=1.0, x0=None):
+def _run_pair(ct, O, cfg, n_iter, M=None, mode="continuation", rho_fixed=1.0, x0=None, inner="sqs", n_inner=1):
     g = cfg.geom
     M = M or cfg.M
     d = I.synthesize(cfg)
@@ -221,7 +221,8 @@ def _run_pair(ct, O, cfg, n_iter, M=None, mode="continuation", rho_fixed=1.0, x0
     dl, S = geo.sqs_denom(w.cuda(), m0.cuda())
     dlo, So = O.sqs_denom(g, I.to_oracle_sino(w), I.to_oracle_image(m0).astype(np.uint8))
     assert np.array_equal(I.to_oracle_image(S.cpu().numpy()).astype(np.uint8), So)
-    sol = ct.OSLALM(geo, M, mode=mode, rho_fixed=rho_fixed, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr)
+    sol = ct.OSLALM(geo, M, mode=mode, rho_fixed=rho_fixed, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr,
+                    inner=inner, n_inner=n_inner)
     yc, wc = y.cuda(), w.cuda()
     sol.set_data(yc, wc, dl, S)
     x = torch.zeros(geo.img_shape, device="cuda") if x0 is None else x0.clone().cuda()
@@ -229,11 +230,12 @@ def _run_pair(ct, O, cfg, n_iter, M=None, mode="continuation", rho_fixed=1.0, x0
     xo, logo, _, _ = O.oslalm_run(g, I.to_oracle_sino(y), I.to_oracle_sino(w), dlo, So,
                                   np.zeros(O.img_shape(g)) if x0 is None else I.to_oracle_image(x0),
                                   M=M, mode=mode, rho_fixed=rho_fixed, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr,
-                                  n_iter=n_iter)
+                                  n_iter=n_iter, inner=inner, n_inner=n_inner)
     xg = I.to_oracle_image(x.cpu().numpy())
     Sm = So > 0
     rms_hu = math.sqrt(((xg - xo)[Sm] ** 2).mean()) / I.HU
-    MARGINS.append({"case": f"OS-LALM {cfg.name} M={M} {mode} rho={rho_fixed} iters={n_iter}", "rms_HU": rms_hu,
+    MARGINS.append({"case": f"OS-LALM {cfg.name} M={M} {mode} rho={rho_fixed} iters={n_iter} inner={inner}x{n_inner}",
+                    "rms_HU": rms_hu,
                     "restarts_gpu": int(np.array(log)[:, 2].sum()), "restarts_oracle": int(logo[:, 2].sum())})
     return xg, xo, np.array(log), logo, rms_hu
 
@@ -338,3 +340,41 @@ def test_exchange_path_single_rank(ct):
     assert np.array_equal(la[:, 2], lb[:, 2])
     assert np.allclose(la[:, 1], lb[:, 1], rtol=1e-5)
     assert rel_l2(xb, xa) <= 1e-6
+
+
+@pytest.mark.parametrize("n_inner", [1, 2, 5])
+def test_oslalm_inner_fista(ct, O, n_inner):
+    """NEXT-1: n warm-started inner FISTA iterations vs the oracle, c1 geometry."""
+    cfg = I.config("c1")
+    xg, xo, log, logo, rms = _run_pair(ct, O, cfg, 8, inner="fista", n_inner=n_inner)
+    assert rms <= 0.5, rms
+    assert np.array_equal(log[:, 2], logo[:, 2])
+
+
+def test_oslalm_inner_fista_3d(ct, O):
+    g = geoms_small()["axial_c3"]
+    ell = [(0.0, 0.0, 0.0, 4.0, 3.5, 2.0, 0.0, 0.02), (1.0, -0.5, 0.3, 1.2, 0.8, 0.9, 0.4, 0.01)]
+    d = I.noisy_data(g, ell, 1e5, 0.0, 78)
+    geo = ct.Geometry(g)
+    m0 = torch.ones(geo.img_shape, dtype=torch.uint8)
+    dl, S = geo.sqs_denom(d["w"].cuda(), m0.cuda())
+    dlo, So = O.sqs_denom(g, I.to_oracle_sino(d["w"]), I.to_oracle_image(m0).astype(np.uint8))
+    beta, delta = 2.0 ** 10, 2e-4
+    sol = ct.OSLALM(geo, 4, beta=beta, delta=delta, nbr=26, inner="fista", n_inner=3)
+    sol.set_data(d["y"].cuda(), d["w"].cuda(), dl, S)
+    x = torch.zeros(geo.img_shape, device="cuda")
+    sol.run(x, 6)
+    xo, _, _, _ = O.oslalm_run(g, I.to_oracle_sino(d["y"]), I.to_oracle_sino(d["w"]), dlo, So, np.zeros(O.img_shape(g)),
+                               M=4, beta=beta, delta=delta, nbr=26, n_iter=6, inner="fista", n_inner=3)
+    xg = I.to_oracle_image(x.cpu().numpy())
+    rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
+    MARGINS.append({"case": "OS-LALM axial_c3 small inner=fista x3", "rms_HU": rms})
+    assert rms <= 0.5, rms
+
+
+def test_inner_mode_validation(ct):
+    geo = ct.Geometry(I.config("c1").geom)
+    with pytest.raises(ct.CTError, match="CT_EINVAL"):
+        ct.OSLALM(geo, 4, beta=1.0, delta=1e-3, nbr=8, inner="sqs", n_inner=2)
+    with pytest.raises(ct.CTError, match="CT_EINVAL"):
+        ct.OSLALM(geo, 4, beta=1.0, delta=1e-3, nbr=8, inner="fista", n_inner=0)
