@@ -125,6 +125,7 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
         return fail(CT_EINVAL, "spacings must be positive and dsd > dso");
     if (fabs(d->dx - d->dy) > 1e-9 * d->dx) return fail(CT_EINVAL, "dx must equal dy (square voxels)");
     if (!is2d && nt > 128) return fail(CT_EUNSUPPORTED, "nt = %d > 128 detector rows", nt);
+    if (!is2d && nz > 4096) return fail(CT_EUNSUPPORTED, "nz = %d > 4096 slices", nz);
     if (d->kind == CT_CONE_HELICAL && !(d->pitch > 0)) return fail(CT_EINVAL, "helical geometry needs pitch > 0");
     if ((double)d->nx * d->ny * nz >= 2147483647.0 || (double)d->na * d->ns * nt >= 2147483647.0)
         return fail(CT_EUNSUPPORTED, "image or sinogram has >= 2^31 elements (32-bit kernel indexing)");
@@ -263,12 +264,19 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
     return CT_OK;
 }
 
+// 3D back-projection variant: axial scans use 64-slice register chunks (every view's
+// cone covers a chunk); helical scans use whole-column shared-memory accumulators so
+// the work follows each view's active slices.
+static bool back3d_use_chunks(const ct_geom* g) { return g->d.kind == CT_CONE_AXIAL; }
+
 static void back_grid(const ct_geom* g, dim3& grid) {
     const DevGeom& dg = g->dg;
     if (dg.kind == CT_FAN2D)
         grid = dim3((dg.nx + 31) / 32, (dg.ny + 7) / 8, 1);
-    else
+    else if (back3d_use_chunks(g))
         grid = dim3((dg.nx + 3) / 4, (dg.ny + 1) / 2, (dg.nz + 63) / 64);
+    else
+        grid = dim3((dg.nx + 3) / 4, (dg.ny + 1) / 2, 1);
 }
 
 static size_t back_nblocks(const ct_geom* g) {
@@ -284,8 +292,17 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
     back_grid(g, grid);
     if (dg.kind == CT_FAN2D)
         back2d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
-    else
-        back3d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+    else if (back3d_use_chunks(g))
+        back3d_chunk_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+    else {
+        const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * (size_t)dg.nz;
+        static int configured[4] = {0, 0, 0, 0};
+        if (smem > 48 * 1024 && configured[EPI] < (int)smem) {
+            cudaFuncSetAttribute(back3d_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured[EPI] = (int)smem;
+        }
+        back3d_kernel<EPI><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+    }
     CT_LAUNCHED(1);
     return CT_OK;
 }

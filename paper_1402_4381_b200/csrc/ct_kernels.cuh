@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
 }
 
 // ---------------------------------------------------------------------------
-// K2 (3D cone): voxel-driven back projection; warp = one column x 64 slices
+// K2 (3D cone, axial): voxel-driven back projection; warp = one column x 64 slices
 // ---------------------------------------------------------------------------
 // Block = 4x2 columns (8 warps); lane l owns slices zlo + l and zlo + 32 + l.
 // Views are processed in batches of 32: lane l computes the column's footprint
@@ -620,8 +620,10 @@ __global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int s
 //  (2) for each slice, sum_r F_t(iz, r) Q(r) is the integral of the row-wise
 //      constant Q over the slice's extent on the detector (in row units):
 //      PF(u1) - PF(u0) with PF the piecewise-linear cumulative sum.
+// Used for axial scans, where every view's cone covers the whole chunk; helical scans
+// use the column kernel below, whose work follows each view's active slices.
 template <int EPI>
-__global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, int stride, int count,
+__global__ void __launch_bounds__(256, 3) back3d_chunk_kernel(DevGeom g, int first, int stride, int count,
                                                        const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     constexpr int kRows = 128;                 // >= nt (validated)
     __shared__ Foot table[8][32];
@@ -739,6 +741,139 @@ __global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, in
     if (EPI == EPI_GUPD) {
         block_sum_store<256>(xi, &ga.xi_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]);
         xi_arrive<256>(ga, gridDim.x * gridDim.y * gridDim.z);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2 (3D cone): voxel-driven back projection; warp = one whole voxel column
+// ---------------------------------------------------------------------------
+// Block = 4x2 columns (8 warps); each warp owns one column's nz slices as
+// shared-memory accumulators.  Views are processed in batches of 32: lane l
+// computes the column's footprint for view vb + l (and the view's active slice
+// range, i.e. the slices its cone meets) into the warp's shared table.  For each
+// view the warp then
+//  (1) forms the transaxially filtered detector rows  Q(r) = sum_c lphi F_s(c) y[k][c][r]
+//      (lanes = rows: unit-stride loads) and their prefix sums (warp scan), and
+//  (2) walks only the active slices (lanes = slices): sum_r F_t(iz, r) Q(r) is the
+//      integral of the row-wise constant Q over the slice's extent on the detector,
+//      PF(u(iz + 1)) - PF(u(iz)) with PF the piecewise-linear cumulative sum.
+// Work per (column, view) is proportional to the slices the cone actually meets,
+// which matters for helical scans (a view sees ~20-30 % of a long volume).
+constexpr int kBackRows = 128;   // >= nt (validated)
+
+__host__ __device__ constexpr size_t back3d_smem_fixed() {
+    return sizeof(Foot) * 8 * 32 + sizeof(float) * 8 * kBackRows + sizeof(float) * 8 * (kBackRows + 4);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, int stride, int count,
+                                                       const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    Foot* table = reinterpret_cast<Foot*>(sm_raw);
+    float* Qs = reinterpret_cast<float*>(sm_raw + sizeof(Foot) * 8 * 32);
+    float* Ps = Qs + 8 * kBackRows;
+    float* ACC = Ps + 8 * (kBackRows + 4);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int ix = blockIdx.x * 4 + (wid & 3);
+    const int iy = blockIdx.y * 2 + (wid >> 2);
+    const bool colok = ix < g.nx && iy < g.ny;
+    const int nt = g.nt, ns = g.ns, nz = g.nz;
+    const int col = ((colok ? iy : 0) * g.nx + (colok ? ix : 0)) * nz;
+    Foot* tab = table + wid * 32;
+    float* Q = Qs + wid * kBackRows;
+    float* PF = Ps + wid * (kBackRows + 4);
+    float* acc = ACC + wid * nz;
+    bool any = false;
+    for (int iz = lane; iz < nz; iz += 32) {
+        acc[iz] = 0.0f;
+        // voxels outside the support S are not needed by OS-LALM / D_L
+        any |= colok && (ga.mask == nullptr || ga.mask[col + iz]);
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (any) {
+        const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
+        for (int vb = 0; vb < count; vb += 32) {
+            const int kk = vb + lane;
+            if (kk < count) {
+                Foot f;
+                column_footprint(g, g.views[first + kk * stride], xc, yc, f);
+                // slices met by rows [-1/2, nt - 1/2]:  q = qf + (r - rbase) kz  (+ qi)
+                const float qa = f.ax.qf + (-0.5f - g.rbase) * f.ax.kz;
+                const float qb = f.ax.qf + ((float)nt - 0.5f - g.rbase) * f.ax.kz;
+                const int za = max(__float2int_rd(qa) + f.ax.qi, 0);
+                const int zb = min(__float2int_rd(qb) + f.ax.qi, nz - 1);
+                if (!(f.n > 0 && zb >= za)) f.n = 0;
+                f.rows = za | ((zb - za + 1) << 16);
+                tab[lane] = f;
+            }
+            __syncwarp();
+            const int nb = min(32, count - vb);
+            for (int j = 0; j < nb; j++) {
+                Foot f;
+                load_foot(&tab[j], f);
+                if (f.n <= 0) continue;
+                const int za = f.rows & 0xffff, nzs = f.rows >> 16;
+                const float* yv = y + (size_t)(vb + j) * ns * nt;     // this view's sinogram
+                const int off0 = f.cA * nt;
+                // (1) filtered rows and their prefix sums (lanes = rows)
+                float carry = 0.0f;
+                for (int p0 = 0; p0 < nt; p0 += 32) {
+                    const int p = p0 + lane;
+                    const bool inr = p < nt;
+                    const float* yr = yv + (off0 + (inr ? p : 0));
+                    float q;
+                    if (f.n <= 4) {   // warp-uniform: issue all loads first, then the FMAs
+                        float v[4];
+#pragma unroll
+                        for (int c = 0; c < 4; c++) v[c] = (inr && c < f.n) ? __ldg(yr + c * nt) : 0.0f;
+                        q = f.w[0] * v[0] + f.w[1] * v[1] + f.w[2] * v[2] + f.w[3] * v[3];
+                    } else {
+                        float v[kMaxFoot];
+#pragma unroll
+                        for (int c = 0; c < kMaxFoot; c++) v[c] = (inr && c < f.n) ? __ldg(yr + c * nt) : 0.0f;
+                        q = 0.0f;
+#pragma unroll
+                        for (int c = 0; c < kMaxFoot; c++) q += f.w[c] * v[c];
+                    }
+                    if (inr) Q[p] = q;
+                    float inc = q;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        float t = __shfl_up_sync(0xffffffffu, inc, o);
+                        if (lane >= o) inc += t;
+                    }
+                    if (inr) PF[p + 1] = carry + inc;
+                    carry += __shfl_sync(0xffffffffu, inc, 31);
+                }
+                if (lane == 0) PF[0] = 0.0f;
+                __syncwarp();
+                // (2) the active slices (lanes = slices)
+                const float fnr = (float)nt;
+                const float ubase = g.rbase + 0.5f;
+                for (int s0 = 0; s0 < nzs; s0 += 32) {
+                    const int iz = za + s0 + lane;
+                    const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
+                    const float u0 = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubase), 0.0f), fnr);
+                    const int p0 = min(__float2int_rd(u0), nt - 1);
+                    const float pf = PF[p0] + (u0 - (float)p0) * Q[p0];
+                    float up = __shfl_down_sync(0xffffffffu, pf, 1);
+                    if (lane == 31) {   // upper edge of this pass's last slice
+                        const float u1 = fminf(fmaxf(fmaf(zi + 1.0f, f.ax.inv_kz, ubase), 0.0f), fnr);
+                        const int p1 = min(__float2int_rd(u1), nt - 1);
+                        up = PF[p1] + (u1 - (float)p1) * Q[p1];
+                    }
+                    if (s0 + lane < nzs) acc[iz] += ltheta(f.ax, iz) * (up - pf);
+                }
+                __syncwarp();
+            }
+        }
+    }
+    __syncwarp();
+    double xi = 0.0;
+    for (int iz = lane; iz < nz; iz += 32) xi += back_epilogue<EPI>((size_t)(col + iz), colok, acc[iz], x, ga);
+    if (EPI == EPI_GUPD) {
+        block_sum_store<256>(xi, &ga.xi_part[blockIdx.y * gridDim.x + blockIdx.x]);
+        xi_arrive<256>(ga, gridDim.x * gridDim.y);
     }
 }
 
