@@ -16,6 +16,7 @@
 
 #include "../../include/ct_oslalm.h"
 #include "ct_kernels.cuh"
+#include "ct_fan2d.cuh"
 
 using namespace ct;
 
@@ -90,6 +91,7 @@ struct ct_geom {
     DevGeomD dgd;
     float4* d_views = nullptr;
     double2* d_vz = nullptr;
+    unsigned long long* acc2d = nullptr;   // fan 2D forward: [na][ns] 64-bit fixed-point sums (kept zero)
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
 };
@@ -138,6 +140,23 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     if (wmax > kMaxFoot - 1)
         return fail(CT_EUNSUPPORTED, "voxel footprint may be %.2f channels wide (> %d)", wmax, kMaxFoot - 1);
 
+    int dg_fpar = 1, dg_fspan = 1;
+    if (is2d) {
+        // fwd2d_tile_kernel: (1) lanes l and l + P must hit different first channels: a pixel
+        // step along the warp's line moves the footprint by >= dx sin(pi/4 - delta) mag_min / ds
+        // channels (delta = ray-direction spread over a tile); (2) the tile's channel span.
+        double tdiag = kF2T * sqrt(2.0) * d->dx;
+        double delta = asin(std::min(0.999, 0.5 * tdiag / (d->dso - rmax)));
+        double shift = d->dx * sin(M_PI / 4 - delta) * d->dsd / ((d->dso + rmax) * d->ds);
+        int P = (int)ceil(1.02 / std::max(shift, 1e-9));
+        // unclipped tile span + the kMaxFoot bins a lane may address past its footprint
+        int span = (int)ceil(tdiag * d->dsd / ((d->dso - rmax) * d->ds)) + 3 + kMaxFoot;
+        if (!(shift > 0) || P > 8 || (size_t)8 * P * span * 4 > 160 * 1024)
+            return fail(CT_EUNSUPPORTED, "fan-beam forward tiles: pixel step %.3f channels (P = %d), span %d", shift, P,
+                        span);
+        dg_fpar = P;
+        dg_fspan = span;
+    }
     int dev = d->device;
     DeviceGuard guard(dev);
     ct_geom* g = new ct_geom();
@@ -156,6 +175,7 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     dg.dso = (float)d->dso; dg.dsd = (float)d->dsd;
     dg.dsd_ds = (float)(d->dsd / d->ds);
     dg.cbase = (float)((d->ns - 1) / 2.0 + d->offs);
+    dg.cedge = (float)((d->ns - 1) / 2.0 + d->offs + 0.5);
     dg.rbase = (float)((nt - 1) / 2.0 + d->offt);
     dg.dt = is2d ? 1.0f : (float)d->dt;
     {
@@ -198,13 +218,18 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     if (e == cudaSuccess) e = cudaMalloc(&g->d_vz, sizeof(double2) * d->na);
     if (e == cudaSuccess) e = cudaMemcpy(g->d_views, hv.data(), sizeof(float4) * d->na, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->d_vz, hvz.data(), sizeof(double2) * d->na, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && is2d) e = cudaMalloc(&g->acc2d, sizeof(unsigned long long) * d->na * d->ns);
+    if (e == cudaSuccess && is2d) e = cudaMemset(g->acc2d, 0, sizeof(unsigned long long) * d->na * d->ns);
     if (e != cudaSuccess) {
         cudaFree(g->d_views);
         cudaFree(g->d_vz);
+        cudaFree(g->acc2d);
         delete g;
         return fail(e == cudaErrorMemoryAllocation ? CT_ENOMEM : CT_ECUDA, "geometry tables: %s", cudaGetErrorString(e));
     }
     dg.views = g->d_views;
+    dg.fpar = dg_fpar;
+    dg.fspan = dg_fspan;
     gd.vz = g->d_vz;
     *out = g;
     return CT_OK;
@@ -216,6 +241,7 @@ extern "C" void ct_geom_destroy(ct_geom* g) {
     if (g->comm && g_nccl.ok) g_nccl.CommDestroy(g->comm);
     cudaFree(g->d_views);
     cudaFree(g->d_vz);
+    cudaFree(g->acc2d);
     delete g;
 }
 
@@ -247,9 +273,18 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
     if (v.count == 0) return CT_OK;
     const DevGeom& dg = g->dg;
     if (dg.kind == CT_FAN2D) {
-        constexpr int TC = 32;
-        dim3 grid((dg.ns + TC - 1) / TC, v.count);
-        fwd2d_kernel<TC, 256, RESID><<<grid, 256, 0, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+        const size_t smem = sizeof(float) * 8 * dg.fpar * dg.fspan;
+        static size_t configured = 0;
+        if (smem > 48 * 1024 && configured < smem) {
+            cudaFuncSetAttribute(fwd2d_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured = smem;
+        }
+        dim3 grid((dg.nx + kF2T - 1) / kF2T, (dg.ny + kF2T - 1) / kF2T, (v.count + kF2VC - 1) / kF2VC);
+        fwd2d_tile_kernel<<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, x, g->acc2d);
+        const int cells = v.count * dg.ns;
+        fwd2d_finalize_kernel<RESID><<<(cells + 255) / 256, 256, 0, st>>>(dg, v.first, v.stride, v.count, g->acc2d, out,
+                                                                          yobs, w, scale);
+        CT_LAUNCHED(1);
     } else {
         constexpr int TC = 16;
         dim3 grid((dg.ns + TC - 1) / TC, v.count);

@@ -30,10 +30,12 @@ struct DevGeom {
     float dso, dsd;
     float dsd_ds;             // dsd / ds  (radians -> channel units)
     float cbase;              // channel coordinate of fan angle 0: (ns-1)/2 + offs
+    float cedge;              // cbase + 1/2 (rounded once): bin c's left edge is c - cedge (centred units)
     float rbase;              // row coordinate of t = 0: (nt-1)/2 + offt
     float dt;
     float zs0, dzs;           // helical source height z_s(v) = zs0 + v dzs (dzs = 0: axial)
     float zhalf;              // bound on |z - z_s| of any voxel a view can see (mm)
+    int fpar, fspan;          // fan 2D forward: lane-parity buffers P and tile channel-span bound
     const float4* views;      // per view: (sin beta, cos beta, qi, qf) with
                               // (z_s - zb0)/dz = qi + qf, qi integer (exact in fp32)
 };

@@ -1,0 +1,327 @@
+// ct_fan2d.cuh — 2D fan-beam projector pair (K1 fwd2d, K2 back2d), sm_100a, fp32.
+//
+// Same SF-TR/A1 weights as ct_common.cuh (reading O2 / G1), organised around
+// the pixel-corner ("vertex") grid: a pixel's trapezoid breakpoints are the arc
+// positions of its four corners, and each corner is shared by four pixels.  Both
+// kernels evaluate the vertex positions with the ONE routine `vertex_ch` below and
+// the pixel footprint with `pixel_foot` / `foot_weights`, so a_ij is the same fp32
+// expression in A and A' (matched pair).
+//
+//   back2d: CTA = 32x8 pixel tile; per batch of views the CTA evaluates the tile's
+//           33x9 vertex positions into shared memory (1.16 atan per pixel-view
+//           instead of 5), then thread = pixel gathers its 2-6 sinogram bins per view.
+//   fwd2d:  CTA = (32x32 pixel tile, chunk of views); the same vertex table; lane =
+//           pixel, warp = row or column; a deterministic shared-memory reduction per
+//           tile and an exact 64-bit fixed-point sum over tiles (see fwd2d_tile_kernel).
+#pragma once
+#include "ct_common.cuh"
+
+namespace ct {
+
+// Pixel-corner ("vertex") coordinates: vertex (vx, vy) is the lower-left corner of
+// pixel (ix, iy) = (vx, vy).  Every kernel derives them with these two expressions.
+__device__ __forceinline__ float vertex_px(const DevGeom& g, int vx) { return fmaf((float)vx, g.dx, g.x0 - 0.5f * g.dx); }
+__device__ __forceinline__ float vertex_py(const DevGeom& g, int vy) { return fmaf((float)vy, g.dy, g.y0 - 0.5f * g.dy); }
+
+// Centred channel coordinate (channel units, fan angle 0 -> 0) of the point (px, py).
+// Explicit fmaf/__fmul_rn pin the rounding, so every kernel gets identical bits.
+__device__ __forceinline__ float vertex_ch(const DevGeom& g, float sb, float cb, float px, float py) {
+    const float along = fmaf(px, sb, fmaf(-py, cb, g.dso));   // > 0: the image is inside the orbit
+    const float perp = fmaf(px, cb, __fmul_rn(py, sb));
+    return __fmul_rn(fast_atan(__fdividef(perp, along)), g.dsd_ds);
+}
+
+// Left edge of detector bin c in centred channel units (bin c spans [L(c), L(c + 1)]);
+// cedge = cbase + 1/2 is rounded once on the host, so L(c) is the same float everywhere.
+__device__ __forceinline__ float bin_edge(const DevGeom& g, int c) { return __fsub_rn((float)c, g.cedge); }
+
+// Footprint of one pixel for one view (centred channel units).
+struct Foot2 {
+    float t0, t1, t2, t3;   // sorted breakpoints
+    float lphi;             // A1 amplitude dx / max(|cos phi0|, |sin phi0|)
+    int cA, n;              // first channel, channel count (n <= 0: off the detector)
+    bool clL, clR;          // footprint clipped by the detector's left / right edge
+};
+
+// CLAMP = false (forward tiles): cA / n describe the unclipped footprint (bins may lie off
+// the detector; the caller drops them).  Bin edges are evaluated from the channel index
+// alone (bin_edge), so the on-detector weights are bit-identical to the clamped ones.
+template <bool CLAMP = true>
+__device__ __forceinline__ void pixel_foot(const DevGeom& g, float sb, float cb, float xc, float yc, float v00, float v10,
+                                           float v01, float v11, Foot2& f) {
+    // The projections of the two diagonals overlap (they cross inside the pixel), so
+    // sorting each diagonal's pair gives the breakpoints with 4 more min/max.
+    const float a0 = fminf(v00, v11), a1 = fmaxf(v00, v11);
+    const float b0 = fminf(v10, v01), b1 = fmaxf(v10, v01);
+    f.t0 = fminf(a0, b0); f.t1 = fmaxf(a0, b0);
+    f.t2 = fminf(a1, b1); f.t3 = fmaxf(a1, b1);
+    const float dirx = fabsf(fmaf(g.dso, sb, xc)), diry = fabsf(fmaf(-g.dso, cb, yc));
+    const float lo = fminf(dirx, diry), hi = fmaxf(dirx, diry);
+    const float r = __fdividef(lo, hi);
+    f.lphi = __fmul_rn(g.dx, sqrt_approx(fmaf(r, r, 1.0f)));
+    int a = __float2int_rd(__fadd_rn(f.t0, g.cedge));
+    int b = __float2int_rd(__fadd_rn(f.t3, g.cedge));
+    if (CLAMP) {
+        f.clL = a < 0;
+        f.clR = b > g.ns - 1;
+        a = max(a, 0);
+        b = min(b, g.ns - 1);
+    } else {
+        f.clL = f.clR = false;
+    }
+    f.cA = a;
+    f.n = b - a + 1;
+}
+
+// Unit-height trapezoid CDF in coordinates u = s - t0 (branch-free, degenerate widths
+// safe).  F(u) = a^2/(2 w1) + m + b - b^2/(2 w3) with a, m, b the clamped pieces.
+struct Trap2 {
+    float t0, w1, t2r, t3r, h0, h3, mass;
+    __device__ __forceinline__ explicit Trap2(const Foot2& f) {
+        t0 = f.t0;
+        w1 = __fsub_rn(f.t1, f.t0);
+        t2r = __fsub_rn(f.t2, f.t0);
+        t3r = __fsub_rn(f.t3, f.t0);
+        h0 = __fdividef(0.5f, fmaxf(w1, 1e-20f));
+        h3 = __fdividef(0.5f, fmaxf(__fsub_rn(t3r, t2r), 1e-20f));
+        mass = __fmul_rn(0.5f, __fsub_rn(__fadd_rn(t3r, t2r), w1));   // (t3 + t2 - t1 - t0) / 2
+    }
+    __device__ __forceinline__ float F(float u) const {
+        const float a = fminf(fmaxf(u, 0.0f), w1);
+        const float m = __fsub_rn(fminf(fmaxf(u, w1), t2r), w1);
+        const float b = __fsub_rn(fminf(fmaxf(u, t2r), t3r), t2r);
+        return fmaf(-__fmul_rn(b, b), h3, fmaf(__fmul_rn(a, a), h0, __fadd_rn(m, b)));
+    }
+    // CDF at the left edge of bin c
+    __device__ __forceinline__ float at(const DevGeom& g, int c) const { return F(__fsub_rn(bin_edge(g, c), t0)); }
+};
+
+// sum_j lphi F_s(cA + j) yk[j]: the n - 1 interior bin edges are evaluated once each.
+__device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, const float* __restrict__ yk) {
+    const Trap2 T(f);
+    // F = 0 left of t0 and F = mass right of t3: only clipped ends need an evaluation
+    float Fp = f.clL ? T.at(g, f.cA) : 0.0f, s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kMaxFoot - 1; j++) {
+        if (j + 1 >= f.n) break;
+        const float Fn = T.at(g, f.cA + j + 1);
+        s = fmaf(__fsub_rn(Fn, Fp), __ldg(&yk[j]), s);
+        Fp = Fn;
+    }
+    const float Fend = f.clR ? T.at(g, f.cA + f.n) : T.mass;
+    s = fmaf(__fsub_rn(Fend, Fp), __ldg(&yk[f.n - 1]), s);
+    return f.lphi * s;
+}
+
+// ---------------------------------------------------------------------------
+// K1 (2D fan): pixel-driven forward projection with a deterministic reduction
+// ---------------------------------------------------------------------------
+// CTA = (32x32 pixel tile, chunk of kF2VC views).  Per view:
+//  (a) the tile's 33x33 vertex positions go to shared memory (1.06 atan per pixel),
+//      together with their extremes (the tile's channel span);
+//  (b) warp = one pixel row (or column, whichever the rays cross more steeply), lane =
+//      pixel; round j (warp-uniform) adds lane l's weight of bin cA_l + j times x_l into
+//      the warp's shared channel buffer l % P.  Lanes l and l + P have different cA
+//      (consecutive pixels advance >= 1/P channel, validated at create), so every add in
+//      one instruction goes to a distinct address: no atomics, fixed order;
+//  (c) the 8 x P buffers are summed in fixed order over the tile's channel span and
+//      added to the 64-bit fixed-point accumulator acc[k][c] (2^-32 units) with integer
+//      atomics, which are exact and order-independent: the result is bit-reproducible.
+//      fwd2d_finalize converts, applies the residual epilogue r = scale W (Ax - y) and
+//      re-zeroes acc.
+constexpr int kF2T = 32;      // tile edge (pixels)
+constexpr int kF2VC = 8;      // views per CTA
+constexpr float kFix = 4294967296.0f;   // 2^32
+
+__global__ void __launch_bounds__(256) fwd2d_tile_kernel(DevGeom g, int first, int stride, int count,
+                                                        const float* __restrict__ x,
+                                                        unsigned long long* __restrict__ acc) {
+    extern __shared__ float wb[];                 // [8 warps][P][SPAN]
+    __shared__ float xs[kF2T][kF2T + 1];
+    __shared__ float V[kF2T + 1][kF2T + 1];
+    __shared__ float red[2][8];
+    const int P = g.fpar, SPAN = g.fspan;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int vx0 = blockIdx.x * kF2T, vy0 = blockIdx.y * kF2T;
+    const int nvx = min(kF2T, g.nx - vx0), nvy = min(kF2T, g.ny - vy0);   // valid pixels in the tile
+    bool any = false;
+    for (int e = tid; e < kF2T * kF2T; e += 256) {
+        const int j = e >> 5, i = e & 31;
+        const float v = (i < nvx && j < nvy) ? __ldg(&x[(vy0 + j) * g.nx + vx0 + i]) : 0.0f;
+        xs[j][i] = v;
+        any |= v != 0.0f;
+    }
+    if (!__syncthreads_or(any)) return;   // nothing to project from this tile
+    for (int e = tid; e < 8 * P * SPAN; e += 256) wb[e] = 0.0f;
+    float* mybuf = wb + (w * P + lane % P) * SPAN;
+    const int k0 = blockIdx.z * kF2VC, k1 = min(count, k0 + kF2VC);
+    const float xcen = g.x0 + (vx0 + 0.5f * (nvx - 1)) * g.dx, ycen = g.y0 + (vy0 + 0.5f * (nvy - 1)) * g.dy;
+    // this thread's vertex coordinates (view-independent)
+    const float pxl = vertex_px(g, vx0 + lane), pxe = vertex_px(g, vx0 + kF2T);
+    const float pyl = vertex_py(g, vy0 + lane), pye = vertex_py(g, vy0 + kF2T);
+    float pyr[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) pyr[r] = vertex_py(g, vy0 + w + 8 * r);
+    for (int k = k0; k < k1; k++) {
+        const float4 vw = __ldg(&g.views[first + k * stride]);
+        const float sb = vw.x, cb = vw.y;
+        float vmin = 3.0e38f, vmax = -3.0e38f;
+        auto put = [&](int j, int i, float px, float py) {
+            if (i <= nvx && j <= nvy) {
+                const float t = vertex_ch(g, sb, cb, px, py);
+                V[j][i] = t;
+                vmin = fminf(vmin, t);
+                vmax = fmaxf(vmax, t);
+            }
+        };
+#pragma unroll
+        for (int r = 0; r < 4; r++) put(w + 8 * r, lane, pxl, pyr[r]);
+        if (w == 0) put(kF2T, lane, pxl, pye);         // top vertex row
+        else if (w == 1) put(lane, kF2T, pxe, pyl);    // right vertex column
+        else if (w == 2 && lane == 0) put(kF2T, kF2T, pxe, pye);
+        // channel span of the tile = extremes of its vertex table (a bound for every pixel)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+            vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        }
+        if (lane == 0) { red[0][w] = vmin; red[1][w] = vmax; }
+        __syncthreads();
+        float tmin = red[0][0], tmax = red[1][0];
+#pragma unroll
+        for (int i = 1; i < 8; i++) { tmin = fminf(tmin, red[0][i]); tmax = fmaxf(tmax, red[1][i]); }
+        const int cLoU = __float2int_rd(__fadd_rn(tmin, g.cedge));   // unclipped span
+        const int cHiU = __float2int_rd(__fadd_rn(tmax, g.cedge));
+        const bool hit = cHiU >= 0 && cLoU <= g.ns - 1;
+        if (hit) {
+            // rays cross rows steeply (|d_y| >= |d_x|): warps walk rows, lanes = ix
+            const bool rowmode = fabsf(ycen - g.dso * cb) >= fabsf(xcen + g.dso * sb);
+#pragma unroll 1
+            for (int q = 0; q < kF2T / 8; q++) {
+                const int il = rowmode ? lane : w + 8 * q, jl = rowmode ? w + 8 * q : lane;
+                const float xv = xs[jl][il];
+                const bool act = xv != 0.0f;
+                Foot2 f;
+                int n = 0;
+                if (act) {
+                    pixel_foot<false>(g, sb, cb, fmaf((float)(vx0 + il), g.dx, g.x0), fmaf((float)(vy0 + jl), g.dy, g.y0),
+                                      V[jl][il], V[jl][il + 1], V[jl + 1][il], V[jl + 1][il + 1], f);
+                    n = f.n;
+                }
+                const int nmax = __reduce_max_sync(0xffffffffu, n);
+                if (nmax == 0) continue;
+                const Trap2 T(f);
+                const float lx = f.lphi * xv;
+                float* bp = mybuf + (f.cA - cLoU);
+                float Fp = 0.0f;   // unclipped: F = 0 at the left edge of bin cA
+#pragma unroll
+                for (int j = 0; j < kMaxFoot; j++) {
+                    if (j >= nmax) break;
+                    // bins j >= n add exactly 0 (Fn = Fp = mass) to distinct addresses
+                    const float Fn = (j + 1 < n) ? T.at(g, f.cA + j + 1) : T.mass;
+                    if (act) bp[j] += lx * __fsub_rn(Fn, Fp);
+                    Fp = Fn;
+                    __syncwarp();   // round j's stores are visible to round j + 1's loads
+                }
+            }
+        }
+        __syncthreads();
+        if (hit) {
+            const int span = cHiU - cLoU + 1;
+            unsigned long long* ak = acc + (size_t)k * g.ns;
+            for (int t = tid; t < span; t += 256) {
+                float s = 0.0f;
+                for (int b = 0; b < 8 * P; b++) {
+                    s += wb[b * SPAN + t];
+                    wb[b * SPAN + t] = 0.0f;
+                }
+                const int c = cLoU + t;
+                if (s != 0.0f && c >= 0 && c < g.ns) atomicAdd(ak + c, (unsigned long long)__float2ll_rn(s * kFix));
+            }
+        }
+        // the next view's vertex phase writes V only after every warp passed this barrier
+        __syncthreads();
+    }
+}
+
+// out[k][c] = acc * 2^-32 (RESID: scale W (Ax - y)); acc is re-zeroed for the next launch.
+template <bool RESID>
+__global__ void __launch_bounds__(256) fwd2d_finalize_kernel(DevGeom g, int first, int stride, int count,
+                                                            unsigned long long* __restrict__ acc, float* __restrict__ out,
+                                                            const float* __restrict__ yobs, const float* __restrict__ wts,
+                                                            float scale) {
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= count * g.ns) return;
+    const long long q = (long long)acc[i];
+    acc[i] = 0ull;
+    const float s = (float)((double)q * (1.0 / 4294967296.0));
+    if (RESID) {
+        const int k = i / g.ns, c = i - k * g.ns;
+        const size_t gi = (size_t)(first + k * stride) * g.ns + c;
+        const float yo = yobs ? __ldg(&yobs[gi]) : 0.0f;
+        out[i] = scale * __ldg(&wts[gi]) * (s - yo);
+    } else {
+        out[i] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2 (2D fan): voxel-driven back projection, one thread per pixel
+// ---------------------------------------------------------------------------
+// CTA = 32x8 pixel tile.  Per batch of kB2VB views the warps fill the tile's 33x9
+// vertex table for every view (warp w: vertex row w; the top row and right column of
+// view kk by warp kk % 8), then thread = pixel walks the batch's views.
+constexpr int kB2VB = 16;   // views per vertex-table batch
+
+template <int EPI>
+__global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int stride, int count,
+                                                    const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
+    __shared__ float V[kB2VB][9][33];
+    __shared__ float2 SC[kB2VB];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ix = blockIdx.x * 32 + lane;
+    const int iy = blockIdx.y * 8 + w;
+    const bool valid = ix < g.nx && iy < g.ny;
+    const size_t jv = (size_t)(valid ? iy : 0) * g.nx + (valid ? ix : 0);
+    // voxels outside the support S are not needed by OS-LALM / D_L: skip their views
+    const bool act = valid && (ga.mask == nullptr || ga.mask[jv]);
+    float acc = 0.0f;
+    if (__syncthreads_or(act)) {
+        const int vx0 = blockIdx.x * 32, vy0 = blockIdx.y * 8;
+        const float pxl = vertex_px(g, vx0 + lane), pxe = vertex_px(g, vx0 + 32);
+        const float pyw = vertex_py(g, vy0 + w), pye = vertex_py(g, vy0 + 8), pyl = vertex_py(g, vy0 + min(lane, 8));
+        const float xc = fmaf((float)ix, g.dx, g.x0), yc = fmaf((float)iy, g.dy, g.y0);
+        for (int kb = 0; kb < count; kb += kB2VB) {
+            const int nb = min(kB2VB, count - kb);
+            for (int kk = 0; kk < nb; kk++) {
+                const float4 vw = __ldg(&g.views[first + (kb + kk) * stride]);
+                V[kk][w][lane] = vertex_ch(g, vw.x, vw.y, pxl, pyw);
+                if ((kk & 7) == w) {
+                    V[kk][8][lane] = vertex_ch(g, vw.x, vw.y, pxl, pye);                   // top row
+                    if (lane <= 8) V[kk][lane][32] = vertex_ch(g, vw.x, vw.y, pxe, pyl);   // right column
+                    if (lane == 0) SC[kk] = make_float2(vw.x, vw.y);
+                }
+            }
+            __syncthreads();
+            if (act) {
+                for (int kk = 0; kk < nb; kk++) {
+                    const float2 sc = SC[kk];
+                    Foot2 f;
+                    pixel_foot(g, sc.x, sc.y, xc, yc, V[kk][w][lane], V[kk][w][lane + 1], V[kk][w + 1][lane],
+                               V[kk][w + 1][lane + 1], f);
+                    if (f.n <= 0) continue;
+                    acc += foot_dot(g, f, y + (size_t)(kb + kk) * g.ns + f.cA);
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const size_t j = (size_t)iy * g.nx + ix;
+    const double xi = back_epilogue<EPI>(j, valid, acc, x, ga);
+    if (EPI == EPI_GUPD) {
+        block_sum_store<256>(xi, &ga.xi_part[blockIdx.y * gridDim.x + blockIdx.x]);
+        xi_arrive<256>(ga, gridDim.x * gridDim.y);
+    }
+}
+
+}  // namespace ct

@@ -1,7 +1,7 @@
 // ct_kernels.cuh — sm_100a kernels of the OS-LALM hot path.
 //
-//   K1  fwd2d / fwd3d   : y_k = A_v x (+ fused weighted residual r = s W (A x - y))
-//   K2  back2d / back3d : x = A_v' y  (+ fused g-update / restart-indicator epilogue) P:391-395
+//   K1  fwd3d (fwd2d in ct_fan2d.cuh): y_k = A_v x (+ fused weighted residual r = s W (A x - y))
+//   K2  back3d (back2d in ct_fan2d.cuh): x = A_v' y  (+ fused g-update / restart-indicator epilogue) P:391-395
 //   K3  sqs_update      : rho-scaled non-negative SQS step with the Fair stencil
 //   K4  xi_finalize     : fixed-order fp64 sum of xi, counter l and rho_l update
 //   K5  (setup)         : D_L = A'(W A 1_S) from K1/K2 + mask finalisation
@@ -81,125 +81,6 @@ __device__ __forceinline__ void wedge_line(const DevGeom& g, const Wedge& w, int
         float u0 = (fminf(a, b) - g.y0) / g.dy - w.margin, u1 = (fmaxf(a, b) - g.y0) / g.dy + w.margin;
         lo = max(0, __float2int_ru(u0));
         hi = min(g.ny - 1, __float2int_rd(u1));
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Register sliding window of kMaxFoot channel accumulators.
-// Contributions arrive in non-decreasing first-channel order along a line.
-// ---------------------------------------------------------------------------
-struct Window {
-    float acc[kMaxFoot];
-    int base;
-    __device__ __forceinline__ void reset(int b) {
-        base = b;
-#pragma unroll
-        for (int k = 0; k < kMaxFoot; k++) acc[k] = 0.0f;
-    }
-};
-
-// ---------------------------------------------------------------------------
-// K1 (2D fan): forward projection of one (view, channel tile)
-// ---------------------------------------------------------------------------
-// CTA = (tile of TC channels, view k).  Each thread owns whole sweep lines of
-// the tile's wedge, walks their pixels in channel order, computes each pixel's
-// footprint once and accumulates into a register window; window flushes go to
-// the thread's private smem column, which a fixed-order reduction sums.
-template <int TC, int NTHR, bool RESID>
-__global__ void __launch_bounds__(NTHR) fwd2d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
-                                                     float* __restrict__ out, const float* __restrict__ yobs,
-                                                     const float* __restrict__ wts, float scale) {
-    __shared__ float P[TC][NTHR + 1];
-    const int c0 = blockIdx.x * TC;
-    const int k = blockIdx.y;
-    const int v = first + k * stride;
-    const float4 vw = g.views[v];
-    const float sb = vw.x, cb = vw.y;
-    const int tid = threadIdx.x;
-#pragma unroll
-    for (int c = 0; c < TC; c++) P[c][tid] = 0.0f;
-    Wedge w = make_wedge(g, sb, cb, c0, TC);
-    for (int L = tid; L < w.nlines; L += NTHR) {
-        int lo, hi;
-        wedge_line(g, w, L, lo, hi);
-        if (lo > hi) continue;
-        Window win;
-        win.reset(-1000000);
-        int n_in = hi - lo + 1;
-        for (int q = 0; q < n_in; q++) {
-            int u = w.increasing ? lo + q : hi - q;
-            int ix = w.rows ? u : L, iy = w.rows ? L : u;
-            float xv = __ldg(&x[iy * g.nx + ix]);
-            if (xv == 0.0f) continue;
-            Trans tr;
-            transaxial(g, sb, cb, g.x0 + ix * g.dx, g.y0 + iy * g.dy, tr);
-            int cA, n;
-            bool clL, clR;
-            foot_range_ends(g, tr, cA, n, clL, clR);
-            if (n <= 0 || cA + n <= c0 || cA >= c0 + TC) continue;
-            TrapCdf F(tr);
-            float lx = tr.lphi * xv;
-            if (cA >= win.base) {
-                // shift the window so that base == cA, flushing channels that are done
-                while (win.base < cA) {
-                    int cc = win.base - c0;
-                    if (cc >= 0 && cc < TC) P[cc][tid] += win.acc[0];
-#pragma unroll
-                    for (int j = 0; j < kMaxFoot - 1; j++) win.acc[j] = win.acc[j + 1];
-                    win.acc[kMaxFoot - 1] = 0.0f;
-                    win.base++;
-                    if (win.base < cA - kMaxFoot) {  // jump: everything left is zero
-                        int jmp = cA - win.base;
-#pragma unroll
-                        for (int j = 0; j < kMaxFoot; j++) {
-                            int c1 = win.base + j - c0;
-                            if (c1 >= 0 && c1 < TC && win.acc[j] != 0.0f) P[c1][tid] += win.acc[j];
-                        }
-                        win.reset(win.base + jmp);
-                    }
-                }
-                const float e = (float)cA - 0.5f - tr.cc;
-                // interior bin edges only: F = 0 left of t0 and F = total right of t3
-                float Fp = clL ? F(e) : 0.0f;
-                const float Fend = clR ? F(e + (float)n) : 0.5f * (tr.t3 + tr.t2 - tr.t1 - tr.t0);
-#pragma unroll
-                for (int j = 0; j < kMaxFoot; j++) {
-                    if (j >= n) break;
-                    const float Fn = (j + 1 < n) ? F(e + (float)(j + 1)) : Fend;
-                    win.acc[j] += lx * (Fn - Fp);
-                    Fp = Fn;
-                }
-            } else {
-                // out-of-order footprint (rounding at a line end): direct smem adds
-                for (int j = 0; j < n; j++) {
-                    int c = cA + j - c0;
-                    if (c >= 0 && c < TC) P[c][tid] += xv * chan_weight(F, tr.cc, tr.lphi, cA + j);
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kMaxFoot; j++) {
-            int c = win.base + j - c0;
-            if (c >= 0 && c < TC) P[c][tid] += win.acc[j];
-        }
-    }
-    __syncthreads();
-    // fixed-order reduction over threads: NTHR/TC threads per channel
-    constexpr int PER = NTHR / TC;
-    int c = tid / PER, part = tid % PER;
-    float s = 0.0f;
-    for (int t = part; t < NTHR; t += PER) s += P[c][t];
-#pragma unroll
-    for (int o = PER / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, PER);
-    if (part == 0 && c0 + c < g.ns) {
-        size_t oi = (size_t)k * g.ns + c0 + c;
-        if (RESID) {
-            size_t gi = (size_t)v * g.ns + c0 + c;
-            float yo = yobs ? __ldg(&yobs[gi]) : 0.0f;
-            out[oi] = scale * __ldg(&wts[gi]) * (s - yo);
-        } else {
-            out[oi] = s;
-        }
     }
 }
 
@@ -360,7 +241,6 @@ __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, in
     const float sb = vw.x, cb = vw.y;
     const int gi = threadIdx.x / NTP, r = threadIdx.x % NTP;
     const bool row_ok = r < g.nt;
-    const float qr_off = ((float)r - g.rbase);
     Foot* tab = table + gi * NTP;
     float acc[TC];
 #pragma unroll
@@ -557,54 +437,6 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
         if (ga.mask[j]) return (double)(gg - Gp) * (double)(Gp - G);
     }
     return 0.0;
-}
-
-// ---------------------------------------------------------------------------
-// K2 (2D fan): voxel-driven back projection, one thread per pixel
-// ---------------------------------------------------------------------------
-template <int EPI>
-__global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int stride, int count,
-                                                    const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
-    const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int iy = blockIdx.y * 8 + (threadIdx.x >> 5);
-    const bool valid = ix < g.nx && iy < g.ny;
-    const size_t jv = (size_t)(valid ? iy : 0) * g.nx + (valid ? ix : 0);
-    // voxels outside the support S are not needed by OS-LALM / D_L: skip their views
-    const bool act = valid && (ga.mask == nullptr || ga.mask[jv]);
-    float acc = 0.0f;
-    if (act) {
-        const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
-        for (int k = 0; k < count; k++) {
-            const float4 vw = g.views[first + k * stride];
-            Trans tr;
-            transaxial(g, vw.x, vw.y, xc, yc, tr);
-            int cA, n;
-            bool clL, clR;
-            foot_range_ends(g, tr, cA, n, clL, clR);
-            if (n <= 0) continue;
-            TrapCdf F(tr);
-            const float* yk = y + k * g.ns + cA;
-            const float e = (float)cA - 0.5f - tr.cc;
-            // interior bin edges only: F = 0 left of t0 and F = total right of t3
-            float Fp = clL ? F(e) : 0.0f, s = 0.0f;
-#pragma unroll
-            for (int j = 0; j < kMaxFoot - 1; j++) {
-                if (j + 1 >= n) break;
-                const float Fn = F(e + (float)(j + 1));
-                s += (Fn - Fp) * __ldg(&yk[j]);
-                Fp = Fn;
-            }
-            const float Fend = clR ? F(e + (float)n) : 0.5f * (tr.t3 + tr.t2 - tr.t1 - tr.t0);
-            s += (Fend - Fp) * __ldg(&yk[n - 1]);
-            acc += tr.lphi * s;
-        }
-    }
-    size_t j = (size_t)iy * g.nx + ix;
-    double xi = back_epilogue<EPI>(j, valid, acc, x, ga);
-    if (EPI == EPI_GUPD) {
-        block_sum_store<256>(xi, &ga.xi_part[blockIdx.y * gridDim.x + blockIdx.x]);
-        xi_arrive<256>(ga, gridDim.x * gridDim.y);
-    }
 }
 
 // ---------------------------------------------------------------------------
