@@ -118,6 +118,16 @@ def allreduce_max(v, ws):
     return float(t.item())
 
 
+def load_traffic(config_id):
+    """DRAM bytes per launch of each bench step from one committed `ncu --set full` capture
+    (profiles/traffic.json, written by tools/ncu_traffic.py); {} if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(config_id, {})
+    except Exception:
+        return {}
+
+
 def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
@@ -320,14 +330,17 @@ def main():
     N = int(np.prod(geo.img_shape))
     upd_ms = kt["sqs_update"][0] / max(kt["sqs_update"][1], 1)
     upd_bytes = 21 * N        # x, G, g, D_L read (16 B) + mask (1 B) + x' write (4 B) per voxel
+    traffic = load_traffic(cfg.name)
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["fp32_tflops"], "traffic": None,
+                "frac": achieved / pk["fp32_tflops"], "traffic": traffic.get(dom, {}).get("bytes_per_launch"),
+                "traffic_src": traffic.get(dom, {}).get("src"),
                 "peak_src": f"derived: {N_SM} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
                 "flop_per_launch": flop_launch, "ms_per_launch": ms_launch,
                 "share_of_step": kt[dom][0] / total_kt}
     streaming = {"bound": "hbm", "kernel": "sqs_update", "achieved": upd_bytes / (upd_ms / 1e3) / 1e9,
                  "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": upd_bytes / (upd_ms / 1e3) / 1e9 / pk["hbm_gbs"],
-                 "traffic": None, "bytes_per_launch": upd_bytes, "ms_per_launch": upd_ms}
+                 "traffic": traffic.get("sqs_update", {}).get("bytes_per_launch"), "bytes_per_launch": upd_bytes,
+                 "ms_per_launch": upd_ms}
     kernel_ms = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / total_kt} for k, v in kt.items() if v[1]}
 
     # ---- end to end: host (pinned) inputs in, image out, inside the timed region

@@ -26,22 +26,29 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = None, extra=()) -> str:
+    """Build libct_oslalm.so (or a tuning variant at `out` with extra nvcc flags, e.g. -D...)."""
+    lib = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, os.path.join(HERE, "csrc", "ct_abi.cu"), "-ldl"]
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, *extra, "-o", tmp, os.path.join(HERE, "csrc", "ct_abi.cu"), "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libct_oslalm.so")
-    with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+    if out is None:
+        with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
+            f.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_1402_4381_b200.build [--force] [--out PATH -DNAME=V ...]
+    a = sys.argv[1:]
+    out = a[a.index("--out") + 1] if "--out" in a else None
+    extra = [x for x in a if x.startswith("-D")]
+    print(build(force="--force" in a, verbose=out is None, out=out, extra=extra))

@@ -97,7 +97,13 @@ struct Trap2 {
 };
 
 // sum_j lphi F_s(cA + j) yk[j]: the n - 1 interior bin edges are evaluated once each.
+constexpr int kPre = 4;   // prefetched bins
 __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, const float* __restrict__ yk) {
+    // issue the bin loads before the CDF arithmetic (latency hiding)
+    float yv[kPre];
+#pragma unroll
+    for (int j = 0; j < kPre; j++) yv[j] = (j + 1 < f.n) ? __ldg(&yk[j]) : 0.0f;
+    const float ylast = __ldg(&yk[f.n - 1]);
     const Trap2 T(f);
     // F = 0 left of t0 and F = mass right of t3: only clipped ends need an evaluation
     float Fp = f.clL ? T.at(g, f.cA) : 0.0f, s = 0.0f;
@@ -105,11 +111,11 @@ __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, cons
     for (int j = 0; j < kMaxFoot - 1; j++) {
         if (j + 1 >= f.n) break;
         const float Fn = T.at(g, f.cA + j + 1);
-        s = fmaf(__fsub_rn(Fn, Fp), __ldg(&yk[j]), s);
+        s = fmaf(__fsub_rn(Fn, Fp), j < kPre ? yv[j < kPre ? j : 0] : __ldg(&yk[j]), s);
         Fp = Fn;
     }
     const float Fend = f.clR ? T.at(g, f.cA + f.n) : T.mass;
-    s = fmaf(__fsub_rn(Fend, Fp), __ldg(&yk[f.n - 1]), s);
+    s = fmaf(__fsub_rn(Fend, Fp), ylast, s);
     return f.lphi * s;
 }
 
@@ -117,8 +123,7 @@ __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, cons
 // K1 (2D fan): pixel-driven forward projection with a deterministic reduction
 // ---------------------------------------------------------------------------
 // CTA = (32x32 pixel tile, chunk of kF2VC views).  Per view:
-//  (a) the tile's 33x33 vertex positions go to shared memory (1.06 atan per pixel),
-//      together with their extremes (the tile's channel span);
+//  (a) the tile's 33x33 vertex positions go to shared memory (1.06 atan per pixel);
 //  (b) warp = one pixel row (or column, whichever the rays cross more steeply), lane =
 //      pixel; round j (warp-uniform) adds lane l's weight of bin cA_l + j times x_l into
 //      the warp's shared channel buffer l % P.  Lanes l and l + P have different cA
@@ -129,17 +134,22 @@ __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, cons
 //      atomics, which are exact and order-independent: the result is bit-reproducible.
 //      fwd2d_finalize converts, applies the residual epilogue r = scale W (Ax - y) and
 //      re-zeroes acc.
+#ifndef CT_FWD2D_MINB
+#define CT_FWD2D_MINB 1   // min resident CTAs per SM for the register budget (tuning: -D; 4-6 measured slower)
+#endif
+#ifndef CT_BACK2D_MINB
+#define CT_BACK2D_MINB 1
+#endif
 constexpr int kF2T = 32;      // tile edge (pixels)
 constexpr int kF2VC = 8;      // views per CTA
 constexpr float kFix = 4294967296.0f;   // 2^32
 
-__global__ void __launch_bounds__(256) fwd2d_tile_kernel(DevGeom g, int first, int stride, int count,
+__global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom g, int first, int stride, int count,
                                                         const float* __restrict__ x,
                                                         unsigned long long* __restrict__ acc) {
     extern __shared__ float wb[];                 // [8 warps][P][SPAN]
     __shared__ float xs[kF2T][kF2T + 1];
     __shared__ float V[kF2T + 1][kF2T + 1];
-    __shared__ float red[2][8];
     const int P = g.fpar, SPAN = g.fspan;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int vx0 = blockIdx.x * kF2T, vy0 = blockIdx.y * kF2T;
@@ -165,31 +175,25 @@ __global__ void __launch_bounds__(256) fwd2d_tile_kernel(DevGeom g, int first, i
     for (int k = k0; k < k1; k++) {
         const float4 vw = __ldg(&g.views[first + k * stride]);
         const float sb = vw.x, cb = vw.y;
-        float vmin = 3.0e38f, vmax = -3.0e38f;
-        auto put = [&](int j, int i, float px, float py) {
-            if (i <= nvx && j <= nvy) {
-                const float t = vertex_ch(g, sb, cb, px, py);
-                V[j][i] = t;
-                vmin = fminf(vmin, t);
-                vmax = fmaxf(vmax, t);
-            }
-        };
+        if (nvx == kF2T && nvy == kF2T) {   // full tile (uniform branch): no bounds checks
 #pragma unroll
-        for (int r = 0; r < 4; r++) put(w + 8 * r, lane, pxl, pyr[r]);
-        if (w == 0) put(kF2T, lane, pxl, pye);         // top vertex row
-        else if (w == 1) put(lane, kF2T, pxe, pyl);    // right vertex column
-        else if (w == 2 && lane == 0) put(kF2T, kF2T, pxe, pye);
-        // channel span of the tile = extremes of its vertex table (a bound for every pixel)
+            for (int r = 0; r < 4; r++) V[w + 8 * r][lane] = vertex_ch(g, sb, cb, pxl, pyr[r]);
+            if (w == 0) V[kF2T][lane] = vertex_ch(g, sb, cb, pxl, pye);          // top vertex row
+            else if (w == 1) V[lane][kF2T] = vertex_ch(g, sb, cb, pxe, pyl);     // right vertex column
+            else if (w == 2 && lane == 0) V[kF2T][kF2T] = vertex_ch(g, sb, cb, pxe, pye);
+        } else {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
-            vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+            for (int r = 0; r < 4; r++)
+                if (lane <= nvx && w + 8 * r <= nvy) V[w + 8 * r][lane] = vertex_ch(g, sb, cb, pxl, pyr[r]);
+            if (w == 0 && lane <= nvx) V[nvy][lane] = vertex_ch(g, sb, cb, pxl, vertex_py(g, vy0 + nvy));
+            else if (w == 1 && lane <= nvy) V[lane][nvx] = vertex_ch(g, sb, cb, vertex_px(g, vx0 + nvx), pyl);
         }
-        if (lane == 0) { red[0][w] = vmin; red[1][w] = vmax; }
         __syncthreads();
-        float tmin = red[0][0], tmax = red[1][0];
-#pragma unroll
-        for (int i = 1; i < 8; i++) { tmin = fminf(tmin, red[0][i]); tmax = fmaxf(tmax, red[1][i]); }
+        // channel span of the tile: u -> perp/along is linear-fractional, so the arc position is
+        // quasi-linear and its extremes over the (convex) tile are at the corners; the margin
+        // covers the fp32 error of the vertex values (< 1e-4 channel)
+        const float q0 = V[0][0], q1 = V[0][nvx], q2 = V[nvy][0], q3 = V[nvy][nvx];
+        const float tmin = fminf(fminf(q0, q1), fminf(q2, q3)) - 2e-3f, tmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)) + 2e-3f;
         const int cLoU = __float2int_rd(__fadd_rn(tmin, g.cedge));   // unclipped span
         const int cHiU = __float2int_rd(__fadd_rn(tmax, g.cedge));
         const bool hit = cHiU >= 0 && cLoU <= g.ns - 1;
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(256) fwd2d_finalize_kernel(DevGeom g, int firs
 constexpr int kB2VB = 16;   // views per vertex-table batch
 
 template <int EPI>
-__global__ void __launch_bounds__(256) back2d_kernel(DevGeom g, int first, int stride, int count,
+__global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, int first, int stride, int count,
                                                     const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     __shared__ float V[kB2VB][9][33];
     __shared__ float2 SC[kB2VB];
