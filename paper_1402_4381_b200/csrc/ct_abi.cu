@@ -61,6 +61,9 @@ struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -76,11 +79,17 @@ static bool load_nccl() {
     g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
     g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
     g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+    g_nccl.ReduceScatter = (decltype(g_nccl.ReduceScatter))dlsym(h, "ncclReduceScatter");
+    g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
     g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
-    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter &&
+                g_nccl.AllGather && g_nccl.CommDestroy;
     return g_nccl.ok;
 }
+
+static const char* nccl_err(ncclResult_t r) { return g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error"; }
+
 
 // ---------------------------------------------------------------------------
 // geometry
@@ -92,9 +101,17 @@ struct ct_geom {
     float4* d_views = nullptr;
     double2* d_vz = nullptr;
     unsigned long long* acc2d = nullptr;   // fan 2D forward: [na][ns] 64-bit fixed-point sums (kept zero)
+    int2* ext3d = nullptr;                 // cone forward: nonzero column range per image row / column
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
 };
+
+static int allreduce(const ct_geom* g, float* buf, size_t n, cudaStream_t st) {
+    ncclResult_t r = g_nccl.AllReduce(buf, buf, n, ncclFloat32, ncclSum, g->comm, st);
+    if (r != ncclSuccess)
+        return fail(CT_ENCCL, "ncclAllReduce: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error");
+    return CT_OK;
+}
 
 static inline int nz_of(const ct_geom* g) { return g->d.kind == CT_FAN2D ? 1 : g->d.nz; }
 static inline int nt_of(const ct_geom* g) { return g->d.kind == CT_FAN2D ? 1 : g->d.nt; }
@@ -220,10 +237,12 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     if (e == cudaSuccess) e = cudaMemcpy(g->d_vz, hvz.data(), sizeof(double2) * d->na, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && is2d) e = cudaMalloc(&g->acc2d, sizeof(unsigned long long) * d->na * d->ns);
     if (e == cudaSuccess && is2d) e = cudaMemset(g->acc2d, 0, sizeof(unsigned long long) * d->na * d->ns);
+    if (e == cudaSuccess && !is2d) e = cudaMalloc(&g->ext3d, sizeof(int2) * (d->nx + d->ny));
     if (e != cudaSuccess) {
         cudaFree(g->d_views);
         cudaFree(g->d_vz);
         cudaFree(g->acc2d);
+        cudaFree(g->ext3d);
         delete g;
         return fail(e == cudaErrorMemoryAllocation ? CT_ENOMEM : CT_ECUDA, "geometry tables: %s", cudaGetErrorString(e));
     }
@@ -242,6 +261,7 @@ extern "C" void ct_geom_destroy(ct_geom* g) {
     cudaFree(g->d_views);
     cudaFree(g->d_vz);
     cudaFree(g->acc2d);
+    cudaFree(g->ext3d);
     delete g;
 }
 
@@ -257,14 +277,14 @@ static int check_views(const ct_geom* g, ct_views v) {
 // ---------------------------------------------------------------------------
 template <int TC, int NTP, bool RESID>
 static void launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const float* x, float* out, const float* yobs,
-                         const float* w, float scale, cudaStream_t st) {
+                         const float* w, float scale, const int2* ext, cudaStream_t st) {
     constexpr size_t smem = fwd3d_smem<TC, NTP, 256>();
     static bool configured = false;   // per template instance
     if (!configured) {
         cudaFuncSetAttribute(fwd3d_kernel<TC, NTP, 256, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    fwd3d_kernel<TC, NTP, 256, RESID><<<grid, 256, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale);
+    fwd3d_kernel<TC, NTP, 256, RESID><<<grid, 256, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
 }
 
 template <bool RESID>
@@ -286,14 +306,19 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
                                                                           yobs, w, scale);
         CT_LAUNCHED(1);
     } else {
+        // per line, the columns holding a nonzero voxel of x (trims the wedge walk)
+        const int next = dg.nx + dg.ny;
+        fwd3d_extent_init<<<(next + 255) / 256, 256, 0, st>>>(g->ext3d, next);
+        fwd3d_extent_kernel<<<(dg.nx * dg.ny + 7) / 8, 256, 0, st>>>(dg, x, g->ext3d);
         constexpr int TC = 16;
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32)
-            launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, st);
+            launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
         else if (dg.nt <= 64)
-            launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, st);
+            launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
         else
-            launch_fwd3d<TC, 128, RESID>(dg, grid, v, x, out, yobs, w, scale, st);
+            launch_fwd3d<TC, 128, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
+        CT_LAUNCHED(2);
     }
     CT_LAUNCHED(1);
     return CT_OK;
@@ -376,13 +401,17 @@ extern "C" int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask, flo
     size_t N = n_vox(g);
     float* one = (float*)scratch;
     float* sino = (float*)(((uintptr_t)(one + N) + 255) & ~(uintptr_t)255);
-    ct_views all{0, 1, g->d.na};
+    // multi-rank: this rank's contiguous block of all views, partial D_L summed with NCCL
+    int base = g->d.na / g->nranks, extra = g->d.na % g->nranks;
+    ct_views all{g->rank * base + std::min(g->rank, extra), 1, base + (g->rank < extra ? 1 : 0)};
     mask_to_float_kernel<<<nblk(N), 256, 0, st>>>(mask, one, N);
     CT_LAUNCHED(1);
     if (int e = launch_fwd<true>(g, all, one, sino, nullptr, w, 1.0f, st)) return e;
     GupdArgs ga{};
     ga.mask = mask;   // D_L is only needed on S (set to 0 elsewhere below)
     if (int e = launch_back<EPI_STORE>(g, all, sino, dl, ga, st)) return e;
+    if (g->comm)
+        if (int e = allreduce(g, dl, N, st)) return e;
     mask_finalize_kernel<<<nblk(N), 256, 0, st>>>(mask, dl, N);
     CT_LAUNCHED(1);
     return CT_OK;
@@ -455,6 +484,13 @@ struct ct_oslalm_state {
     float* Gtmp;
     float* sino;
     float* vbuf[2] = {nullptr, nullptr};
+    // multi-rank slab path: rank prank of P owns image rows [iy0, iy1), i.e.
+    // elements [off0, off0 + S) of every padded image buffer (P * S >= N elements)
+    int P = 1, prank = 0, slab = 0, iy0 = 0, iy1 = 0;
+    bool has_comm = false;
+    size_t S = 0, off0 = 0, Npad = 0;
+    float* xp[2] = {nullptr, nullptr};   // full images (all-gathered), ping-pong
+    double* xi_ex = nullptr;             // [0] this rank's xi, [1] all-reduced xi
     double* xi_part;
     Scalars* sc;
     double* dlog;        // M x 3 doubles (per iteration)
@@ -536,8 +572,24 @@ static int check_cfg(const ct_geom* g, const ct_oslalm_cfg* c) {
     return check_reg(g, &c->reg);
 }
 
+// Rows per slab for P ranks (the last slab may be short; buffers are padded to P * S).
+static void slab_geometry(const ct_geom* g, int P, int rank, int* iy0, int* iy1, size_t* S) {
+    int R = (g->d.ny + P - 1) / P;
+    *iy0 = std::min(g->d.ny, rank * R);
+    *iy1 = std::min(g->d.ny, (rank + 1) * R);
+    *S = (size_t)R * g->d.nx * nz_of(g);
+}
+
+static bool use_slabs(const ct_geom* g, const ct_oslalm_cfg* c) {
+    // FISTA's n stencil passes would need a halo exchange per pass: it keeps the all-reduce path
+    return g->comm != nullptr && c->inner == CT_INNER_SQS;
+}
+
 static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[12], size_t* total) {
-    size_t N = n_vox(g);
+    int iy0, iy1;
+    size_t S;
+    slab_geometry(g, g->nranks, g->rank, &iy0, &iy1, &S);
+    const size_t N = std::max(n_vox(g), (size_t)g->nranks * S);   // padded image length
     int maxcount = (g->d.na + c->M - 1) / c->M;
     size_t sino = (size_t)maxcount * n_cells_view(g);
     size_t nparts = std::max(back_nblocks(g), (size_t)nblk(N));
@@ -553,6 +605,9 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[12
     off[8] = o; o += align256((size_t)c->M * 3 * 8);  // device log
     const bool two_v = c->inner == CT_INNER_FISTA && c->n_inner > 1;
     off[9] = o; o += two_v ? 2 * align256(N * 4) : 0;  // FISTA extrapolation points v (ping-pong)
+    const bool slab = use_slabs(g, c);
+    off[10] = o; o += slab ? 2 * align256(N * 4) : 0;  // slab path: all-gathered full images (ping-pong)
+    off[11] = o; o += align256(2 * 8);                 // xi exchange
     *total = o;
 }
 
@@ -589,10 +644,22 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
     s->xi_part = (double*)(b + off[6]);
     s->sc = (Scalars*)(b + off[7]);
     s->dlog = (double*)(b + off[8]);
+    s->P = g->nranks;
+    s->prank = g->rank;
+    slab_geometry(g, s->P, s->prank, &s->iy0, &s->iy1, &s->S);
+    s->Npad = std::max(s->N, (size_t)s->P * s->S);
+    s->off0 = (size_t)s->prank * s->S;
+    s->slab = use_slabs(g, c) ? 1 : 0;
+    s->has_comm = g->comm != nullptr;
     if (c->inner == CT_INNER_FISTA && c->n_inner > 1) {
         s->vbuf[0] = (float*)(b + off[9]);
-        s->vbuf[1] = (float*)(b + off[9] + align256(s->N * 4));
+        s->vbuf[1] = (float*)(b + off[9] + align256(s->Npad * 4));
     }
+    if (s->slab) {
+        s->xp[0] = (float*)(b + off[10]);
+        s->xp[1] = (float*)(b + off[10] + align256(s->Npad * 4));
+    }
+    s->xi_ex = (double*)(b + off[11]);
     cudaError_t e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming);
@@ -656,12 +723,6 @@ static ct_views rank_views(const ct_geom* g, int M, int m) {
     return ct_views{m + k0 * M, M, n};
 }
 
-static int allreduce(const ct_geom* g, float* buf, size_t n, cudaStream_t st) {
-    ncclResult_t r = g_nccl.AllReduce(buf, buf, n, ncclFloat32, ncclSum, g->comm, st);
-    if (r != ncclSuccess)
-        return fail(CT_ENCCL, "ncclAllReduce: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error");
-    return CT_OK;
-}
 
 // G+ = M A_m'(W (A_m x - y)) for subset m with the requested epilogue.
 static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const float* x, int m, int epi, cudaStream_t st) {
@@ -695,7 +756,35 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
         tmark_end(s, st, 2, t1);
         return e;
     }
-    // multi-rank: partial back-projection (on S), NCCL sum, then the unfused epilogue
+    if (s->slab) {
+        // multi-rank slab path: partial back-projection (this rank's views), reduce-scatter of
+        // the padded image into this rank's row slab of G+, slab g-update + xi, all-reduce of
+        // the ranks' xi (8 bytes), K4 on every rank
+        float* Gnew = s->Gbuf[epi == EPI_INIT ? s->curG : s->curG ^ 1];
+        int t1 = tmark(s, st);
+        if (int e = launch_back<EPI_STORE>(g, v, s->sino, s->Gtmp, ga, st)) return e;
+        tmark_end(s, st, 2, t1);
+        int t2 = tmark(s, st);
+        ncclResult_t r = g_nccl.ReduceScatter(s->Gtmp, Gnew + s->off0, s->S, ncclFloat32, ncclSum, g->comm, st);
+        if (r != ncclSuccess) return fail(CT_ENCCL, "ncclReduceScatter: %s", nccl_err(r));
+        const size_t j0 = s->off0, j1 = std::min(s->N, s->off0 + s->S);
+        if (epi == EPI_INIT) {
+            if (j1 > j0) CT_CUDA(cudaMemcpyAsync(s->gs + j0, Gnew + j0, (j1 - j0) * 4, cudaMemcpyDeviceToDevice, st));
+            tmark_end(s, st, 4, t2);
+            return CT_OK;
+        }
+        ga.G_old = s->Gbuf[s->curG];
+        ga.G_new = Gnew;
+        gupd_slab_kernel<<<nblk(std::max(j1, j0 + 1) - j0), 256, 0, st>>>(ga, j0, j1, s->xi_ex);
+        CT_LAUNCHED(1);
+        r = g_nccl.AllReduce(s->xi_ex, s->xi_ex + 1, 1, ncclFloat64, ncclSum, g->comm, st);
+        if (r != ncclSuccess) return fail(CT_ENCCL, "ncclAllReduce(xi): %s", nccl_err(r));
+        xi_rule_kernel<<<1, 256, 0, st>>>(ga, s->xi_ex + 1);
+        CT_LAUNCHED(1);
+        tmark_end(s, st, 4, t2);
+        return CT_OK;
+    }
+    // multi-rank (FISTA inner solver): partial back-projection, NCCL sum, unfused epilogue
     int t1 = tmark(s, st);
     if (int e = launch_back<EPI_STORE>(g, v, s->sino, s->Gtmp, ga, st)) return e;
     tmark_end(s, st, 2, t1);
@@ -719,21 +808,33 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
     const ct_geom* g = s->g;
     const ct_oslalm_cfg& c = s->cfg;
     int M = c.M;
-    float* xa = x;
-    float* xb = s->xalt;
+    // slab path: iterate on the state's full-image buffers (all-gathered after each update)
+    float* xa = s->slab ? s->xp[0] : x;
+    float* xb = s->slab ? s->xp[1] : s->xalt;
+    if (s->slab) CT_CUDA(cudaMemcpyAsync(xa, x, s->N * 4, cudaMemcpyDeviceToDevice, st));
+    // rows this rank updates (all rows on one rank)
+    const int ry0 = s->slab ? s->iy0 : 0, ry1 = s->slab ? s->iy1 : g->d.ny;
+    const size_t rj0 = (size_t)ry0 * g->d.nx * nz_of(g), rj1 = (size_t)ry1 * g->d.nx * nz_of(g);
     float inv_d = (float)(1.0 / c.reg.delta);
     int kernels = 0;
     for (int j = 0; j < M; j++) {
         int t0 = tmark(s, st);
         if (c.inner == CT_INNER_SQS) {
-            if (c.reg.nbr == 8)
-                sqs_update_kernel<8><<<nblk(s->N), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
-                                                                  &s->sc->rho, (float)c.reg.beta, inv_d, s->N);
-            else
-                sqs_update3d_kernel<<<dim3((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (g->dg.ny + kK3Y - 1) / kK3Y), 256,
-                                      0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask, &s->sc->rho,
-                                               (float)c.reg.beta, inv_d);
-            CT_LAUNCHED(1);
+            if (ry1 > ry0) {
+                if (c.reg.nbr == 8)
+                    sqs_update_kernel<8><<<nblk(rj1 - rj0), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl,
+                                                                          d->mask, &s->sc->rho, (float)c.reg.beta, inv_d,
+                                                                          rj0, rj1);
+                else
+                    sqs_update3d_kernel<<<dim3((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (ry1 - ry0 + kK3Y - 1) / kK3Y),
+                                          256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
+                                                        &s->sc->rho, (float)c.reg.beta, inv_d, ry0, ry1);
+                CT_LAUNCHED(1);
+            }
+            if (s->slab) {   // every rank needs the full x+ for its next forward projection
+                ncclResult_t r = g_nccl.AllGather(xb + s->off0, xb, s->S, ncclFloat32, g->comm, st);
+                if (r != ncclSuccess) return fail(CT_ENCCL, "ncclAllGather: %s", nccl_err(r));
+            }
         } else {
             // n warm-started FISTA iterations: v_0 = x_0 = x_k (= xa), result in xb
             double t = 1.0;
@@ -770,6 +871,7 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
     if (xa != x) {
         CT_CUDA(cudaMemcpyAsync(x, xa, s->N * 4, cudaMemcpyDeviceToDevice, st));
     }
+    if (s->slab) kernels += M;   // xi_rule per step
     if (nk) *nk = kernels;
     return CT_OK;
 }
@@ -811,6 +913,8 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
             if (ge.exec) { cudaGraphExecDestroy(ge.exec); ge.exec = nullptr; }
     }
     if (int e = check_data(g, d, x)) return e;
+    if (g->nranks != s->P || g->rank != s->prank || (g->comm != nullptr) != s->has_comm)
+        return fail(CT_ESTATE, "communicator changed after state creation (create the state after ct_comm_init)");
     DeviceGuard guard(g->d.device);
     cudaStream_t st = (cudaStream_t)stream;
     if (int e = ensure_initialised(s, d, x, st)) return e;

@@ -130,63 +130,9 @@ __device__ __forceinline__ void column_footprint(const DevGeom& g, float4 vw, fl
 // columns are computed group-parallel (one column per thread) into a shared
 // table; then, for each column, thread r computes the column's axial sum
 //   A(r) = sum_iz x[iz] l_theta(iz) F_t(iz, r)      (z-fastest layout: coalesced)
-// and adds lphi F_s(c) A(r) to its register accumulators of the tile's channels.
-// The column's channel offset is warp-uniform, so a jump table selects a fully
-// static (register-indexed) 8-channel update: no atomics, no shared-memory RMW.
-template <int TC>
-__device__ __forceinline__ void tile_add(float (&acc)[TC], int o, const float (&w)[kMaxFoot], float A) {
-    static_assert(TC <= 32, "offset table covers TC <= 32");
-#define CT_ADD(O)                                                                   \
-    case O:                                                                         \
-        _Pragma("unroll") for (int j = 0; j < kMaxFoot; j++) {                     \
-            if ((O) + j >= 0 && (O) + j < TC) acc[((O) + j >= 0 && (O) + j < TC) ? (O) + j : 0] += w[j] * A; \
-        }                                                                           \
-        break;
-    switch (o) {
-        CT_ADD(-7)
-        CT_ADD(-6)
-        CT_ADD(-5)
-        CT_ADD(-4)
-        CT_ADD(-3)
-        CT_ADD(-2)
-        CT_ADD(-1)
-        CT_ADD(0)
-        CT_ADD(1)
-        CT_ADD(2)
-        CT_ADD(3)
-        CT_ADD(4)
-        CT_ADD(5)
-        CT_ADD(6)
-        CT_ADD(7)
-        CT_ADD(8)
-        CT_ADD(9)
-        CT_ADD(10)
-        CT_ADD(11)
-        CT_ADD(12)
-        CT_ADD(13)
-        CT_ADD(14)
-        CT_ADD(15)
-        CT_ADD(16)
-        CT_ADD(17)
-        CT_ADD(18)
-        CT_ADD(19)
-        CT_ADD(20)
-        CT_ADD(21)
-        CT_ADD(22)
-        CT_ADD(23)
-        CT_ADD(24)
-        CT_ADD(25)
-        CT_ADD(26)
-        CT_ADD(27)
-        CT_ADD(28)
-        CT_ADD(29)
-        CT_ADD(30)
-        CT_ADD(31)
-        default: break;
-    }
-#undef CT_ADD
-}
-
+// and adds lphi F_s(c) A(r) to its own row of the group's shared accumulator
+// [channel][row] (thread r is the only writer of row r: no atomics, fixed order).
+// Lines are trimmed to the columns that hold a nonzero voxel (fwd3d_extent_kernel).
 // Axial sum of one column for detector row r (forward projector):
 //   A(r) = sum_iz x[iz] l_theta(iz) F_t(iz, r),  F_t = overlap / kz.
 // Table fields (set in the footprint phase): ax.qf = lower edge of row 0's extent
@@ -226,14 +172,21 @@ __device__ __forceinline__ float fwd_axial_any(const Foot& f, const float* __res
     return A;
 }
 
+// Accumulator channels of a tile: a column overlapping the tile starts at most
+// kMaxFoot - 1 channels left of it and spans at most kMaxFoot channels.
+template <int TC>
+__host__ __device__ constexpr int fwd3d_tcp() { return TC + 2 * kMaxFoot - 2; }
+
 template <int TC, int NTP, int NTHR, bool RESID>
-__global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
-                                                        float* __restrict__ out, const float* __restrict__ yobs,
-                                                        const float* __restrict__ wts, float scale) {
+__global__ void __launch_bounds__(NTHR) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
+                                                     float* __restrict__ out, const float* __restrict__ yobs,
+                                                     const float* __restrict__ wts, float scale,
+                                                     const int2* __restrict__ ext) {
     constexpr int G = NTHR / NTP;
+    constexpr int TCP = fwd3d_tcp<TC>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float (*P)[TC][NTP + 1] = reinterpret_cast<float (*)[TC][NTP + 1]>(smem_raw);
-    Foot* table = reinterpret_cast<Foot*>(smem_raw + sizeof(float) * G * TC * (NTP + 1));
+    float* Pacc = reinterpret_cast<float*>(smem_raw);                                    // [G][TCP][NTP]
+    Foot* table = reinterpret_cast<Foot*>(smem_raw + sizeof(float) * G * TCP * NTP);     // [G][NTP]
     const int c0 = blockIdx.x * TC;
     const int k = blockIdx.y;
     const int v = first + k * stride;
@@ -242,22 +195,28 @@ __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, in
     const int gi = threadIdx.x / NTP, r = threadIdx.x % NTP;
     const bool row_ok = r < g.nt;
     Foot* tab = table + gi * NTP;
-    float acc[TC];
+    // thread r owns row r of its group's accumulator (stride NTP: distinct banks, no sharing)
+    float* Pg = Pacc + gi * TCP * NTP + r;
 #pragma unroll
-    for (int c = 0; c < TC; c++) acc[c] = 0.0f;
-    Wedge w = make_wedge(g, sb, cb, c0, TC);
+    for (int c = 0; c < TCP; c++) Pg[c * NTP] = 0.0f;
+    const Wedge w = make_wedge(g, sb, cb, c0, TC);
     const int nz = g.nz;
     for (int L = gi; L < w.nlines; L += G) {
         int lo, hi;
         wedge_line(g, w, L, lo, hi);
+        if (ext) {   // columns of this line that hold a nonzero voxel (fwd3d_extent_kernel)
+            const int2 e = __ldg(&ext[w.rows ? L : g.ny + L]);
+            lo = max(lo, e.x);
+            hi = min(hi, e.y);
+        }
         if (lo > hi) continue;
         const int n_in = hi - lo + 1;
         for (int cb0 = 0; cb0 < n_in; cb0 += NTP) {
             // group-parallel footprints of up to NTP columns of this line
-            int q = cb0 + r;
+            const int q = cb0 + r;
             if (q < n_in) {
-                int u = lo + q;
-                int ix = w.rows ? u : L, iy = w.rows ? L : u;
+                const int u = lo + q;
+                const int ix = w.rows ? u : L, iy = w.rows ? L : u;
                 Foot f;
                 column_footprint(g, vw, g.x0 + ix * g.dx, g.y0 + iy * g.dy, f);
                 if (!(f.n > 0 && f.cA + f.n > c0 && f.cA < c0 + TC)) f.n = 0;   // misses the tile
@@ -284,26 +243,39 @@ __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, in
                         A1 = fwd_axial_any(f1, x, r, nz, g.rbase);
                     }
                 }
-                if (f0.n > 0) tile_add<TC>(acc, f0.cA - c0, f0.w, A0);
-                if (f1.n > 0) tile_add<TC>(acc, f1.cA - c0, f1.w, A1);
+                // lphi F_s(c) A(r) into channels cA..cA+n-1 (warp-uniform n: no divergence)
+                if (f0.n > 0) {
+                    float* p = Pg + (f0.cA - c0 + kMaxFoot - 1) * NTP;
+#pragma unroll
+                    for (int jj = 0; jj < kMaxFoot; jj++) {
+                        if (jj >= f0.n) break;
+                        p[jj * NTP] = fmaf(f0.w[jj], A0, p[jj * NTP]);
+                    }
+                }
+                if (f1.n > 0) {
+                    float* p = Pg + (f1.cA - c0 + kMaxFoot - 1) * NTP;
+#pragma unroll
+                    for (int jj = 0; jj < kMaxFoot; jj++) {
+                        if (jj >= f1.n) break;
+                        p[jj * NTP] = fmaf(f1.w[jj], A1, p[jj * NTP]);
+                    }
+                }
             }
             asm volatile("bar.sync %0, %1;" ::"r"(gi + 1), "r"(NTP) : "memory");
         }
     }
-#pragma unroll
-    for (int c = 0; c < TC; c++) P[gi][c][r] = acc[c];
     __syncthreads();
     // fixed-order sum over groups; thread (c, r) pairs cover the tile, r fastest
     for (int idx = threadIdx.x; idx < TC * NTP; idx += NTHR) {
-        int c = idx / NTP, rr = idx % NTP;
+        const int c = idx / NTP, rr = idx % NTP;
         if (rr >= g.nt || c0 + c >= g.ns) continue;
         float s = 0.0f;
 #pragma unroll
-        for (int q = 0; q < G; q++) s += P[q][c][rr];
-        size_t oi = ((size_t)k * g.ns + c0 + c) * g.nt + rr;
+        for (int q = 0; q < G; q++) s += Pacc[(q * TCP + c + kMaxFoot - 1) * NTP + rr];
+        const size_t oi = ((size_t)k * g.ns + c0 + c) * g.nt + rr;
         if (RESID) {
-            size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
-            float yo = yobs ? __ldg(&yobs[gidx]) : 0.0f;
+            const size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
+            const float yo = yobs ? __ldg(&yobs[gidx]) : 0.0f;
             out[oi] = scale * __ldg(&wts[gidx]) * (s - yo);
         } else {
             out[oi] = s;
@@ -313,7 +285,30 @@ __global__ void __launch_bounds__(NTHR, 3) fwd3d_kernel(DevGeom g, int first, in
 
 template <int TC, int NTP, int NTHR>
 constexpr size_t fwd3d_smem() {
-    return sizeof(float) * (NTHR / NTP) * TC * (NTP + 1) + sizeof(Foot) * NTHR;
+    return sizeof(float) * (NTHR / NTP) * fwd3d_tcp<TC>() * NTP + sizeof(Foot) * NTHR;
+}
+
+// Per image line, the range of columns holding a nonzero voxel (forward-projection
+// trimming): ext[iy] = [min ix, max ix] over row iy, ext[ny + ix] = [min iy, max iy].
+// Integer atomics: order-independent.  Warp = one column (lanes walk z, coalesced).
+__global__ void fwd3d_extent_init(int2* ext, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) ext[i] = make_int2(0x7fffffff, -1);
+}
+
+__global__ void __launch_bounds__(256) fwd3d_extent_kernel(DevGeom g, const float* __restrict__ x, int2* ext) {
+    const int col = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (col >= g.nx * g.ny) return;
+    bool any = false;
+    const float* xc = x + (size_t)col * g.nz;
+    for (int iz = lane; iz < g.nz; iz += 32) any |= __ldg(&xc[iz]) != 0.0f;
+    if (__any_sync(0xffffffffu, any) && lane == 0) {
+        const int ix = col % g.nx, iy = col / g.nx;
+        atomicMin(&ext[iy].x, ix);
+        atomicMax(&ext[iy].y, ix);
+        atomicMin(&ext[g.ny + ix].x, iy);
+        atomicMax(&ext[g.ny + ix].y, iy);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -746,8 +741,9 @@ __global__ void __launch_bounds__(256) sqs_update_kernel(DevGeom g, const float*
                                                         const float* __restrict__ G, const float* __restrict__ gs,
                                                         const float* __restrict__ dl, const uint8_t* __restrict__ m,
                                                         const double* __restrict__ rho_p, float beta, float inv_delta,
-                                                        size_t N) {
-    size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                                        size_t j0, size_t N) {
+    // updates voxels [j0, N) (multi-rank: this rank's slab of rows; x is the full image)
+    size_t j = j0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= N) return;
     if (!m[j]) {
         xn[j] = 0.0f;
@@ -777,10 +773,12 @@ constexpr int kK3Y = 8;
 __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
                                                           const float* __restrict__ G, const float* __restrict__ gs,
                                                           const float* __restrict__ dl, const uint8_t* __restrict__ m,
-                                                          const double* __restrict__ rho_p, float beta, float inv_delta) {
+                                                          const double* __restrict__ rho_p, float beta, float inv_delta,
+                                                          int iy_begin, int iy_end) {
+    // updates rows [iy_begin, iy_end) (multi-rank: this rank's slab; x is the full image)
     __shared__ float Pl[3][10][34];
     const int tz = threadIdx.x & 31, tx = threadIdx.x >> 5;
-    const int ix0 = blockIdx.x * 8, z0 = blockIdx.y * 32, iy0 = blockIdx.z * kK3Y;
+    const int ix0 = blockIdx.x * 8, z0 = blockIdx.y * 32, iy0 = iy_begin + blockIdx.z * kK3Y;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
     const float rho = (float)*rho_p;
     auto load_plane = [&](int slot, int iy) {
@@ -802,7 +800,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
     constexpr float r2 = 0.70710678118654752f, r3 = 0.57735026918962576f;
     for (int t = 0; t < kK3Y; t++) {
         const int iy = iy0 + t;
-        if (iy >= ny) break;
+        if (iy >= iy_end) break;
         load_plane((t + 2) % 3, iy + 1);
         __syncthreads();
         if (inb) {
@@ -926,6 +924,40 @@ __global__ void __launch_bounds__(256) gupd_kernel(const float* __restrict__ Gp,
     }
     block_sum_store<256>(xi, &ga.xi_part[blockIdx.x]);
     xi_arrive<256>(ga, gridDim.x);
+}
+
+// Multi-rank slab path: G+ (already reduce-scattered into G_new[j0, j1)) -> g-update and
+// this rank's xi; the last block stores the rank's fixed-order xi sum in *xi_out (the
+// ranks' sums are then all-reduced and xi_rule_kernel applies K4 on every rank).
+__global__ void __launch_bounds__(256) gupd_slab_kernel(GupdArgs ga, size_t j0, size_t j1, double* xi_out) {
+    const size_t j = j0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double xi = 0.0;
+    if (j < j1) {
+        const float rho = (float)*ga.rho;
+        const float P = ga.G_new[j], G = ga.G_old[j], gg = ga.gs[j];
+        ga.gs[j] = (rho * P + gg) / (1.0f + rho);
+        if (ga.mask[j]) xi = (double)(gg - P) * (double)(P - G);
+    }
+    block_sum_store<256>(xi, &ga.xi_part[blockIdx.x]);
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&ga.sc->arrive, 1u);
+        last = (prev == gridDim.x - 1u);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double sum = 0.0;
+        for (unsigned b = 0; b < gridDim.x; b++) sum += __ldcg(&ga.xi_part[b]);
+        *xi_out = sum;
+        ga.sc->arrive = 0;
+    }
+}
+
+// K4 on the all-reduced xi (one block)
+__global__ void __launch_bounds__(256) xi_rule_kernel(GupdArgs ga, const double* xi_glob) {
+    xi_finalize_block<256>(xi_glob, 1, ga);
 }
 
 // ---------------------------------------------------------------------------

@@ -4,6 +4,9 @@
   PAPER.md P:541-559 (eqs. max_M_axial, max_M_helical; s_axial ~ 40, s_helical ~ 24).
 * ``rank_view_block`` — the multi-GPU partition of one subset's views:
   rank p of P owns a contiguous block of the subset's n_m views.
+* ``rank_slab`` — the multi-GPU partition of the image for the SQS update: rank p owns a
+  contiguous block of image rows (iy); buffers are padded to P equal slabs (mirror of
+  ``slab_geometry`` in ct_abi.cu).
 """
 from __future__ import annotations
 
@@ -30,3 +33,9 @@ def rank_view_block(count: int, rank: int, nranks: int) -> tuple[int, int]:
     base, extra = divmod(count, nranks)
     k0 = rank * base + min(rank, extra)
     return k0, base + (1 if rank < extra else 0)
+
+
+def rank_slab(ny: int, rank: int, nranks: int) -> tuple[int, int, int]:
+    """Rows [iy0, iy1) of the image owned by `rank`, and the padded rows per slab R (P*R >= ny)."""
+    R = (ny + nranks - 1) // nranks
+    return min(ny, rank * R), min(ny, (rank + 1) * R), R

@@ -47,6 +47,86 @@ def _worker(rank, ws, port, out):
     dist.destroy_process_group()
 
 
+def _slab_worker(rank, ws, port, out):
+    """One OS-LALM inner step with the slab decomposition of the SQS update (ct_abi.cu
+    subset_gradient / enqueue_iteration, slab path): partial back-projections summed and
+    scattered by rows, slab g-update and xi partial, xi summed, slab update from the full
+    x, rows gathered.  Compared with the same step computed whole on one process."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import oracle as O
+    from paper_1402_4381_b200 import host
+    from tests import geomutil as GU
+    g = GU.small_geoms()["fan_c2"]
+    M, m, beta, delta, rho = 3, 1, 2.0 ** 10, 2e-4, 0.4
+    first, stride, count = host.subset_views(g["na"], M, m)
+    rng = np.random.default_rng(1)
+    shape = O.img_shape(g)
+    x = rng.random(shape) * 0.02
+    r = rng.standard_normal(O.sino_shape(g, count))
+    G, gs, dl = rng.standard_normal(shape), rng.standard_normal(shape), rng.random(shape) + 0.5
+    mask = np.ones(shape, np.uint8)
+
+    def step(rows):
+        """(x+ on rows, g+ on rows, xi over rows) given full x and the summed G+."""
+        gr, cu = O.reg_grad(g, beta, delta, 8, mask, x)
+        s_dir = rho * G + (1 - rho) * gs
+        xn = np.maximum(0.0, x - (s_dir + gr) / (rho * dl + cu))
+        return xn[..., rows, :], Gp
+
+    k0, n = host.rank_view_block(count, rank, ws)
+    part = O.back(g, r[k0:k0 + n], first + k0 * stride, stride, n)
+    t = torch.from_numpy(part.copy())
+    dist.all_reduce(t)                      # reduce-scatter = all-reduce + own rows
+    iy0, iy1, R = host.rank_slab(shape[-2], rank, ws)
+    Gp = t.numpy()
+    rows = slice(iy0, iy1)
+    xi_part = float(((gs - Gp) * (Gp - G))[..., rows, :].sum())
+    xi = torch.tensor([xi_part], dtype=torch.float64)
+    dist.all_reduce(xi)
+    xrows, _ = step(rows)
+    pad = np.zeros(shape[:-2] + (R, shape[-1]))
+    pad[..., :iy1 - iy0, :] = xrows
+    bufs = [torch.zeros_like(torch.from_numpy(pad)) for _ in range(ws)]
+    dist.all_gather(bufs, torch.from_numpy(pad))
+    xg = np.concatenate([b.numpy() for b in bufs], axis=-2)[..., :shape[-2], :]
+    if rank == 0:
+        Gf = O.back(g, r, first, stride, count)
+        xi_f = float(((gs - Gf) * (Gf - G)).sum())
+        gr, cu = O.reg_grad(g, beta, delta, 8, mask, x)
+        xf = np.maximum(0.0, x - (rho * G + (1 - rho) * gs + gr) / (rho * dl + cu))
+        out.put((float(np.abs(xg - xf).max()), abs(xi.item() - xi_f) / abs(xi_f)))
+    dist.destroy_process_group()
+
+
+def test_slab_partition_covers_rows():
+    from paper_1402_4381_b200 import host
+    for ny in (1, 20, 64, 512, 513):
+        for ws in (1, 2, 3, 8):
+            slabs = [host.rank_slab(ny, r, ws) for r in range(ws)]
+            assert slabs[0][0] == 0 and slabs[-1][1] == ny
+            for (a0, a1, R), (b0, b1, _) in zip(slabs, slabs[1:]):
+                assert a1 == b0 and a1 - a0 <= R
+            assert ws * slabs[0][2] >= ny
+
+
+def test_gloo_two_rank_slab_update():
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] <= 1e-12 and res[1] <= 1e-10
+
+
 def test_view_block_partition_covers_subset():
     from paper_1402_4381_b200 import host
     for count in (1, 7, 41, 287):
