@@ -324,10 +324,13 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
     return CT_OK;
 }
 
+#ifndef CT_BACK3D_CHUNKS
+#define CT_BACK3D_CHUNKS 0   // 1: axial scans use the 64-slice register-chunk kernel (tuning A/B)
+#endif
 // 3D back-projection variant: axial scans use 64-slice register chunks (every view's
 // cone covers a chunk); helical scans use whole-column shared-memory accumulators so
 // the work follows each view's active slices.
-static bool back3d_use_chunks(const ct_geom* g) { return g->d.kind == CT_CONE_AXIAL; }
+static bool back3d_use_chunks(const ct_geom* g) { return CT_BACK3D_CHUNKS && g->d.kind == CT_CONE_AXIAL; }
 
 static void back_grid(const ct_geom* g, dim3& grid) {
     const DevGeom& dg = g->dg;

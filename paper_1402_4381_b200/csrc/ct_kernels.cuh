@@ -592,9 +592,32 @@ __host__ __device__ constexpr size_t back3d_smem_fixed() {
     return sizeof(Foot) * 8 * 32 + sizeof(float) * 8 * kBackRows + sizeof(float) * 8 * (kBackRows + 4);
 }
 
+// Two filtered detector rows (float2) of one view: q = sum_{c < n} w[c] y[c][r..r+1].
+template <int NC>
+__device__ __forceinline__ void filt_rows2(const float2* __restrict__ yr, int pitch2, bool inr, const Foot& f, float& q0,
+                                           float& q1) {
+    float2 vv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) vv[c] = (inr && c < f.n) ? __ldg(yr + c * pitch2) : make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        q0 = fmaf(f.w[c], vv[c].x, q0);
+        q1 = fmaf(f.w[c], vv[c].y, q1);
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ void filt_rows1(const float* __restrict__ yr, int pitch, bool inr, const Foot& f, float& q0) {
+    float vv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) vv[c] = (inr && c < f.n) ? __ldg(yr + c * pitch) : 0.0f;
+#pragma unroll
+    for (int c = 0; c < NC; c++) q0 = fmaf(f.w[c], vv[c], q0);
+}
+
 template <int EPI>
-__global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, int stride, int count,
-                                                       const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
+__global__ void __launch_bounds__(256) back3d_kernel(DevGeom g, int first, int stride, int count,
+                                                    const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     Foot* table = reinterpret_cast<Foot*>(sm_raw);
     float* Qs = reinterpret_cast<float*>(sm_raw + sizeof(Foot) * 8 * 32);
@@ -619,6 +642,7 @@ __global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, in
     any = __any_sync(0xffffffffu, any);
     if (any) {
         const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
+        const float ub = g.rbase + 0.5f;   // row-edge coordinate: detector row r covers u in [r, r + 1)
         for (int vb = 0; vb < count; vb += 32) {
             const int kk = vb + lane;
             if (kk < count) {
@@ -640,56 +664,69 @@ __global__ void __launch_bounds__(256, 3) back3d_kernel(DevGeom g, int first, in
                 load_foot(&tab[j], f);
                 if (f.n <= 0) continue;
                 const int za = f.rows & 0xffff, nzs = f.rows >> 16;
-                const float* yv = y + (size_t)(vb + j) * ns * nt;     // this view's sinogram
-                const int off0 = f.cA * nt;
-                // (1) filtered rows and their prefix sums (lanes = rows)
+                // rows met by the active slices, from an even row (float2 loads)
+                const float zq = (float)(za - f.ax.qi) - f.ax.qf;
+                // two rows per lane (float2) for tall detectors; float2 rows need an even row pitch
+                const bool even = (nt & 1) == 0 && nt > 32;
+                const int r_lo = min(max(__float2int_rd(fmaf(zq, f.ax.inv_kz, ub)), 0), nt - 1) & (even ? ~1 : ~0);
+                const int r_hi = min(max(__float2int_rd(fmaf(zq + (float)nzs, f.ax.inv_kz, ub)), 0), nt - 1);
+                const int nr = r_hi - r_lo + 1;
+                const float* yv = y + ((size_t)(vb + j) * ns + f.cA) * nt + r_lo;
+                // (1) filtered rows Q(r) = sum_c lphi F_s(c) y[c][r] and prefix sums
+                //     PF[k] = sum_{r < r_lo + k} Q(r): lane = two rows (float2), pair sum + warp scan
                 float carry = 0.0f;
-                for (int p0 = 0; p0 < nt; p0 += 32) {
-                    const int p = p0 + lane;
-                    const bool inr = p < nt;
-                    const float* yr = yv + (off0 + (inr ? p : 0));
-                    float q;
-                    if (f.n <= 4) {   // warp-uniform: issue all loads first, then the FMAs
-                        float v[4];
-#pragma unroll
-                        for (int c = 0; c < 4; c++) v[c] = (inr && c < f.n) ? __ldg(yr + c * nt) : 0.0f;
-                        q = f.w[0] * v[0] + f.w[1] * v[1] + f.w[2] * v[2] + f.w[3] * v[3];
+                const int RPL = even ? 2 : 1;
+                for (int p0 = 0; p0 < nr; p0 += 32 * RPL) {
+                    const int p = p0 + RPL * lane;
+                    const bool inr = p < nr;
+                    float q0 = 0.0f, q1 = 0.0f;
+                    if (even) {
+                        const float2* yr = reinterpret_cast<const float2*>(yv + (inr ? p : 0));
+                        // warp-uniform channel count: issue all loads, then the FMAs
+                        if (f.n <= 3) filt_rows2<3>(yr, nt >> 1, inr, f, q0, q1);
+                        else if (f.n <= 4) filt_rows2<4>(yr, nt >> 1, inr, f, q0, q1);
+                        else filt_rows2<kMaxFoot>(yr, nt >> 1, inr, f, q0, q1);
+                        if (p + 1 >= nr) q1 = 0.0f;   // row past r_hi (odd count)
                     } else {
-                        float v[kMaxFoot];
-#pragma unroll
-                        for (int c = 0; c < kMaxFoot; c++) v[c] = (inr && c < f.n) ? __ldg(yr + c * nt) : 0.0f;
-                        q = 0.0f;
-#pragma unroll
-                        for (int c = 0; c < kMaxFoot; c++) q += f.w[c] * v[c];
+                        const float* yr = yv + (inr ? p : 0);
+                        if (f.n <= 3) filt_rows1<3>(yr, nt, inr, f, q0);
+                        else if (f.n <= 4) filt_rows1<4>(yr, nt, inr, f, q0);
+                        else filt_rows1<kMaxFoot>(yr, nt, inr, f, q0);
                     }
-                    if (inr) Q[p] = q;
-                    float inc = q;
+                    const float s2 = q0 + q1;
+                    float inc = s2;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
-                        float t = __shfl_up_sync(0xffffffffu, inc, o);
+                        const float t = __shfl_up_sync(0xffffffffu, inc, o);
                         if (lane >= o) inc += t;
                     }
-                    if (inr) PF[p + 1] = carry + inc;
+                    const float ex = carry + inc - s2;
+                    if (inr) {
+                        Q[p] = q0;
+                        PF[p] = ex;
+                        if (even) {
+                            Q[p + 1] = q1;
+                            PF[p + 1] = ex + q0;
+                        }
+                        if (p + RPL >= nr) PF[p + RPL] = ex + s2;   // upper edge of the last row
+                    }
                     carry += __shfl_sync(0xffffffffu, inc, 31);
                 }
-                if (lane == 0) PF[0] = 0.0f;
                 __syncwarp();
-                // (2) the active slices (lanes = slices)
-                const float fnr = (float)nt;
-                const float ubase = g.rbase + 0.5f;
+                // (2) active slices (lanes = slices): integral of the row-wise constant Q over
+                //     the slice's extent on the detector, PF(u(iz + 1)) - PF(u(iz))
+                const float fnr = (float)nr, ubl = ub - (float)r_lo;
                 for (int s0 = 0; s0 < nzs; s0 += 32) {
-                    const int iz = za + s0 + lane;
-                    const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
-                    const float u0 = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubase), 0.0f), fnr);
-                    const int p0 = min(__float2int_rd(u0), nt - 1);
-                    const float pf = PF[p0] + (u0 - (float)p0) * Q[p0];
-                    float up = __shfl_down_sync(0xffffffffu, pf, 1);
-                    if (lane == 31) {   // upper edge of this pass's last slice
-                        const float u1 = fminf(fmaxf(fmaf(zi + 1.0f, f.ax.inv_kz, ubase), 0.0f), fnr);
-                        const int p1 = min(__float2int_rd(u1), nt - 1);
-                        up = PF[p1] + (u1 - (float)p1) * Q[p1];
+                    if (s0 + lane < nzs) {
+                        const int iz = za + s0 + lane;
+                        const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
+                        const float u0 = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubl), 0.0f), fnr);
+                        const float u1 = fminf(fmaxf(fmaf(zi + 1.0f, f.ax.inv_kz, ubl), 0.0f), fnr);
+                        const int k0 = min(__float2int_rd(u0), nr - 1), k1 = min(__float2int_rd(u1), nr - 1);
+                        const float lo = fmaf(u0 - (float)k0, Q[k0], PF[k0]);
+                        const float hi = fmaf(u1 - (float)k1, Q[k1], PF[k1]);
+                        acc[iz] = fmaf(ltheta(f.ax, iz), hi - lo, acc[iz]);
                     }
-                    if (s0 + lane < nzs) acc[iz] += ltheta(f.ax, iz) * (up - pf);
                 }
                 __syncwarp();
             }
