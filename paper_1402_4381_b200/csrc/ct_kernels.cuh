@@ -177,8 +177,15 @@ __device__ __forceinline__ float fwd_axial_any(const Foot& f, const float* __res
 template <int TC>
 __host__ __device__ constexpr int fwd3d_tcp() { return TC + 2 * kMaxFoot - 2; }
 
+#ifndef CT_FWD3D_MINB
+#define CT_FWD3D_MINB 4   // min resident CTAs per SM for the register budget (A/B: 4 beats 1 by 1.3-1.5x)
+#endif
+#ifndef CT_BACK3D_MINB
+#define CT_BACK3D_MINB 4
+#endif
+
 template <int TC, int NTP, int NTHR, bool RESID>
-__global__ void __launch_bounds__(NTHR) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
+__global__ void __launch_bounds__(NTHR, CT_FWD3D_MINB) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
                                                      float* __restrict__ out, const float* __restrict__ yobs,
                                                      const float* __restrict__ wts, float scale,
                                                      const int2* __restrict__ ext) {
@@ -616,7 +623,7 @@ __device__ __forceinline__ void filt_rows1(const float* __restrict__ yr, int pit
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(256) back3d_kernel(DevGeom g, int first, int stride, int count,
+__global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, int first, int stride, int count,
                                                     const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     Foot* table = reinterpret_cast<Foot*>(sm_raw);
