@@ -83,7 +83,7 @@ def lib():
         L.or_bit_reversal.argtypes = [i, ip]; L.or_bit_reversal.restype = None
         L.or_rho_l.argtypes = [ctypes.c_long, d]; L.or_rho_l.restype = d
         L.or_subset_grad.argtypes = [G, i, i, dp, dp, dp, dp]; L.or_subset_grad.restype = None
-        L.or_oslalm_run.argtypes = [G, dp, dp, dp, u8, i, i, d, d, d, d, i, i, i, dp, dp, dp, dp, i, i]
+        L.or_oslalm_run.argtypes = [G, dp, dp, dp, u8, i, i, d, d, d, d, i, i, i, dp, dp, dp, dp, i, i, i, d, dp]
         L.or_inner_fista.argtypes = [G, d, d, i, u8, dp, d, dp, dp, i, dp]
         L.or_inner_fista.restype = None
         L.or_oslalm_run.restype = None
@@ -105,6 +105,13 @@ def geom(g: dict) -> _Geom:
               "dso", "dsd", "orbit_deg", "orbit_start_deg", "pitch"):
         setattr(s, k, float(g.get(k, 0.0)))
     return s
+
+
+def _alpha_ptr(a, n):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous and a.size >= n, "alpha_out: float64[n_iter]"
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
 def _d(a):
@@ -240,9 +247,12 @@ def inner_fista(g, beta, delta, nbr, mask, dl, rho, xk, s, n):
 
 
 def oslalm_run(g, y, w, dl, mask, x0, *, M, mode="continuation", rho_fixed=1.0, rho_min=1e-3,
-               beta, delta, nbr, n_iter, trailing=False, inner="sqs", n_inner=1):
+               beta, delta, nbr, n_iter, trailing=False, inner="sqs", n_inner=1, bb=False, alpha_min=1e-6,
+               alpha_out=None):
     """Run O7; returns (x, log[n_steps,3] = (rho, xi, restart), g, G).
-    inner = "sqs" (one Huber-curvature SQS step, G14) or "fista" (n_inner FISTA iterations, NEXT-1)."""
+    inner = "sqs" (one Huber-curvature SQS step, G14) or "fista" (n_inner FISTA iterations, NEXT-1).
+    bb = True: Barzilai-Borwein scaling H_k = alpha_k D_L (NEXT-2); alpha_out (float64 array of
+    n_iter, optional) receives the alpha used in each outer iteration."""
     y, yp = _d(np.reshape(y, sino_shape(g, g["na"])))
     w, wp = _d(np.reshape(w, sino_shape(g, g["na"])))
     dl, dp = _d(np.reshape(dl, img_shape(g)))
@@ -255,5 +265,6 @@ def oslalm_run(g, y, w, dl, mask, x0, *, M, mode="continuation", rho_fixed=1.0, 
     _, gp = _d(gs); _, Gp = _d(Gs)
     lib().or_oslalm_run(geom(g), yp, wp, dp, mp, M, 0 if mode == "fixed" else 1, rho_fixed, rho_min,
                         beta, delta, nbr, n_iter, 1 if trailing else 0, xp, lp, gp, Gp,
-                        0 if inner == "sqs" else 1, int(n_inner))
+                        0 if inner == "sqs" else 1, int(n_inner), 1 if bb else 0, float(alpha_min),
+                        _alpha_ptr(alpha_out, n_iter))
     return x, log, gs, Gs

@@ -511,11 +511,23 @@ void or_inner_fista(const or_geom* g, double beta, double delta, int nbr, const 
  * projection pair (so the state is ready for another iteration; x unchanged).
  * log (nullable) receives per inner step: rho, xi, restart flag (3 doubles).
  * g_out, G_out (nullable) receive the final split gradient and subset gradient.
+ *
+ * bb = 1: Barzilai-Borwein scaling (NEXT-2, supplement P:1472-1492).  The SQS
+ * Hessian L_diag = D_L is replaced by H_k = alpha_k D_L, with alpha_k fitting the secant
+ * equation y_k ~ H_k s_k in the L_diag^{-1}-weighted least-squares sense subject to
+ * alpha <= 1 (eq. scale_factor_alpha_k):
+ *     alpha_k = min(1, max(alpha_min, (y_k' s_k) / (s_k' D_L s_k)))   (sums over S),
+ *     s_k = x^k - x^{k-1},  y_k = grad l(x^k) - grad l(x^{k-1}).
+ * OS reading (DESIGN.md B-BB): k counts outer iterations; x^k is the image after outer
+ * iteration k and grad l(x^k) is approximated by the mean of the M subset gradients
+ * M grad l_m computed during iteration k.  alpha = 1 for iterations 1 and 2 (no secant
+ * pair yet); alpha_k (from iterations k-1, k) is used in iteration k + 1.  alpha_log
+ * (nullable) receives the alpha used in each outer iteration.
  */
 void or_oslalm_run(const or_geom* g, const double* y, const double* w, const double* dl, const uint8_t* mask,
                    int M, int mode, double rho_fixed, double rho_min, double beta, double delta, int nbr,
                    int n_iter, int trailing, double* x, double* log, double* g_out, double* G_out, int inner,
-                   int n_inner) {
+                   int n_inner, int bb, double alpha_min, double* alpha_log) {
     size_t N = (size_t)nzv(g) * g->ny * g->nx;
     size_t cells = (size_t)ntv(g) * g->ns;
     int maxcount = (g->na + M - 1) / M;
@@ -533,7 +545,15 @@ void or_oslalm_run(const or_geom* g, const double* y, const double* w, const dou
     memcpy(sg, G, N * sizeof(double));
     long l = 0;
     int step = 0;
-    for (int k = 1; k <= n_iter; k++)
+    /* Barzilai-Borwein state: H = alpha D_L (alpha = 1: the plain SQS Hessian) */
+    double alpha = 1.0;
+    double* hd = (double*)malloc(N * sizeof(double));        /* alpha D_L */
+    double* xprev = bb ? (double*)malloc(N * sizeof(double)) : NULL;
+    double* gbar = bb ? (double*)calloc(N, sizeof(double)) : NULL;
+    double* gprev = bb ? (double*)malloc(N * sizeof(double)) : NULL;
+    for (int k = 1; k <= n_iter; k++) {
+        for (size_t q = 0; q < N; q++) hd[q] = alpha * dl[q];
+        if (alpha_log) alpha_log[k - 1] = alpha;
         for (int j = 0; j < M; j++, step++) {
             double rho = mode == 0 ? rho_fixed : or_rho_l(l, rho_min);
             if (inner == 0) {
@@ -542,14 +562,14 @@ void or_oslalm_run(const or_geom* g, const double* y, const double* w, const dou
                 for (size_t q = 0; q < N; q++) {
                     if (!mask[q]) { x[q] = 0.0; continue; }
                     double s = rho * G[q] + (1.0 - rho) * sg[q];
-                    double xn = x[q] - (s + gr[q]) / (rho * dl[q] + cu[q]);
+                    double xn = x[q] - (s + gr[q]) / (rho * hd[q] + cu[q]);
                     x[q] = xn > 0.0 ? xn : 0.0;
                 }
             } else {
                 /* n warm-started FISTA iterations on the inner problem (NEXT-1) */
                 for (size_t q = 0; q < N; q++) cu[q] = rho * G[q] + (1.0 - rho) * sg[q];   /* s */
                 memcpy(gr, x, N * sizeof(double));                                         /* x_k */
-                or_inner_fista(g, beta, delta, nbr, mask, dl, rho, gr, cu, n_inner, x);
+                or_inner_fista(g, beta, delta, nbr, mask, hd, rho, gr, cu, n_inner, x);
             }
             if (log) { log[3 * step] = rho; log[3 * step + 1] = 0.0; log[3 * step + 2] = 0.0; }
             if (!trailing && k == n_iter && j == M - 1) break;
@@ -564,8 +584,28 @@ void or_oslalm_run(const or_geom* g, const double* y, const double* w, const dou
             int restart = xi > 0.0;
             if (mode == 1) l = restart ? 0 : l + 1;
             if (log) { log[3 * step + 1] = xi; log[3 * step + 2] = restart; }
+            if (bb)
+                for (size_t q = 0; q < N; q++) gbar[q] += G[q] / M;   /* mean of the iteration's M grad l_m */
         }
+        if (bb && step < n_iter * M) {   /* end of outer iteration k (completed) */
+            if (k >= 2) {
+                double num = 0.0, den = 0.0;
+                for (size_t q = 0; q < N; q++)
+                    if (mask[q]) {
+                        double sq = x[q] - xprev[q];
+                        num += (gbar[q] - gprev[q]) * sq;
+                        den += dl[q] * sq * sq;
+                    }
+                double a = den > 0.0 ? num / den : 1.0;
+                alpha = a > 1.0 ? 1.0 : (a < alpha_min ? alpha_min : a);
+            }
+            memcpy(xprev, x, N * sizeof(double));
+            memcpy(gprev, gbar, N * sizeof(double));
+            memset(gbar, 0, N * sizeof(double));
+        }
+    }
     if (g_out) memcpy(g_out, sg, N * sizeof(double));
     if (G_out) memcpy(G_out, G, N * sizeof(double));
-    free(order); free(G); free(Gp); free(sg); free(gr); free(cu); free(pbuf);
+    free(order); free(G); free(Gp); free(sg); free(gr); free(cu); free(pbuf); free(hd);
+    free(xprev); free(gbar); free(gprev);
 }
