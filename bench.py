@@ -223,6 +223,7 @@ def main():
     ap.add_argument("--iters", type=int, default=None, help="override n_iter (default: the config's)")
     ap.add_argument("--inner", default="sqs", choices=("sqs", "fista"), help="inner solver (NEXT-1: fista)")
     ap.add_argument("--n-inner", type=int, default=1, help="inner FISTA iterations (with --inner fista)")
+    ap.add_argument("--bb", action="store_true", help="Barzilai-Borwein scaling of the SQS Hessian (NEXT-2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -260,7 +261,7 @@ def main():
     scratch = torch.empty(ctlib.ct_sqs_denom_scratch_bytes(geo.h), dtype=torch.uint8, device=dev)
     x = torch.zeros(geo.img_shape, dtype=torch.float32, device=dev)
     sol = ctlib.OSLALM(geo, cfg.M, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr, inner=args.inner,
-                       n_inner=args.n_inner)
+                       n_inner=args.n_inner, bb=args.bb)
     sol.set_data(y, w, dl, mask)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -384,11 +385,12 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "iters_per_s": iters_per_s, "setup_ms_per_step": 1e3 * (T - Ti) / args.steps,
             "config": {"workload": workload_name(cfg), "config_id": cfg.name, "M": cfg.M, "n_iter": n_iter,
-                       "inner": f"{args.inner} x{args.n_inner}",
+                       "inner": f"{args.inner} x{args.n_inner}" + (" + BB" if args.bb else ""),
                        "views_per_subset": (g["na"] + cfg.M - 1) // cfg.M, "U_full_scan": U,
                        "nnz_full_scan": nnz, "work_per_step": work,
                        "l2": "flushed between steps (512 MiB write, untimed)",
-                       "parallelism": f"views of each subset split over {ws} GPU(s), NCCL all-reduce of G+"},
+                       "parallelism": (f"views of each subset split over {ws} GPU(s); NCCL reduce-scatter of G+ "
+                                       "into row slabs, slab update, all-gather of x+" if ws > 1 else "1 GPU")},
             "gpu_launches": int(launches), "roofline": roofline, "roofline_streaming": streaming,
             "kernel_ms": kernel_ms, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
             "peaks": {"fp32_tflops": pk["fp32_tflops"], "hbm_gbs": pk["hbm_gbs"], "src": pk["src"]},

@@ -170,6 +170,14 @@ typedef struct {
     int n_inner;      /* inner iterations: 1 for CT_INNER_SQS, 1..64 for FISTA   */
     int inner;        /* ct_inner_mode                                           */
     ct_reg reg;
+    /* Barzilai-Borwein scaling (NEXT-2, supplement P:1472-1492): with bb = 1 the
+     * SQS Hessian D_L is replaced by H_k = alpha_k D_L, alpha_k fitted to the secant
+     * equation y_k ~ H_k s_k in the D_L^{-1}-weighted least-squares sense, alpha <= 1:
+     *   alpha_k = min(1, max(alpha_min, y_k's_k / s_k'D_L s_k)),  s_k = x^k - x^{k-1},
+     * y_k = difference of the mean subset gradients of outer iterations k and k-1
+     * (reading B-BB); alpha = 1 for the first two outer iterations.          */
+    int bb;           /* 0 or 1                                                  */
+    double alpha_min; /* lower clip of alpha, in (0, 1] (1e-6)                   */
 } ct_oslalm_cfg;
 
 /* Caller-owned device arrays describing the problem. */
@@ -199,6 +207,7 @@ typedef struct {
     long long* l;    /* continuation counter                              */
     long long* step; /* inner steps taken                                 */
     int initialised; /* 0 until the first ct_oslalm_iter/run              */
+    double* alpha;   /* BB scale used by the next outer iteration (1 without BB) */
 } ct_oslalm_state_view;
 
 /*

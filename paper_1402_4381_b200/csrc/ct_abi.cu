@@ -493,7 +493,11 @@ struct ct_oslalm_state {
     bool has_comm = false;
     size_t S = 0, off0 = 0, Npad = 0;
     float* xp[2] = {nullptr, nullptr};   // full images (all-gathered), ping-pong
-    double* xi_ex = nullptr;             // [0] this rank's xi, [1] all-reduced xi
+    double* xi_ex = nullptr;             // [0] this rank's xi, [1] all-reduced xi, [2..3] BB sums
+    float* xprev = nullptr;              // BB: x after the previous outer iteration
+    float* gbar = nullptr;               // BB: mean subset gradient of the current iteration
+    float* gprev = nullptr;              // BB: ... of the previous iteration
+    double* bb_part = nullptr;
     double* xi_part;
     Scalars* sc;
     double* dlog;        // M x 3 doubles (per iteration)
@@ -572,6 +576,8 @@ static int check_cfg(const ct_geom* g, const ct_oslalm_cfg* c) {
         return fail(CT_EINVAL, "CT_INNER_SQS takes exactly one step (n_inner = %d); use CT_INNER_FISTA", c->n_inner);
     if (c->inner == CT_INNER_FISTA && (c->n_inner < 1 || c->n_inner > 64))
         return fail(CT_EINVAL, "n_inner = %d outside [1, 64]", c->n_inner);
+    if (c->bb != 0 && c->bb != 1) return fail(CT_EINVAL, "bb must be 0 or 1");
+    if (c->bb && !(c->alpha_min > 0 && c->alpha_min <= 1)) return fail(CT_EINVAL, "alpha_min must be in (0, 1]");
     return check_reg(g, &c->reg);
 }
 
@@ -588,7 +594,7 @@ static bool use_slabs(const ct_geom* g, const ct_oslalm_cfg* c) {
     return g->comm != nullptr && c->inner == CT_INNER_SQS;
 }
 
-static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[12], size_t* total) {
+static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16], size_t* total) {
     int iy0, iy1;
     size_t S;
     slab_geometry(g, g->nranks, g->rank, &iy0, &iy1, &S);
@@ -610,14 +616,15 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[12
     off[9] = o; o += two_v ? 2 * align256(N * 4) : 0;  // FISTA extrapolation points v (ping-pong)
     const bool slab = use_slabs(g, c);
     off[10] = o; o += slab ? 2 * align256(N * 4) : 0;  // slab path: all-gathered full images (ping-pong)
-    off[11] = o; o += align256(2 * 8);                 // xi exchange
+    off[11] = o; o += align256(4 * 8);                 // xi / BB sums exchange
+    off[12] = o; o += c->bb ? 3 * align256(N * 4) + align256(2 * 8 * nblk(N)) : 0;   // BB: x_prev, gbar, gbar_prev, partials
     *total = o;
 }
 
 extern "C" int ct_oslalm_state_bytes(const ct_geom* g, const ct_oslalm_cfg* c, size_t* out) {
     if (!g || !out) return fail(CT_EINVAL, "ct_oslalm_state_bytes: null argument");
     if (int e = check_cfg(g, c)) return e;
-    size_t off[12];
+    size_t off[16];
     state_layout(g, c, off, out);
     return CT_OK;
 }
@@ -626,7 +633,7 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
                                       ct_oslalm_state** out) {
     if (!g || !ws || !out) return fail(CT_EINVAL, "ct_oslalm_state_create: null argument");
     if (int e = check_cfg(g, c)) return e;
-    size_t off[12], total;
+    size_t off[16], total;
     state_layout(g, c, off, &total);
     if (bytes < total) return fail(CT_ENOMEM, "workspace of %zu bytes < required %zu", bytes, total);
     if ((uintptr_t)ws & 255) return fail(CT_EINVAL, "workspace must be 256-byte aligned");
@@ -663,6 +670,12 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
         s->xp[1] = (float*)(b + off[10] + align256(s->Npad * 4));
     }
     s->xi_ex = (double*)(b + off[11]);
+    if (c->bb) {
+        s->xprev = (float*)(b + off[12]);
+        s->gbar = (float*)(b + off[12] + align256(s->Npad * 4));
+        s->gprev = (float*)(b + off[12] + 2 * align256(s->Npad * 4));
+        s->bb_part = (double*)(b + off[12] + 3 * align256(s->Npad * 4));
+    }
     cudaError_t e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming);
@@ -714,6 +727,7 @@ extern "C" int ct_oslalm_state_get(const ct_oslalm_state* s, ct_oslalm_state_vie
     out->l = &s->sc->l;
     out->step = &s->sc->step;
     out->initialised = s->initialised;
+    out->alpha = &s->sc->alpha;
     return CT_OK;
 }
 
@@ -747,6 +761,8 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
     ga.rho_min = s->cfg.rho_min;
     ga.log3 = s->dlog;
     ga.log_slot = s->log_slot;
+    ga.gbar = epi == EPI_GUPD ? s->gbar : nullptr;   // BB: accumulate the iteration's mean subset gradient
+    ga.inv_M = 1.0f / (float)M;
     if (g->comm == nullptr) {   // single GPU: fused epilogue
         if (epi == EPI_INIT) {
             ga.G_new = s->Gbuf[s->curG];
@@ -826,12 +842,13 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
             if (ry1 > ry0) {
                 if (c.reg.nbr == 8)
                     sqs_update_kernel<8><<<nblk(rj1 - rj0), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl,
-                                                                          d->mask, &s->sc->rho, (float)c.reg.beta, inv_d,
-                                                                          rj0, rj1);
+                                                                          d->mask, &s->sc->rho, &s->sc->alpha, (float)c.reg.beta,
+                                                                          inv_d, rj0, rj1);
                 else
                     sqs_update3d_kernel<<<dim3((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (ry1 - ry0 + kK3Y - 1) / kK3Y),
                                           256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
-                                                        &s->sc->rho, (float)c.reg.beta, inv_d, ry0, ry1);
+                                                        &s->sc->rho, &s->sc->alpha, (float)c.reg.beta, inv_d, ry0,
+                                                        ry1);
                 CT_LAUNCHED(1);
             }
             if (s->slab) {   // every rank needs the full x+ for its next forward projection
@@ -850,7 +867,8 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
                 float* vout = last ? nullptr : s->vbuf[i & 1];
 #define CT_FISTA(NB, LAST)                                                                                         \
     fista_step_kernel<NB, LAST><<<nblk(s->N), 256, 0, st>>>(g->dg, v, xprev, xa, xb, vout, s->Gbuf[s->curG], s->gs, \
-                                                            d->dl, d->mask, &s->sc->rho, (float)c.reg.beta, inv_d, mom, s->N)
+                                                            d->dl, d->mask, &s->sc->rho, &s->sc->alpha, (float)c.reg.beta, \
+                                                            inv_d, mom, s->N)
                 if (c.reg.nbr == 8) {
                     if (last) CT_FISTA(8, true); else CT_FISTA(8, false);
                 } else {
@@ -871,6 +889,21 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
         s->curG ^= 1;
         kernels += 2 + (c.inner == CT_INNER_FISTA ? c.n_inner : 1) + (g->comm ? 1 : 0);
     }
+    if (c.bb) {
+        // Barzilai-Borwein scale for the next outer iteration (reading B-BB), over this rank's
+        // rows (all rows on one rank; gbar is valid on the rank's slab in the slab path)
+        const size_t bj0 = s->slab ? s->off0 : 0, bj1 = s->slab ? std::min(s->N, s->off0 + s->S) : s->N;
+        BBArgs bbA{xa, s->xprev, s->gbar, s->gprev, d->dl, d->mask, s->bb_part, g->comm ? s->xi_ex + 2 : nullptr,
+                   s->sc, c.alpha_min};
+        bb_alpha_kernel<<<nblk(std::max(bj1, bj0 + 1) - bj0), 256, 0, st>>>(bbA, bj0, bj1);
+        kernels += 1;
+        if (g->comm) {
+            ncclResult_t r = g_nccl.AllReduce(s->xi_ex + 2, s->xi_ex + 2, 2, ncclFloat64, ncclSum, g->comm, st);
+            if (r != ncclSuccess) return fail(CT_ENCCL, "ncclAllReduce(BB): %s", nccl_err(r));
+            bb_rule_kernel<<<1, 1, 0, st>>>(s->sc, s->xi_ex + 2, c.alpha_min);
+            kernels += 1;
+        }
+    }
     if (xa != x) {
         CT_CUDA(cudaMemcpyAsync(x, xa, s->N * 4, cudaMemcpyDeviceToDevice, st));
     }
@@ -886,6 +919,7 @@ static int ensure_initialised(ct_oslalm_state* s, const ct_oslalm_data* d, float
     CT_LAUNCHED(1);
     zero_offmask_kernel<<<nblk(s->N), 256, 0, st>>>(x, d->mask, s->N);
     CT_LAUNCHED(1);
+    if (c.bb) CT_CUDA(cudaMemsetAsync(s->gbar, 0, s->Npad * 4, st));
     if (int e = subset_gradient(s, d, x, s->order[0], EPI_INIT, st)) return e;
     s->initialised = 1;
     return CT_OK;
@@ -899,7 +933,7 @@ static int check_data(const ct_geom* g, const ct_oslalm_data* d, const float* x)
 static bool cfg_equal(const ct_oslalm_cfg& a, const ct_oslalm_cfg& b) {
     return a.M == b.M && a.mode == b.mode && a.rho_fixed == b.rho_fixed && a.rho_min == b.rho_min &&
            a.n_inner == b.n_inner && a.inner == b.inner && a.reg.beta == b.reg.beta && a.reg.delta == b.reg.delta &&
-           a.reg.nbr == b.reg.nbr;
+           a.reg.nbr == b.reg.nbr && a.bb == b.bb && a.alpha_min == b.alpha_min;
 }
 
 extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_data* d, ct_oslalm_state* s,
@@ -909,7 +943,7 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
     if (cfg && !cfg_equal(*cfg, s->cfg)) {
         if (int e = check_cfg(g, cfg)) return e;
         if (cfg->M != s->cfg.M) return fail(CT_ESTATE, "M changed after state creation");
-        if (cfg->inner != s->cfg.inner || cfg->n_inner != s->cfg.n_inner)
+        if (cfg->inner != s->cfg.inner || cfg->n_inner != s->cfg.n_inner || cfg->bb != s->cfg.bb)
             return fail(CT_ESTATE, "inner solver changed after state creation (workspace layout)");
         s->cfg = *cfg;
         for (auto& ge : s->graphs)

@@ -329,6 +329,10 @@ struct Scalars {
     long long step;    // inner steps taken
     unsigned int arrive;   // blocks of the current back-projection that have stored their xi partial
     int pad;
+    double alpha;      // Barzilai-Borwein scale of the SQS Hessian, H = alpha D_L (1 without BB)
+    long long kiter;   // outer iterations completed (BB secant bookkeeping)
+    unsigned int arrive_bb;
+    int pad2;
 };
 
 __device__ __forceinline__ double rho_l(long long l, double rho_min) {
@@ -354,6 +358,8 @@ struct GupdArgs {
     double rho_fixed, rho_min;
     double* log3;
     int log_slot;
+    float* gbar;           // BB (nullable): running mean of the iteration's subset gradients
+    float inv_M;
 };
 
 // xi = fixed-order fp64 sum of the partials; l <- (xi > 0) ? 0 : l + 1; rho <- rho_l.
@@ -436,6 +442,7 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
         float Gp = acc, G = ga.G_old[j], gg = ga.gs[j];
         ga.G_new[j] = Gp;
         ga.gs[j] = (rho * Gp + gg) / (1.0f + rho);
+        if (ga.gbar) ga.gbar[j] += Gp * ga.inv_M;
         if (ga.mask[j]) return (double)(gg - Gp) * (double)(Gp - G);
     }
     return 0.0;
@@ -784,8 +791,8 @@ template <int NBR>
 __global__ void __launch_bounds__(256) sqs_update_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
                                                         const float* __restrict__ G, const float* __restrict__ gs,
                                                         const float* __restrict__ dl, const uint8_t* __restrict__ m,
-                                                        const double* __restrict__ rho_p, float beta, float inv_delta,
-                                                        size_t j0, size_t N) {
+                                                        const double* __restrict__ rho_p, const double* __restrict__ alpha_p,
+                                                        float beta, float inv_delta, size_t j0, size_t N) {
     // updates voxels [j0, N) (multi-rank: this rank's slab of rows; x is the full image)
     size_t j = j0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= N) return;
@@ -801,8 +808,9 @@ __global__ void __launch_bounds__(256) sqs_update_kernel(DevGeom g, const float*
     float gr, cu;
     fair_stencil<NBR>(g, x, m, iy, ix, iz, xj, inv_delta, gr, cu);
     float rho = (float)*rho_p;
+    const float ra = rho * (float)*alpha_p;   // rho alpha: H = alpha D_L (BB; alpha = 1 otherwise)
     float s = rho * G[j] + (1.0f - rho) * gs[j];
-    float den = rho * dl[j] + 2.0f * beta * cu;
+    float den = ra * dl[j] + 2.0f * beta * cu;
     float v = xj - (s + beta * gr) / den;
     xn[j] = fmaxf(v, 0.0f);
 }
@@ -817,7 +825,8 @@ constexpr int kK3Y = 8;
 __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
                                                           const float* __restrict__ G, const float* __restrict__ gs,
                                                           const float* __restrict__ dl, const uint8_t* __restrict__ m,
-                                                          const double* __restrict__ rho_p, float beta, float inv_delta,
+                                                          const double* __restrict__ rho_p,
+                                                          const double* __restrict__ alpha_p, float beta, float inv_delta,
                                                           int iy_begin, int iy_end) {
     // updates rows [iy_begin, iy_end) (multi-rank: this rank's slab; x is the full image)
     __shared__ float Pl[3][10][34];
@@ -825,6 +834,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
     const int ix0 = blockIdx.x * 8, z0 = blockIdx.y * 32, iy0 = iy_begin + blockIdx.z * kK3Y;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
     const float rho = (float)*rho_p;
+    const float ra = rho * (float)*alpha_p;   // rho alpha (BB)
     auto load_plane = [&](int slot, int iy) {
         for (int e = threadIdx.x; e < 340; e += 256) {
             const int a = e / 34, b = e - a * 34;
@@ -874,7 +884,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                         }
                 }
                 const float sdir = rho * __ldg(&G[j]) + (1.0f - rho) * __ldg(&gs[j]);
-                const float den = rho * __ldg(&dl[j]) + 2.0f * beta * cu;
+                const float den = ra * __ldg(&dl[j]) + 2.0f * beta * cu;
                 xn[j] = fmaxf(xj - (sdir + beta * gr) / den, 0.0f);
             }
         }
@@ -891,8 +901,8 @@ __global__ void __launch_bounds__(256) fista_step_kernel(DevGeom g, const float*
                                                         const float* __restrict__ xk, float* xout, float* __restrict__ vout,
                                                         const float* __restrict__ G, const float* __restrict__ gs,
                                                         const float* __restrict__ dl, const uint8_t* __restrict__ m,
-                                                        const double* __restrict__ rho_p, float beta, float inv_delta,
-                                                        float mom, size_t N) {
+                                                        const double* __restrict__ rho_p, const double* __restrict__ alpha_p,
+                                                        float beta, float inv_delta, float mom, size_t N) {
     size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= N) return;
     if (!m[j]) {
@@ -926,7 +936,7 @@ __global__ void __launch_bounds__(256) fista_step_kernel(DevGeom g, const float*
                 sw += wgt;
             }
     const float rho = (float)*rho_p;
-    const float rdl = rho * dl[j];
+    const float rdl = rho * (float)*alpha_p * dl[j];   // rho H, H = alpha D_L (BB)
     const float s = rho * G[j] + (1.0f - rho) * gs[j];
     const float grad = beta * gr + rdl * (vj - xk[j]) + s;
     const float xp = xprev[j];
@@ -964,6 +974,7 @@ __global__ void __launch_bounds__(256) gupd_kernel(const float* __restrict__ Gp,
         float P = Gp[j], G = ga.G_old[j], gg = ga.gs[j];
         ga.G_new[j] = P;
         ga.gs[j] = (rho * P + gg) / (1.0f + rho);
+        if (ga.gbar) ga.gbar[j] += P * ga.inv_M;
         if (ga.mask[j]) xi = (double)(gg - P) * (double)(P - G);
     }
     block_sum_store<256>(xi, &ga.xi_part[blockIdx.x]);
@@ -980,6 +991,7 @@ __global__ void __launch_bounds__(256) gupd_slab_kernel(GupdArgs ga, size_t j0, 
         const float rho = (float)*ga.rho;
         const float P = ga.G_new[j], G = ga.G_old[j], gg = ga.gs[j];
         ga.gs[j] = (rho * P + gg) / (1.0f + rho);
+        if (ga.gbar) ga.gbar[j] += P * ga.inv_M;
         if (ga.mask[j]) xi = (double)(gg - P) * (double)(P - G);
     }
     block_sum_store<256>(xi, &ga.xi_part[blockIdx.x]);
@@ -999,6 +1011,79 @@ __global__ void __launch_bounds__(256) gupd_slab_kernel(GupdArgs ga, size_t j0, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Barzilai-Borwein scale (NEXT-2, reading B-BB): at the end of outer
+// iteration k, over S and voxels [j0, j1) (this rank's rows):
+//   num = sum (gbar_k - gbar_{k-1})(x^k - x^{k-1}),  den = sum D_L (x^k - x^{k-1})^2,
+// then x_prev <- x, gbar_prev <- gbar, gbar <- 0.  The last block (single rank) sets
+// alpha = clip(num / den, alpha_min, 1) once two iterations are complete; with several
+// ranks it stores (num, den) for an all-reduce and bb_rule_kernel applies the rule.
+struct BBArgs {
+    const float* x;
+    float* xprev;
+    float* gbar;
+    float* gprev;
+    const float* dl;
+    const uint8_t* mask;
+    double* part;          // 2 per block
+    double* out2;          // multi-rank: this rank's (num, den); nullptr: finalize here
+    Scalars* sc;
+    double alpha_min;
+};
+
+__device__ __forceinline__ void bb_rule(Scalars* sc, double num, double den, double alpha_min) {
+    sc->kiter += 1;
+    if (sc->kiter >= 2) {
+        double a = den > 0.0 ? num / den : 1.0;
+        sc->alpha = a > 1.0 ? 1.0 : (a < alpha_min ? alpha_min : a);
+    }
+}
+
+__global__ void __launch_bounds__(256) bb_alpha_kernel(BBArgs b, size_t j0, size_t j1) {
+    const size_t j = j0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double num = 0.0, den = 0.0;
+    if (j < j1) {
+        const float xj = b.x[j], gj = b.gbar[j];
+        if (b.mask[j]) {
+            const double sq = (double)xj - (double)b.xprev[j];
+            num = ((double)gj - (double)b.gprev[j]) * sq;
+            den = (double)b.dl[j] * sq * sq;
+        }
+        b.xprev[j] = xj;
+        b.gprev[j] = gj;
+        b.gbar[j] = 0.0f;
+    }
+    block_sum_store<256>(num, &b.part[2 * blockIdx.x]);
+    __syncthreads();   // block_sum_store's shared scratch is reused
+    block_sum_store<256>(den, &b.part[2 * blockIdx.x + 1]);
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&b.sc->arrive_bb, 1u);
+        last = (prev == gridDim.x - 1u);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double sn = 0.0, sd = 0.0;
+        for (unsigned q = 0; q < gridDim.x; q++) {
+            sn += __ldcg(&b.part[2 * q]);
+            sd += __ldcg(&b.part[2 * q + 1]);
+        }
+        b.sc->arrive_bb = 0;
+        if (b.out2) {
+            b.out2[0] = sn;
+            b.out2[1] = sd;
+        } else {
+            bb_rule(b.sc, sn, sd, b.alpha_min);
+        }
+    }
+}
+
+__global__ void bb_rule_kernel(Scalars* sc, const double* sums2, double alpha_min) {
+    bb_rule(sc, sums2[0], sums2[1], alpha_min);
+}
+
 // K4 on the all-reduced xi (one block)
 __global__ void __launch_bounds__(256) xi_rule_kernel(GupdArgs ga, const double* xi_glob) {
     xi_finalize_block<256>(xi_glob, 1, ga);
@@ -1012,6 +1097,9 @@ __global__ void init_scalars_kernel(Scalars* sc, double rho0) {
     sc->l = 0;
     sc->step = 0;
     sc->arrive = 0;
+    sc->alpha = 1.0;
+    sc->kiter = 0;
+    sc->arrive_bb = 0;
 }
 
 // ---------------------------------------------------------------------------

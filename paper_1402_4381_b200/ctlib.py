@@ -56,7 +56,8 @@ class ct_reg(ctypes.Structure):
 
 class ct_oslalm_cfg(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int), ("mode", ctypes.c_int), ("rho_fixed", ctypes.c_double),
-                ("rho_min", ctypes.c_double), ("n_inner", ctypes.c_int), ("inner", ctypes.c_int), ("reg", ct_reg)]
+                ("rho_min", ctypes.c_double), ("n_inner", ctypes.c_int), ("inner", ctypes.c_int), ("reg", ct_reg),
+                ("bb", ctypes.c_int), ("alpha_min", ctypes.c_double)]
 
 
 class ct_oslalm_data(ctypes.Structure):
@@ -70,7 +71,7 @@ class ct_oslalm_log(ctypes.Structure):
 
 class ct_oslalm_state_view(ctypes.Structure):
     _fields_ = [("g", ctypes.c_void_p), ("G", ctypes.c_void_p), ("rho", ctypes.c_void_p), ("l", ctypes.c_void_p),
-                ("step", ctypes.c_void_p), ("initialised", ctypes.c_int)]
+                ("step", ctypes.c_void_p), ("initialised", ctypes.c_int), ("alpha", ctypes.c_void_p)]
 
 
 _lib = None
@@ -290,10 +291,11 @@ class OSLALM:
     """OS-LALM solver state over a caller-owned (torch) device workspace."""
 
     def __init__(self, geo: Geometry, M, *, mode="continuation", rho_fixed=1.0, rho_min=1e-3, beta, delta, nbr,
-                 n_inner=1, inner="sqs"):
+                 n_inner=1, inner="sqs", bb=False, alpha_min=1e-6):
         self.geo = geo
         self.cfg = ct_oslalm_cfg(int(M), 1 if mode == "continuation" else 0, float(rho_fixed), float(rho_min),
-                                 int(n_inner), 0 if inner == "sqs" else 1, ct_reg(float(beta), float(delta), int(nbr)))
+                                 int(n_inner), 0 if inner == "sqs" else 1, ct_reg(float(beta), float(delta), int(nbr)),
+                                 1 if bb else 0, float(alpha_min))
         L = load()
         n = ctypes.c_size_t()
         _check(L.ct_oslalm_state_bytes(geo.h, ctypes.byref(self.cfg), ctypes.byref(n)))
@@ -375,3 +377,7 @@ class OSLALM:
         l = self._ws_view(v.l, 1, torch.int64).item()
         st = self._ws_view(v.step, 1, torch.int64).item()
         return rho, l, st
+
+    def alpha(self):
+        """Barzilai-Borwein scale alpha used by the next outer iteration (1.0 without BB)."""
+        return self._ws_view(self.state().alpha, 1, torch.float64).item()

@@ -410,3 +410,42 @@ def test_inner_mode_validation(ct):
         ct.OSLALM(geo, 4, beta=1.0, delta=1e-3, nbr=8, inner="sqs", n_inner=2)
     with pytest.raises(ct.CTError, match="CT_EINVAL"):
         ct.OSLALM(geo, 4, beta=1.0, delta=1e-3, nbr=8, inner="fista", n_inner=0)
+
+
+# --------------------------------------------------------------------------- BB (NEXT-2)
+
+@pytest.mark.parametrize("M,n_iter,comm", [(4, 12, False), (1, 30, False), (4, 8, True)])
+def test_oslalm_bb_c1(ct, O, M, n_iter, comm):
+    """Barzilai-Borwein scaling H_k = alpha_k D_L (reading B-BB) against
+    the fp64 oracle: alpha per outer iteration, restart decisions and the image (<= 0.5 HU).
+    comm = True runs the 1-rank slab exchange path (BB sums all-reduced)."""
+    cfg = I.config("c1")
+    g = cfg.geom
+    d = I.synthesize(cfg)
+    geo = ct.Geometry(g)
+    if comm:
+        geo.comm_init(0, 1, ct.ct_comm_get_unique_id())
+    m0 = I.support_mask(cfg)
+    dl, S = geo.sqs_denom(d["w"].cuda(), m0.cuda())
+    sol = ct.OSLALM(geo, M, beta=cfg.beta, delta=cfg.delta, nbr=8, bb=True)
+    sol.set_data(d["y"].cuda(), d["w"].cuda(), dl, S)
+    x = torch.zeros(geo.img_shape, device="cuda")
+    alphas, logs = [1.0], []
+    for k in range(n_iter):
+        logs.append(np.array(sol.run(x, 1, log=True)))
+        alphas.append(sol.alpha())
+    log = np.concatenate(logs)
+    dlo, So = O.sqs_denom(g, I.to_oracle_sino(d["w"]), I.to_oracle_image(m0).astype(np.uint8))
+    ao = np.zeros(n_iter)
+    xo, logo, _, _ = O.oslalm_run(g, I.to_oracle_sino(d["y"]), I.to_oracle_sino(d["w"]), dlo, So,
+                                  np.zeros(O.img_shape(g)), M=M, beta=cfg.beta, delta=cfg.delta, nbr=8,
+                                  n_iter=n_iter, bb=True, alpha_out=ao)
+    a_gpu = np.array(alphas[:n_iter])
+    assert (ao[2:] < 1.0).any()
+    assert np.allclose(a_gpu, ao, rtol=2e-3), (a_gpu, ao)
+    assert np.array_equal(log[:, 2], logo[:, 2])
+    xg = I.to_oracle_image(x.cpu().numpy())
+    rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
+    MARGINS.append({"case": f"OS-LALM+BB c1 M={M} iters={n_iter} comm={comm}", "rms_HU": rms,
+                    "alpha_max_rel": float(np.abs(a_gpu / ao - 1).max())})
+    assert rms <= 0.5, rms
