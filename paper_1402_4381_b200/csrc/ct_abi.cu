@@ -840,7 +840,11 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
         int t0 = tmark(s, st);
         if (c.inner == CT_INNER_SQS) {
             if (ry1 > ry0) {
-                if (c.reg.nbr == 8)
+                if (c.reg.nbr == 8 && nz_of(g) == 1)
+                    sqs_update2d_kernel<<<dim3((g->dg.nx + 31) / 32, (ry1 - ry0 + 7) / 8), 256, 0, st>>>(
+                        g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask, &s->sc->rho, &s->sc->alpha,
+                        (float)c.reg.beta, inv_d, ry0, ry1);
+                else if (c.reg.nbr == 8)
                     sqs_update_kernel<8><<<nblk(rj1 - rj0), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl,
                                                                           d->mask, &s->sc->rho, &s->sc->alpha, (float)c.reg.beta,
                                                                           inv_d, rj0, rj1);

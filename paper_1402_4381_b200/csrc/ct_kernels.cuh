@@ -892,6 +892,61 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
     }
 }
 
+// 2D (8-neighbour) K3 with a shared-memory tile: block = 32 (ix) x 8 (iy) pixels, the
+// 34 x 10 halo tile of x holds NaN outside S or the grid (pair rule = one comparison).
+__global__ void __launch_bounds__(256) sqs_update2d_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
+                                                          const float* __restrict__ G, const float* __restrict__ gs,
+                                                          const float* __restrict__ dl, const uint8_t* __restrict__ m,
+                                                          const double* __restrict__ rho_p,
+                                                          const double* __restrict__ alpha_p, float beta, float inv_delta,
+                                                          int iy_begin, int iy_end) {
+    // updates rows [iy_begin, iy_end) (multi-rank: this rank's slab; x is the full image)
+    __shared__ float T[10][34];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int ix0 = blockIdx.x * 32, iy0 = iy_begin + blockIdx.y * 8;
+    const int nx = g.nx;
+    for (int e = threadIdx.x; e < 340; e += 256) {
+        const int a = e / 34, b = e - a * 34;
+        const int iy = iy0 - 1 + a, ix = ix0 - 1 + b;
+        float v = __int_as_float(0x7fc00000);   // NaN: not in S
+        if (iy >= 0 && iy < g.ny && ix >= 0 && ix < nx) {
+            const int j = iy * nx + ix;
+            if (__ldg(&m[j])) v = __ldg(&x[j]);
+        }
+        T[a][b] = v;
+    }
+    __syncthreads();
+    const int ix = ix0 + tx, iy = iy0 + ty;
+    if (ix >= nx || iy >= iy_end) return;
+    const int j = iy * nx + ix;
+    const float xj = T[ty + 1][tx + 1];
+    if (xj != xj) {
+        xn[j] = 0.0f;   // off S
+        return;
+    }
+    constexpr float r2 = 0.70710678118654752f;
+    float gr = 0.0f, cu = 0.0f;
+#pragma unroll
+    for (int oy = -1; oy <= 1; oy++)
+#pragma unroll
+        for (int ox = -1; ox <= 1; ox++) {
+            if (oy == 0 && ox == 0) continue;
+            const float wgt = (oy * oy + ox * ox) == 1 ? 1.0f : r2;
+            const float xk = T[ty + 1 + oy][tx + 1 + ox];
+            if (xk == xk) {
+                float dpsi, om;
+                fair(xj - xk, inv_delta, dpsi, om);
+                gr += wgt * dpsi;
+                cu += wgt * om;
+            }
+        }
+    const float rho = (float)*rho_p;
+    const float ra = rho * (float)*alpha_p;   // rho alpha: H = alpha D_L (BB; alpha = 1 otherwise)
+    const float sdir = rho * __ldg(&G[j]) + (1.0f - rho) * __ldg(&gs[j]);
+    const float den = ra * __ldg(&dl[j]) + 2.0f * beta * cu;
+    xn[j] = fmaxf(xj - (sdir + beta * gr) / den, 0.0f);
+}
+
 // One FISTA iteration of the inner denoising problem (NEXT-1):
 //   x_i = max(0, v - (grad R(v) + rho D_L (v - x_k) + s) / (rho D_L + 2 beta sum w)),  s = rho G + (1-rho) g
 //   v_i = x_i + mom (x_i - x_{i-1})            (skipped on the last iteration)
