@@ -31,10 +31,6 @@ __device__ __forceinline__ float vertex_ch(const DevGeom& g, float sb, float cb,
     return __fmul_rn(fast_atan(__fdividef(perp, along)), g.dsd_ds);
 }
 
-// Left edge of detector bin c in centred channel units (bin c spans [L(c), L(c + 1)]);
-// cedge = cbase + 1/2 is rounded once on the host, so L(c) is the same float everywhere.
-__device__ __forceinline__ float bin_edge(const DevGeom& g, int c) { return __fsub_rn((float)c, g.cedge); }
-
 // Footprint of one pixel for one view (centred channel units).
 struct Foot2 {
     float t0, t1, t2, t3;   // sorted breakpoints
@@ -44,8 +40,8 @@ struct Foot2 {
 };
 
 // CLAMP = false (forward tiles): cA / n describe the unclipped footprint (bins may lie off
-// the detector; the caller drops them).  Bin edges are evaluated from the channel index
-// alone (bin_edge), so the on-detector weights are bit-identical to the clamped ones.
+// the detector; the caller drops them).  On-detector bin edges are evaluated exactly
+// (Trap2), so the weights are bit-identical to the clamped ones.
 template <bool CLAMP = true>
 __device__ __forceinline__ void pixel_foot(const DevGeom& g, float sb, float cb, float xc, float yc, float v00, float v10,
                                            float v01, float v11, Foot2& f) {
@@ -75,16 +71,23 @@ __device__ __forceinline__ void pixel_foot(const DevGeom& g, float sb, float cb,
 
 // Unit-height trapezoid CDF in coordinates u = s - t0 (branch-free, degenerate widths
 // safe).  F(u) = a^2/(2 w1) + m + b - b^2/(2 w3) with a, m, b the clamped pieces.
+// Bin edges: with t0a = t0 + cedge (absolute channel coordinate of t0) and c0 =
+// max(cA, 0) the first on-detector bin, u(c) = (c0 - t0a) + (c - c0).  c0 - t0a is exact
+// (Sterbenz: c0 = floor(t0a) >= t0a / 2, or c0 = 0), and adding small integers keeps it
+// exact, so the clipped (back) and unclipped (forward) footprints evaluate every
+// on-detector edge from the same float — bit-identical weights — with one add per edge.
 struct Trap2 {
-    float t0, w1, t2r, t3r, h0, h3, mass;
-    __device__ __forceinline__ explicit Trap2(const Foot2& f) {
-        t0 = f.t0;
+    float w1, t2r, t3r, h0, h3, mass, u0;
+    int c0;
+    __device__ __forceinline__ Trap2(const DevGeom& g, const Foot2& f) {
         w1 = __fsub_rn(f.t1, f.t0);
         t2r = __fsub_rn(f.t2, f.t0);
         t3r = __fsub_rn(f.t3, f.t0);
         h0 = __fdividef(0.5f, fmaxf(w1, 1e-20f));
         h3 = __fdividef(0.5f, fmaxf(__fsub_rn(t3r, t2r), 1e-20f));
         mass = __fmul_rn(0.5f, __fsub_rn(__fadd_rn(t3r, t2r), w1));   // (t3 + t2 - t1 - t0) / 2
+        c0 = max(f.cA, 0);
+        u0 = __fsub_rn((float)c0, __fadd_rn(f.t0, g.cedge));
     }
     __device__ __forceinline__ float F(float u) const {
         const float a = fminf(fmaxf(u, 0.0f), w1);
@@ -92,8 +95,6 @@ struct Trap2 {
         const float b = __fsub_rn(fminf(fmaxf(u, t2r), t3r), t2r);
         return fmaf(-__fmul_rn(b, b), h3, fmaf(__fmul_rn(a, a), h0, __fadd_rn(m, b)));
     }
-    // CDF at the left edge of bin c
-    __device__ __forceinline__ float at(const DevGeom& g, int c) const { return F(__fsub_rn(bin_edge(g, c), t0)); }
 };
 
 // sum_j lphi F_s(cA + j) yk[j]: the n - 1 interior bin edges are evaluated once each.
@@ -104,17 +105,17 @@ __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, cons
 #pragma unroll
     for (int j = 0; j < kPre; j++) yv[j] = (j + 1 < f.n) ? __ldg(&yk[j]) : 0.0f;
     const float ylast = __ldg(&yk[f.n - 1]);
-    const Trap2 T(f);
+    const Trap2 T(g, f);   // clamped footprint: c0 = cA
     // F = 0 left of t0 and F = mass right of t3: only clipped ends need an evaluation
-    float Fp = f.clL ? T.at(g, f.cA) : 0.0f, s = 0.0f;
+    float Fp = f.clL ? T.F(T.u0) : 0.0f, s = 0.0f;
 #pragma unroll
     for (int j = 0; j < kMaxFoot - 1; j++) {
         if (j + 1 >= f.n) break;
-        const float Fn = T.at(g, f.cA + j + 1);
+        const float Fn = T.F(__fadd_rn(T.u0, (float)(j + 1)));
         s = fmaf(__fsub_rn(Fn, Fp), j < kPre ? yv[j < kPre ? j : 0] : __ldg(&yk[j]), s);
         Fp = Fn;
     }
-    const float Fend = f.clR ? T.at(g, f.cA + f.n) : T.mass;
+    const float Fend = f.clR ? T.F(__fadd_rn(T.u0, (float)f.n)) : T.mass;
     s = fmaf(__fsub_rn(Fend, Fp), ylast, s);
     return f.lphi * s;
 }
@@ -214,15 +215,19 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
                 }
                 const int nmax = __reduce_max_sync(0xffffffffu, n);
                 if (nmax == 0) continue;
-                const Trap2 T(f);
+                const Trap2 T(g, f);
                 const float lx = f.lphi * xv;
                 float* bp = mybuf + (f.cA - cLoU);
+                // edge cA + j + 1 = c0 + k, k = (cA - c0) + j + 1 an exact small integer in fp32:
+                // u = u0 + k rounds exactly as in the back-projector (edges left of channel 0
+                // only feed dropped bins)
+                const float koff = (float)(f.cA - T.c0);
                 float Fp = 0.0f;   // unclipped: F = 0 at the left edge of bin cA
 #pragma unroll
                 for (int j = 0; j < kMaxFoot; j++) {
                     if (j >= nmax) break;
                     // bins j >= n add exactly 0 (Fn = Fp = mass) to distinct addresses
-                    const float Fn = (j + 1 < n) ? T.at(g, f.cA + j + 1) : T.mass;
+                    const float Fn = (j + 1 < n) ? T.F(__fadd_rn(T.u0, koff + (float)(j + 1))) : T.mass;
                     if (act) bp[j] += lx * __fsub_rn(Fn, Fp);
                     Fp = Fn;
                     __syncwarp();   // round j's stores are visible to round j + 1's loads
