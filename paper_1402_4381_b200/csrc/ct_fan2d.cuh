@@ -89,11 +89,15 @@ struct Trap2 {
         c0 = max(f.cA, 0);
         u0 = __fsub_rn((float)c0, __fadd_rn(f.t0, g.cedge));
     }
+    // Evaluated only at edges with u > 0 (interior edges, and the clipped edge at channel
+    // 0 or ns: u0 = c0 - t0a > 0 there), so the rise piece needs no lower clamp; the fall
+    // piece keeps both clamps (u may exceed t3r by rounding, and w3 may be ~0).
+    // m + b = clamp(u, w1, t3r) - w1 for the flat and fall pieces together.
     __device__ __forceinline__ float F(float u) const {
-        const float a = fminf(fmaxf(u, 0.0f), w1);
-        const float m = __fsub_rn(fminf(fmaxf(u, w1), t2r), w1);
+        const float a = fminf(u, w1);
+        const float mb = __fsub_rn(fminf(fmaxf(u, w1), t3r), w1);
         const float b = __fsub_rn(fminf(fmaxf(u, t2r), t3r), t2r);
-        return fmaf(-__fmul_rn(b, b), h3, fmaf(__fmul_rn(a, a), h0, __fadd_rn(m, b)));
+        return fmaf(-__fmul_rn(b, b), h3, fmaf(__fmul_rn(a, a), h0, mb));
     }
 };
 
