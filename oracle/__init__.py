@@ -86,6 +86,7 @@ def lib():
         L.or_oslalm_run.argtypes = [G, dp, dp, dp, u8, i, i, d, d, d, d, i, i, i, dp, dp, dp, dp, i, i, i, d, dp]
         L.or_inner_fista.argtypes = [G, d, d, i, u8, dp, d, dp, dp, i, dp]
         L.or_inner_fista.restype = None
+        L.or_fbp.argtypes = [G, dp, dp]; L.or_fbp.restype = i
         L.or_oslalm_run.restype = None
         _lib = L
     return _lib
@@ -244,6 +245,17 @@ def inner_fista(g, beta, delta, nbr, mask, dl, rho, xk, s, n):
     _, op = _d(out)
     lib().or_inner_fista(geom(g), beta, delta, nbr, mp, dp, rho, xp, sp, n, op)
     return out
+
+
+def fbp(g, p):
+    """FBP (fan) / FDK (cone, circular orbit) initial image of sinogram p (reading B-FBP);
+    raises for helical scans."""
+    p, pp = _d(np.reshape(p, sino_shape(g, g["na"])))
+    x = np.zeros(img_shape(g))
+    _, xp = _d(x)
+    if lib().or_fbp(geom(g), pp, xp) != 0:
+        raise ValueError("FBP needs a fan or axial cone scan over one full turn")
+    return x
 
 
 def oslalm_run(g, y, w, dl, mask, x0, *, M, mode="continuation", rho_fixed=1.0, rho_min=1e-3,

@@ -609,3 +609,83 @@ void or_oslalm_run(const or_geom* g, const double* y, const double* w, const dou
     free(order); free(G); free(Gp); free(sg); free(gr); free(cu); free(pbuf); free(hd);
     free(xprev); free(gbar); free(gprev);
 }
+
+/* ---------------- NEXT-4: FBP / FDK initial image ---------------- */
+/*
+ * Filtered back-projection for the initial image x^0 ("initialized with a
+ * standard filtered back-projection (FBP) reconstruction"; the paper does not say
+ * which FBP — reading B-FBP in DESIGN.md: the textbook full-scan equiangular
+ * fan-beam FBP (Kak & Slaney, eqs. 3.4.1), with the FDK cone-beam extension for a
+ * cylindrical detector on a circular orbit):
+ *   R'(gamma_k, t) = R(gamma_k, t) * D cos(gamma_k) * D / sqrt(D^2 + zeta^2),
+ *                    zeta = t dso/dsd (row height at the rotation axis; 1 in 2D)
+ *   Q(gamma_n, t)  = tau * sum_k R'(gamma_k, t) g((n - k) tau)     (row-wise)
+ *   g(n tau)       = 1/(8 tau^2) (n = 0), 0 (n even), -1/(2 pi^2 sin^2(n tau)) (n odd)
+ *   f(p)           = dbeta * sum_v Q_v(gamma(p), t(p)) / L(p)^2
+ * with D = dso, tau = ds/dsd the angular channel pitch, L the in-plane source-voxel
+ * distance, gamma(p) / t(p) the fan angle / detector row height of the voxel centre
+ * (O1), linear interpolation in gamma and t (0 outside the detector), dbeta = 2 pi / na.
+ * Returns 0, or -1 for a helical scan or an orbit that is not one full turn.
+ */
+int or_fbp(const or_geom* g, const double* p, double* x) {
+    if (g->kind == OR_CONE_HELICAL || fabs(g->orbit_deg - 360.0) > 1e-9) return -1;
+    int NT = ntv(g), NZ = nzv(g);
+    double D = g->dso, tau = g->ds / g->dsd;
+    int ns = g->ns;
+    size_t cells = (size_t)NT * ns;
+    double* q = (double*)malloc((size_t)g->na * cells * sizeof(double));
+    double* gk = (double*)malloc((2 * (size_t)ns - 1) * sizeof(double));
+    for (int n = -(ns - 1); n <= ns - 1; n++) {
+        double v;
+        if (n == 0) v = 1.0 / (8.0 * tau * tau);
+        else if (n % 2 == 0) v = 0.0;
+        else { double s = sin(n * tau); v = -1.0 / (2.0 * M_PI * M_PI * s * s); }
+        gk[n + ns - 1] = v;
+    }
+#pragma omp parallel for schedule(dynamic)
+    for (int v = 0; v < g->na; v++) {
+        double* rp = (double*)malloc((size_t)ns * sizeof(double));
+        for (int r = 0; r < NT; r++) {
+            double zeta = g->kind == OR_FAN2D ? 0.0 : row_t(g, r) * g->dso / g->dsd;
+            for (int k = 0; k < ns; k++) {
+                double gam = chan_s(g, k) / g->dsd;
+                rp[k] = p[((size_t)v * NT + r) * ns + k] * D * cos(gam) * D / sqrt(D * D + zeta * zeta);
+            }
+            for (int n = 0; n < ns; n++) {
+                double acc = 0.0;
+                for (int k = 0; k < ns; k++) acc += rp[k] * gk[n - k + ns - 1];
+                q[((size_t)v * NT + r) * ns + n] = tau * acc;
+            }
+        }
+        free(rp);
+    }
+    double dbeta = 2.0 * M_PI / g->na;
+    double c0 = (ns - 1) / 2.0 + g->offs, r0 = (NT - 1) / 2.0 + g->offt;
+#pragma omp parallel for schedule(dynamic)
+    for (int iy = 0; iy < g->ny; iy++)
+        for (int iz = 0; iz < NZ; iz++)
+            for (int ix = 0; ix < g->nx; ix++) {
+                double xc = vox_x(g, ix), yc = vox_y(g, iy), zc = vox_z(g, iz), acc = 0.0;
+                for (int v = 0; v < g->na; v++) {
+                    double b = or_view_angle(g, v), sb = sin(b), cb = cos(b);
+                    double along = D + xc * sb - yc * cb, perp = xc * cb + yc * sb;
+                    double L2 = along * along + perp * perp;
+                    double uc = atan2(perp, along) / tau + c0;         /* channel coordinate */
+                    double ur = g->kind == OR_FAN2D ? 0.0 : (zc - or_source_z(g, v)) * g->dsd / sqrt(L2) / g->dt + r0;
+                    int k0 = (int)floor(uc), r0i = (int)floor(ur);
+                    double fk = uc - k0, fr = ur - r0i, val = 0.0;
+                    for (int a = 0; a < 2; a++)
+                        for (int bq = 0; bq < (NT > 1 ? 2 : 1); bq++) {
+                            int k = k0 + a, r = NT > 1 ? r0i + bq : 0;
+                            if (k < 0 || k >= ns || r < 0 || r >= NT) continue;
+                            double wk = a ? fk : 1.0 - fk, wr = NT > 1 ? (bq ? fr : 1.0 - fr) : 1.0;
+                            val += wk * wr * q[((size_t)v * NT + r) * ns + k];
+                        }
+                    acc += val / L2;
+                }
+                x[((size_t)iz * g->ny + iy) * g->nx + ix] = dbeta * acc;
+            }
+    free(q);
+    free(gk);
+    return 0;
+}
