@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--inner", default="sqs", choices=("sqs", "fista"), help="inner solver (NEXT-1: fista)")
     ap.add_argument("--n-inner", type=int, default=1, help="inner FISTA iterations (with --inner fista)")
     ap.add_argument("--bb", action="store_true", help="Barzilai-Borwein scaling of the SQS Hessian (NEXT-2)")
+    ap.add_argument("--init", default="zero", choices=("zero", "fbp"),
+                    help="initial image: zero on S (G10) or the FBP/FDK image (NEXT-4, P:586; inside the timed step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -264,6 +266,8 @@ def main():
                        n_inner=args.n_inner, bb=args.bb)
     sol.set_data(y, w, dl, mask)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    fbp_scratch = (torch.empty(ctlib.ct_fbp_scratch_bytes(geo.h), dtype=torch.uint8, device=dev)
+                   if args.init == "fbp" else None)
 
     def step(ev=None):
         mask.copy_(m0)
@@ -271,7 +275,10 @@ def main():
         if ev is not None:
             ev.record()
         sol.reset()
-        x.zero_()
+        if args.init == "fbp":
+            ctlib.ct_fbp(geo.h, y, x, fbp_scratch)
+        else:
+            x.zero_()
         for _ in range(n_iter):
             sol.iterate(x)
 
@@ -385,7 +392,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "iters_per_s": iters_per_s, "setup_ms_per_step": 1e3 * (T - Ti) / args.steps,
             "config": {"workload": workload_name(cfg), "config_id": cfg.name, "M": cfg.M, "n_iter": n_iter,
-                       "inner": f"{args.inner} x{args.n_inner}" + (" + BB" if args.bb else ""),
+                       "inner": f"{args.inner} x{args.n_inner}" + (" + BB" if args.bb else ""), "init": args.init,
                        "views_per_subset": (g["na"] + cfg.M - 1) // cfg.M, "U_full_scan": U,
                        "nnz_full_scan": nnz, "work_per_step": work,
                        "l2": "flushed between steps (512 MiB write, untimed)",

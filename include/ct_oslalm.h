@@ -152,6 +152,21 @@ int ct_count_vv(const ct_geom* g, ct_views v, const uint8_t* mask, void* scratch
 
 /* ------------------------------------------------------------------------ */
 /* OS-LALM                                                                  */
+/*
+ * FBP / FDK initial image x^0 (NEXT-4; "initialized with a standard filtered
+ * back-projection (FBP) reconstruction"; reading B-FBP): full-scan equiangular
+ * fan-beam FBP (Ram-Lak taps, cos gamma pre-weight, 1/L^2 back-projection weight,
+ * linear interpolation), with the FDK extension (cone weight D / sqrt(D^2 + zeta^2),
+ * bilinear interpolation) for axial cone beam.
+ *   y        : [na][ns][nt] post-log sinogram (device, read-only)
+ *   x        : [ny][nx][nz] output image in mm^-1 (device, overwritten)
+ *   scratch  : ct_fbp_scratch_bytes() bytes of device memory (filtered sinogram)
+ * Errors: CT_EINVAL (null pointers), CT_EUNSUPPORTED (helical scan, or an orbit that is
+ * not one full turn).  The image is not clipped to x >= 0 (OS-LALM's first update does).
+ */
+int ct_fbp_scratch_bytes(const ct_geom* g, size_t* out);
+int ct_fbp(const ct_geom* g, const float* y, float* x, void* scratch, void* stream);
+
 /* ------------------------------------------------------------------------ */
 
 typedef enum { CT_RHO_FIXED = 0, CT_RHO_CONTINUATION = 1 } ct_rho_mode;

@@ -17,6 +17,7 @@
 #include "../../include/ct_oslalm.h"
 #include "ct_kernels.cuh"
 #include "ct_fan2d.cuh"
+#include "ct_fbp.cuh"
 
 using namespace ct;
 
@@ -389,6 +390,35 @@ extern "C" int ct_back_proj(const ct_geom* g, ct_views v, const float* y, float*
     GupdArgs ga{};
     if (accumulate) return launch_back<EPI_ACCUM>(g, v, y, x, ga, (cudaStream_t)stream);
     return launch_back<EPI_STORE>(g, v, y, x, ga, (cudaStream_t)stream);
+}
+
+// FBP / FDK initial image (NEXT-4; reading B-FBP)
+static int check_fbp(const ct_geom* g) {
+    if (g->d.kind == CT_CONE_HELICAL) return fail(CT_EUNSUPPORTED, "ct_fbp: helical scans are not supported");
+    if (fabs(g->d.orbit_deg - 360.0) > 1e-9) return fail(CT_EUNSUPPORTED, "ct_fbp needs one full turn (orbit 360 deg)");
+    return CT_OK;
+}
+
+extern "C" int ct_fbp_scratch_bytes(const ct_geom* g, size_t* out) {
+    if (!g || !out) return fail(CT_EINVAL, "ct_fbp_scratch_bytes: null argument");
+    if (int e = check_fbp(g)) return e;
+    *out = (size_t)g->d.na * n_cells_view(g) * sizeof(float);
+    return CT_OK;
+}
+
+extern "C" int ct_fbp(const ct_geom* g, const float* y, float* x, void* scratch, void* stream) {
+    if (!g || !y || !x || !scratch) return fail(CT_EINVAL, "ct_fbp: null argument");
+    if (int e = check_fbp(g)) return e;
+    DeviceGuard guard(g->d.device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const DevGeom& dg = g->dg;
+    float* q = (float*)scratch;
+    const size_t smem = sizeof(float) * 2 * dg.ns;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fbp_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fbp_filter_kernel<<<dim3(dg.na, dg.nt), 256, smem, st>>>(dg, y, q);
+    fbp_back_kernel<<<nblk(n_vox(g)), 256, 0, st>>>(dg, q, x, dg.na);
+    CT_LAUNCHED(2);
+    return CT_OK;
 }
 
 extern "C" int ct_sqs_denom_scratch_bytes(const ct_geom* g, size_t* out) {

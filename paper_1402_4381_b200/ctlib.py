@@ -27,7 +27,7 @@ STATUS = {0: "CT_OK", 1: "CT_EINVAL", 2: "CT_EUNSUPPORTED", 3: "CT_ENOMEM", 4: "
 # Symbols declared in include/ct_oslalm.h (checked by tests/test_abi.py)
 EXPORTS = ("ct_geom_create", "ct_geom_destroy", "ct_last_error", "ct_fwd_proj", "ct_back_proj",
            "ct_sqs_denom_scratch_bytes", "ct_sqs_denom", "ct_reg_grad", "ct_count_vv", "ct_oslalm_state_bytes",
-           "ct_oslalm_state_create", "ct_oslalm_state_destroy", "ct_oslalm_state_get", "ct_oslalm_state_reset",
+           "ct_oslalm_state_create", "ct_fbp", "ct_fbp_scratch_bytes", "ct_oslalm_state_destroy", "ct_oslalm_state_get", "ct_oslalm_state_reset",
            "ct_oslalm_set_timing", "ct_oslalm_get_timing", "ct_oslalm_iter",
            "ct_oslalm_run", "ct_comm_init", "ct_comm_get_unique_id", "ct_build_info", "ct_kernel_launches")
 
@@ -102,6 +102,8 @@ def load():
     L.ct_oslalm_state_create.argtypes = [vp, P(ct_oslalm_cfg), vp, sz, P(vp)]
     L.ct_oslalm_state_destroy.argtypes = [vp]; L.ct_oslalm_state_destroy.restype = None
     L.ct_oslalm_state_get.argtypes = [vp, P(ct_oslalm_state_view)]
+    L.ct_fbp_scratch_bytes.argtypes = [vp, P(ctypes.c_size_t)]
+    L.ct_fbp.argtypes = [vp, vp, vp, vp, vp]
     L.ct_oslalm_state_reset.argtypes = [vp]
     L.ct_oslalm_set_timing.argtypes = [vp, i]
     L.ct_oslalm_get_timing.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_longlong)]
@@ -162,6 +164,17 @@ def ct_geom_destroy(h):
 def ct_fwd_proj(h, views, x, y, stream=None):
     _check(load().ct_fwd_proj(h, ct_views(*views), _ptr(x, torch.float32, "x"), _ptr(y, torch.float32, "y"),
                               _stream(stream)))
+
+
+def ct_fbp_scratch_bytes(h):
+    n = ctypes.c_size_t()
+    _check(load().ct_fbp_scratch_bytes(h, ctypes.byref(n)))
+    return n.value
+
+
+def ct_fbp(h, y, x, scratch, stream=None):
+    _check(load().ct_fbp(h, _ptr(y, torch.float32, "y"), _ptr(x, torch.float32, "x"),
+                         ctypes.c_void_p(scratch.data_ptr()), _stream(stream)))
 
 
 def ct_back_proj(h, views, y, x, accumulate=False, stream=None):
@@ -266,6 +279,17 @@ class Geometry:
         scratch = torch.empty(ct_sqs_denom_scratch_bytes(self.h), dtype=torch.uint8, device=self.device)
         ct_sqs_denom(self.h, w, mask, dl, scratch)
         return dl, mask
+
+    def fbp(self, y, stream=None):
+        """FBP / FDK initial image (NEXT-4) of the ABI-layout sinogram y [na][ns][nt]."""
+        L = load()
+        n = ctypes.c_size_t()
+        _check(L.ct_fbp_scratch_bytes(self.h, ctypes.byref(n)))
+        scratch = torch.empty(n.value, dtype=torch.uint8, device=self.device)
+        x = torch.empty(self.img_shape, dtype=torch.float32, device=self.device)
+        _check(L.ct_fbp(self.h, _ptr(y, torch.float32, "y"), _ptr(x, torch.float32, "x"),
+                        ctypes.c_void_p(scratch.data_ptr()), _stream(stream)))
+        return x
 
     def reg_grad(self, x, mask, beta, delta, nbr, want_curv=True):
         grad = torch.empty_like(x)

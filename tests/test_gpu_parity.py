@@ -449,3 +449,53 @@ def test_oslalm_bb_c1(ct, O, M, n_iter, comm):
     MARGINS.append({"case": f"OS-LALM+BB c1 M={M} iters={n_iter} comm={comm}", "rms_HU": rms,
                     "alpha_max_rel": float(np.abs(a_gpu / ao - 1).max())})
     assert rms <= 0.5, rms
+
+
+# --------------------------------------------------------------------------- FBP (NEXT-4)
+
+@pytest.mark.parametrize("name", ["fan_c1", "fan_c2", "fan_offsets", "axial_c3", "axial_offsets"])
+def test_fbp_small(ct, O, name):
+    """GPU FBP / FDK (ct_fbp) vs the fp64 oracle on random sinograms: relative L2 <= 1e-4."""
+    g = geoms_small()[name]
+    geo = ct.Geometry(g)
+    rng = np.random.default_rng(5)
+    y = rng.random(geo.sino_shape(g["na"])).astype(np.float32)
+    xg = geo.fbp(torch.from_numpy(y).cuda()).cpu().numpy()
+    xo = O.fbp(g, I.to_oracle_sino(y))
+    assert rel_l2(I.to_oracle_image(xg), xo, f"fbp {name}") <= 1e-4
+
+
+def test_fbp_full_size_c2_and_helical_rejected(ct, O):
+    """c2 FBP of the synthetic scan vs the oracle (rel L2 <= 1e-4); helical -> CT_EUNSUPPORTED."""
+    cfg = I.config("c2")
+    d = I.synthesize(cfg)
+    geo = ct.Geometry(cfg.geom)
+    xg = geo.fbp(d["y"].cuda()).cpu().numpy()
+    xo = O.fbp(cfg.geom, I.to_oracle_sino(d["y"]))
+    assert rel_l2(I.to_oracle_image(xg), xo, "fbp full-size c2") <= 1e-4
+    gh = geoms_small()["helical_c4"]
+    with pytest.raises(ct.CTError, match="EUNSUPPORTED|helical"):
+        ct.Geometry(gh).fbp(torch.zeros(ct.Geometry(gh).sino_shape(gh["na"]), device="cuda"))
+
+
+def test_oslalm_from_fbp_init(ct, O):
+    """OS-LALM started from the FBP image matches the oracle started from its own FBP."""
+    cfg = I.config("c1")
+    g = cfg.geom
+    d = I.synthesize(cfg)
+    geo = ct.Geometry(g)
+    m0 = I.support_mask(cfg)
+    dl, S = geo.sqs_denom(d["w"].cuda(), m0.cuda())
+    x = geo.fbp(d["y"].cuda())
+    sol = ct.OSLALM(geo, cfg.M, beta=cfg.beta, delta=cfg.delta, nbr=8)
+    sol.set_data(d["y"].cuda(), d["w"].cuda(), dl, S)
+    log = np.array(sol.run(x, 8, log=True))
+    dlo, So = O.sqs_denom(g, I.to_oracle_sino(d["w"]), I.to_oracle_image(m0).astype(np.uint8))
+    x0 = O.fbp(g, I.to_oracle_sino(d["y"]))
+    xo, logo, _, _ = O.oslalm_run(g, I.to_oracle_sino(d["y"]), I.to_oracle_sino(d["w"]), dlo, So, x0,
+                                  M=cfg.M, beta=cfg.beta, delta=cfg.delta, nbr=8, n_iter=8)
+    xg = I.to_oracle_image(x.cpu().numpy())
+    rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
+    MARGINS.append({"case": "OS-LALM c1 from FBP x0, 8 iters", "rms_HU": rms})
+    assert rms <= 0.5, rms
+    assert np.array_equal(log[:, 2], logo[:, 2])
