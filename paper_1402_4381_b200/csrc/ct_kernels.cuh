@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 const int r_lo = min(max(__float2int_rd(fmaf(zq, f.ax.inv_kz, ub)), 0), nt - 1) & (even ? ~1 : ~0);
                 const int r_hi = min(max(__float2int_rd(fmaf(zq + (float)nzs, f.ax.inv_kz, ub)), 0), nt - 1);
                 const int nr = r_hi - r_lo + 1;
-                const float* yv = y + ((size_t)(vb + j) * ns + f.cA) * nt + r_lo;
+                const float* yv = y + (((vb + j) * ns + f.cA) * nt + r_lo);   // < 2^31 (validated at create)
                 // (1) filtered rows Q(r) = sum_c lphi F_s(c) y[c][r] and prefix sums
                 //     PF[k] = sum_{r < r_lo + k} Q(r): lane = two rows (float2), pair sum + warp scan
                 float carry = 0.0f;
@@ -729,18 +729,17 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 __syncwarp();
                 // (2) active slices (lanes = slices): integral of the row-wise constant Q over
                 //     the slice's extent on the detector, PF(u(iz + 1)) - PF(u(iz))
+                //     Lanes evaluate PF at consecutive slice edges; slice iz takes its upper edge
+                //     from the next lane, so a pass of 32 edges completes 31 slices.
                 const float fnr = (float)nr, ubl = ub - (float)r_lo;
-                for (int s0 = 0; s0 < nzs; s0 += 32) {
-                    if (s0 + lane < nzs) {
-                        const int iz = za + s0 + lane;
-                        const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
-                        const float u0 = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubl), 0.0f), fnr);
-                        const float u1 = fminf(fmaxf(fmaf(zi + 1.0f, f.ax.inv_kz, ubl), 0.0f), fnr);
-                        const int k0 = min(__float2int_rd(u0), nr - 1), k1 = min(__float2int_rd(u1), nr - 1);
-                        const float lo = fmaf(u0 - (float)k0, Q[k0], PF[k0]);
-                        const float hi = fmaf(u1 - (float)k1, Q[k1], PF[k1]);
-                        acc[iz] = fmaf(ltheta(f.ax, iz), hi - lo, acc[iz]);
-                    }
+                for (int s0 = 0; s0 < nzs; s0 += 31) {
+                    const int iz = za + s0 + lane;   // lower edge of slice iz (lane 31: upper edge of iz - 1)
+                    const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
+                    const float u = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubl), 0.0f), fnr);
+                    const int k = min(__float2int_rd(u), nr - 1);
+                    const float pf = fmaf(u - (float)k, Q[k], PF[k]);
+                    const float up = __shfl_down_sync(0xffffffffu, pf, 1);
+                    if (lane < 31 && s0 + lane < nzs) acc[iz] = fmaf(ltheta(f.ax, iz), up - pf, acc[iz]);
                 }
                 __syncwarp();
             }
