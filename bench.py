@@ -292,7 +292,9 @@ def main():
     Ui = geo.counts(mask, subset_views(g["na"], cfg.M, 0))[0]
     work = 2 * U0 + 2 * Ui + n_iter * 2 * U
 
-    # ---- warm-up (also captures the CUDA graph)
+    # ---- warm-up (also captures the CUDA graph); the clock sampler starts here so that it is
+    # sampling (nvidia-smi needs ~0.3 s to start) when the timed region begins
+    clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         step()
     barrier(ws)
@@ -303,7 +305,8 @@ def main():
     mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     l0 = ctlib.ct_kernel_launches()
-    with ClockSampler(local) as clk:
+    try:
+        # samples cover the warm-up steps and the timed region (same load)
         barrier(ws)
         for i in range(args.steps):
             flush.zero_()
@@ -311,6 +314,8 @@ def main():
             step(mids[i])
             ends[i].record(st)
         barrier(ws)
+    finally:
+        clk.__exit__(None, None, None)
     launches = ctlib.ct_kernel_launches() - l0
     T = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / 1e3
     Ti = sum(m.elapsed_time(e) for m, e in zip(mids, ends)) / 1e3
@@ -350,6 +355,14 @@ def main():
                  "traffic": traffic.get("sqs_update", {}).get("bytes_per_launch"), "bytes_per_launch": upd_bytes,
                  "ms_per_launch": upd_ms}
     kernel_ms = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / total_kt} for k, v in kt.items() if v[1]}
+    # BASELINE.json's "HBM/L2 gather roofline": every nonzero's operand fetched
+    # through L2 once, T = max(T_HBM, 4 B nnz / BW_L2), BW_L2 = L2-resident read bandwidth
+    # measured here (no vendor number available)
+    l2 = ctlib.ct_peak_l2_read(local)
+    gather_bytes = 4.0 * nnz / M / ws
+    roofline_gather = {"bound": "l2-gather", "kernel": dom, "achieved": gather_bytes / (ms_launch / 1e3) / 1e9,
+                       "peak": l2, "unit": "GB/s", "frac": gather_bytes / (ms_launch / 1e3) / 1e9 / l2,
+                       "bytes_per_launch": gather_bytes, "peak_src": "measured in this run: ct_peak_l2_read (48 MiB buffer streamed 200x, float4 loads)"}
 
     # ---- end to end: host (pinned) inputs in, image out, inside the timed region
     e2e = None
@@ -399,6 +412,7 @@ def main():
                        "parallelism": (f"views of each subset split over {ws} GPU(s); NCCL reduce-scatter of G+ "
                                        "into row slabs, slab update, all-gather of x+" if ws > 1 else "1 GPU")},
             "gpu_launches": int(launches), "roofline": roofline, "roofline_streaming": streaming,
+            "roofline_gather": roofline_gather,
             "kernel_ms": kernel_ms, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
             "peaks": {"fp32_tflops": pk["fp32_tflops"], "hbm_gbs": pk["hbm_gbs"], "src": pk["src"]},
         }

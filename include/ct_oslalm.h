@@ -165,6 +165,10 @@ int ct_count_vv(const ct_geom* g, ct_views v, const uint8_t* mask, void* scratch
  * not one full turn).  The image is not clipped to x >= 0 (OS-LALM's first update does).
  */
 int ct_fbp_scratch_bytes(const ct_geom* g, size_t* out);
+/* Diagnostic (no ct_geom): L2-resident read bandwidth of `device` in GB/s, measured by
+ * streaming a `bytes`-sized buffer `reps` times (allocates and frees its own buffer).
+ * The denominator of the gather roofline that bench.py reports. */
+int ct_peak_l2_read(int device, size_t bytes, int reps, double* gbs);
 int ct_fbp(const ct_geom* g, const float* y, float* x, void* scratch, void* stream);
 
 /* ------------------------------------------------------------------------ */

@@ -392,6 +392,55 @@ extern "C" int ct_back_proj(const ct_geom* g, ct_views v, const float* y, float*
     return launch_back<EPI_STORE>(g, v, y, x, ga, (cudaStream_t)stream);
 }
 
+// ---------------------------------------------------------------------------
+// Diagnostic: L2-resident read bandwidth (the "HBM/L2 gather roofline" denominator of
+// SURVEY §8(d); no vendor L2 number is available).  Every thread streams the buffer
+// `reps` times with float4 loads (grid-stride), so after the first pass it is L2-resident.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) l2_read_kernel(const float4* __restrict__ a, size_t n4, int reps, float* out) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (int r = 0; r < reps; r++)
+        for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+            const float4 v = __ldcg(&a[i]);
+            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+        }
+    if (s.x + s.y + s.z + s.w == 123.456f) out[0] = s.x;   // keeps the loads alive
+}
+
+extern "C" int ct_peak_l2_read(int device, size_t bytes, int reps, double* gbs) {
+    if (!gbs || bytes < 1024 || reps < 1) return fail(CT_EINVAL, "ct_peak_l2_read: bad arguments");
+    DeviceGuard guard(device);
+    float4* a = nullptr;
+    float* out = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaError_t e = cudaMalloc(&a, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&out, sizeof(float));
+    if (e == cudaSuccess) e = cudaMemset(a, 0, bytes);
+    if (e == cudaSuccess) e = cudaEventCreate(&e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&e1);
+    float ms = 0.0f;
+    if (e == cudaSuccess) {
+        const size_t n4 = bytes / 16;
+        const unsigned grid = (unsigned)(sms * 8);
+        l2_read_kernel<<<grid, 256>>>(a, n4, 2, out);   // warm: pulls the buffer into L2
+        cudaEventRecord(e0);
+        l2_read_kernel<<<grid, 256>>>(a, n4, reps, out);
+        cudaEventRecord(e1);
+        e = cudaEventSynchronize(e1);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    }
+    cudaFree(a);
+    cudaFree(out);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (e != cudaSuccess) return fail(CT_ECUDA, "ct_peak_l2_read: %s", cudaGetErrorString(e));
+    *gbs = (double)bytes * reps / (ms / 1e3) / 1e9;
+    return CT_OK;
+}
+
 // FBP / FDK initial image (NEXT-4; reading B-FBP)
 static int check_fbp(const ct_geom* g) {
     if (g->d.kind == CT_CONE_HELICAL) return fail(CT_EUNSUPPORTED, "ct_fbp: helical scans are not supported");

@@ -27,7 +27,7 @@ STATUS = {0: "CT_OK", 1: "CT_EINVAL", 2: "CT_EUNSUPPORTED", 3: "CT_ENOMEM", 4: "
 # Symbols declared in include/ct_oslalm.h (checked by tests/test_abi.py)
 EXPORTS = ("ct_geom_create", "ct_geom_destroy", "ct_last_error", "ct_fwd_proj", "ct_back_proj",
            "ct_sqs_denom_scratch_bytes", "ct_sqs_denom", "ct_reg_grad", "ct_count_vv", "ct_oslalm_state_bytes",
-           "ct_oslalm_state_create", "ct_fbp", "ct_fbp_scratch_bytes", "ct_oslalm_state_destroy", "ct_oslalm_state_get", "ct_oslalm_state_reset",
+           "ct_oslalm_state_create", "ct_fbp", "ct_fbp_scratch_bytes", "ct_peak_l2_read", "ct_oslalm_state_destroy", "ct_oslalm_state_get", "ct_oslalm_state_reset",
            "ct_oslalm_set_timing", "ct_oslalm_get_timing", "ct_oslalm_iter",
            "ct_oslalm_run", "ct_comm_init", "ct_comm_get_unique_id", "ct_build_info", "ct_kernel_launches")
 
@@ -104,6 +104,7 @@ def load():
     L.ct_oslalm_state_get.argtypes = [vp, P(ct_oslalm_state_view)]
     L.ct_fbp_scratch_bytes.argtypes = [vp, P(ctypes.c_size_t)]
     L.ct_fbp.argtypes = [vp, vp, vp, vp, vp]
+    L.ct_peak_l2_read.argtypes = [i, ctypes.c_size_t, i, P(ctypes.c_double)]
     L.ct_oslalm_state_reset.argtypes = [vp]
     L.ct_oslalm_set_timing.argtypes = [vp, i]
     L.ct_oslalm_get_timing.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_longlong)]
@@ -164,6 +165,13 @@ def ct_geom_destroy(h):
 def ct_fwd_proj(h, views, x, y, stream=None):
     _check(load().ct_fwd_proj(h, ct_views(*views), _ptr(x, torch.float32, "x"), _ptr(y, torch.float32, "y"),
                               _stream(stream)))
+
+
+def ct_peak_l2_read(device=0, mib=48, reps=200):
+    """L2-resident read bandwidth (GB/s) of the device (diagnostic)."""
+    v = ctypes.c_double()
+    _check(load().ct_peak_l2_read(int(device), int(mib) * 1024 * 1024, int(reps), ctypes.byref(v)))
+    return v.value
 
 
 def ct_fbp_scratch_bytes(h):
