@@ -21,6 +21,10 @@
 
 using namespace ct;
 
+#ifndef CT_FWD3D_TC
+#define CT_FWD3D_TC 24   // channels per 3D forward CTA (A/B: 24 beats 16 and 32 by ~10 %)
+#endif
+
 // ---------------------------------------------------------------------------
 // errors
 // ---------------------------------------------------------------------------
@@ -311,7 +315,7 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         const int next = dg.nx + dg.ny;
         fwd3d_extent_init<<<(next + 255) / 256, 256, 0, st>>>(g->ext3d, next);
         fwd3d_extent_kernel<<<(dg.nx * dg.ny + 7) / 8, 256, 0, st>>>(dg, x, g->ext3d);
-        constexpr int TC = 16;
+        constexpr int TC = CT_FWD3D_TC;
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32)
             launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);

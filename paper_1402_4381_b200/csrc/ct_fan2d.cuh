@@ -231,7 +231,9 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
                 for (int j = 0; j < kMaxFoot; j++) {
                     if (j >= nmax) break;
                     // bins j >= n add exactly 0 (Fn = Fp = mass) to distinct addresses
-                    const float Fn = (j + 1 < n) ? T.F(__fadd_rn(T.u0, koff + (float)(j + 1))) : T.mass;
+                    // the warp's last round needs no CDF (every lane is at or past its right edge)
+                    float Fn = T.mass;
+                    if (j + 1 < nmax) Fn = (j + 1 < n) ? T.F(__fadd_rn(T.u0, koff + (float)(j + 1))) : T.mass;
                     if (act) bp[j] += lx * __fsub_rn(Fn, Fp);
                     Fp = Fn;
                     __syncwarp();   // round j's stores are visible to round j + 1's loads
