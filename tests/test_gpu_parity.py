@@ -499,3 +499,48 @@ def test_oslalm_from_fbp_init(ct, O):
     MARGINS.append({"case": "OS-LALM c1 from FBP x0, 8 iters", "rms_HU": rms})
     assert rms <= 0.5, rms
     assert np.array_equal(log[:, 2], logo[:, 2])
+
+
+# --------------------------------------------------------------------------- edge cases
+
+def test_axis_aligned_and_diagonal_views(ct, O):
+    """Views at multiples of 45 degrees: pixel edges parallel to the centre ray (zero rise or
+    fall width, degenerate trapezoids) and diagonal views (zero flat part); 2D and 3D."""
+    for g in (GU.geom("fan2d", nx=20, dx=4.0, ns=40, ds=8.1912, na=8),
+              GU.geom("cone_axial", nx=12, nz=6, dx=0.9766, dz=0.625, ns=24, ds=1.0239, nt=8, dt=1.0964, na=8)):
+        geo = ct.Geometry(g)
+        x = rand_image(g, 3, geo.img_shape)
+        yg = geo.fwd(torch.from_numpy(x).cuda(), (0, 1, g["na"])).cpu().numpy()
+        yo = O.fwd(g, I.to_oracle_image(x), 0, 1, g["na"])
+        assert np.isfinite(yg).all()
+        assert rel_l2(I.to_oracle_sino(yg), yo, f"fwd 45deg {g['kind']}") <= 1e-4
+        p = np.random.default_rng(4).random(geo.sino_shape(g["na"])).astype(np.float32)
+        bg = geo.back(torch.from_numpy(p).cuda()).cpu().numpy()
+        bo = O.back(g, I.to_oracle_sino(p), 0, 1, g["na"])
+        assert rel_l2(I.to_oracle_image(bg), bo, f"back 45deg {g['kind']}") <= 1e-4
+
+
+def test_empty_forward_and_one_view_subsets(ct, O):
+    """count = 0 forward projection is a no-op; M = na (one view per subset) OS-LALM matches
+    the oracle."""
+    g = geoms_small()["fan_c1"]
+    geo = ct.Geometry(g)
+    y = torch.full(geo.sino_shape(1), 7.0, device="cuda")
+    ct.ct_fwd_proj(geo.h, (0, 1, 0), torch.zeros(geo.img_shape, device="cuda"), y)
+    assert (y == 7.0).all()
+    ell = [(0.0, 0.0, 0.0, 30.0, 25.0, float("inf"), 0.2, 0.02)]
+    d = I.noisy_data(g, ell, 1e5, 0.0, 9)
+    m0 = torch.ones(geo.img_shape, dtype=torch.uint8)
+    dl, S = geo.sqs_denom(d["w"].cuda(), m0.cuda())
+    M = g["na"]
+    sol = ct.OSLALM(geo, M, beta=2.0 ** 8, delta=2e-4, nbr=8)
+    sol.set_data(d["y"].cuda(), d["w"].cuda(), dl, S)
+    x = torch.zeros(geo.img_shape, device="cuda")
+    log = np.array(sol.run(x, 2, log=True))
+    dlo, So = O.sqs_denom(g, I.to_oracle_sino(d["w"]), I.to_oracle_image(m0).astype(np.uint8))
+    xo, logo, _, _ = O.oslalm_run(g, I.to_oracle_sino(d["y"]), I.to_oracle_sino(d["w"]), dlo, So,
+                                  np.zeros(O.img_shape(g)), M=M, beta=2.0 ** 8, delta=2e-4, nbr=8, n_iter=2)
+    xg = I.to_oracle_image(x.cpu().numpy())
+    rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
+    assert rms <= 0.5, rms
+    assert np.array_equal(log[:, 2], logo[:, 2])
