@@ -678,35 +678,15 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 load_foot(&tab[j], f);
                 if (f.n <= 0) continue;
                 const int za = f.rows & 0xffff, nzs = f.rows >> 16;
-                // rows met by the active slices, from an even row (float2 loads)
-                const float zq = (float)(za - f.ax.qi) - f.ax.qf;
-                // two rows per lane (float2) for tall detectors; float2 rows need an even row pitch
-                const bool even = (nt & 1) == 0 && nt > 32;
-                const int r_lo = min(max(__float2int_rd(fmaf(zq, f.ax.inv_kz, ub)), 0), nt - 1) & (even ? ~1 : ~0);
-                const int r_hi = min(max(__float2int_rd(fmaf(zq + (float)nzs, f.ax.inv_kz, ub)), 0), nt - 1);
-                const int nr = r_hi - r_lo + 1;
-                const float* yv = y + (((vb + j) * ns + f.cA) * nt + r_lo);   // < 2^31 (validated at create)
-                // (1) filtered rows Q(r) = sum_c lphi F_s(c) y[c][r] and prefix sums
-                //     PF[k] = sum_{r < r_lo + k} Q(r): lane = two rows (float2), pair sum + warp scan
-                float carry = 0.0f;
-                const int RPL = even ? 2 : 1;
-                for (int p0 = 0; p0 < nr; p0 += 32 * RPL) {
-                    const int p = p0 + RPL * lane;
-                    const bool inr = p < nr;
+                int r_lo = 0, nr = nt;
+                if (nt == 64) {
+                    // the common 64-row detector: one pass over every row, two rows per lane
+                    // (the rows the active slices miss are cheap to include)
+                    const float2* yr = reinterpret_cast<const float2*>(y + ((vb + j) * ns + f.cA) * 64) + lane;
                     float q0 = 0.0f, q1 = 0.0f;
-                    if (even) {
-                        const float2* yr = reinterpret_cast<const float2*>(yv + (inr ? p : 0));
-                        // warp-uniform channel count: issue all loads, then the FMAs
-                        if (f.n <= 3) filt_rows2<3>(yr, nt >> 1, inr, f, q0, q1);
-                        else if (f.n <= 4) filt_rows2<4>(yr, nt >> 1, inr, f, q0, q1);
-                        else filt_rows2<kMaxFoot>(yr, nt >> 1, inr, f, q0, q1);
-                        if (p + 1 >= nr) q1 = 0.0f;   // row past r_hi (odd count)
-                    } else {
-                        const float* yr = yv + (inr ? p : 0);
-                        if (f.n <= 3) filt_rows1<3>(yr, nt, inr, f, q0);
-                        else if (f.n <= 4) filt_rows1<4>(yr, nt, inr, f, q0);
-                        else filt_rows1<kMaxFoot>(yr, nt, inr, f, q0);
-                    }
+                    if (f.n <= 3) filt_rows2<3>(yr, 32, true, f, q0, q1);
+                    else if (f.n <= 4) filt_rows2<4>(yr, 32, true, f, q0, q1);
+                    else filt_rows2<kMaxFoot>(yr, 32, true, f, q0, q1);
                     const float s2 = q0 + q1;
                     float inc = s2;
 #pragma unroll
@@ -714,17 +694,78 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                         const float t = __shfl_up_sync(0xffffffffu, inc, o);
                         if (lane >= o) inc += t;
                     }
-                    const float ex = carry + inc - s2;
-                    if (inr) {
-                        Q[p] = q0;
-                        PF[p] = ex;
-                        if (even) {
-                            Q[p + 1] = q1;
-                            PF[p + 1] = ex + q0;
-                        }
-                        if (p + RPL >= nr) PF[p + RPL] = ex + s2;   // upper edge of the last row
+                    const float ex = inc - s2;
+                    Q[2 * lane] = q0;
+                    Q[2 * lane + 1] = q1;
+                    PF[2 * lane] = ex;
+                    PF[2 * lane + 1] = ex + q0;
+                    if (lane == 31) PF[64] = inc;
+                } else if (nt == 32) {
+                    // 32-row detector: one pass over every row, one row per lane
+                    const float* yr = y + ((vb + j) * ns + f.cA) * 32 + lane;
+                    float q0 = 0.0f;
+                    if (f.n <= 3) filt_rows1<3>(yr, 32, true, f, q0);
+                    else if (f.n <= 4) filt_rows1<4>(yr, 32, true, f, q0);
+                    else filt_rows1<kMaxFoot>(yr, 32, true, f, q0);
+                    float inc = q0;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const float t = __shfl_up_sync(0xffffffffu, inc, o);
+                        if (lane >= o) inc += t;
                     }
-                    carry += __shfl_sync(0xffffffffu, inc, 31);
+                    Q[lane] = q0;
+                    PF[lane] = inc - q0;
+                    if (lane == 31) PF[32] = inc;
+                } else {
+                    // rows met by the active slices, from an even row (float2 loads)
+                    const float zq = (float)(za - f.ax.qi) - f.ax.qf;
+                    // two rows per lane (float2) for tall detectors; float2 rows need an even row pitch
+                    const bool even = (nt & 1) == 0 && nt > 32;
+                    r_lo = min(max(__float2int_rd(fmaf(zq, f.ax.inv_kz, ub)), 0), nt - 1) & (even ? ~1 : ~0);
+                    const int r_hi = min(max(__float2int_rd(fmaf(zq + (float)nzs, f.ax.inv_kz, ub)), 0), nt - 1);
+                    nr = r_hi - r_lo + 1;
+                    const float* yv = y + (((vb + j) * ns + f.cA) * nt + r_lo);   // < 2^31 (validated at create)
+                    // (1) filtered rows Q(r) = sum_c lphi F_s(c) y[c][r] and prefix sums
+                    //     PF[k] = sum_{r < r_lo + k} Q(r): lane = two rows (float2), pair sum + warp scan
+                    float carry = 0.0f;
+                    const int RPL = even ? 2 : 1;
+                    for (int p0 = 0; p0 < nr; p0 += 32 * RPL) {
+                        const int p = p0 + RPL * lane;
+                        const bool inr = p < nr;
+                        float q0 = 0.0f, q1 = 0.0f;
+                        if (even) {
+                            const float2* yr = reinterpret_cast<const float2*>(yv + (inr ? p : 0));
+                            // warp-uniform channel count: issue all loads, then the FMAs
+                            if (f.n <= 3) filt_rows2<3>(yr, nt >> 1, inr, f, q0, q1);
+                            else if (f.n <= 4) filt_rows2<4>(yr, nt >> 1, inr, f, q0, q1);
+                            else filt_rows2<kMaxFoot>(yr, nt >> 1, inr, f, q0, q1);
+                            if (p + 1 >= nr) q1 = 0.0f;   // row past r_hi (odd count)
+                        } else {
+                            const float* yr = yv + (inr ? p : 0);
+                            if (f.n <= 3) filt_rows1<3>(yr, nt, inr, f, q0);
+                            else if (f.n <= 4) filt_rows1<4>(yr, nt, inr, f, q0);
+                            else filt_rows1<kMaxFoot>(yr, nt, inr, f, q0);
+                        }
+                        const float s2 = q0 + q1;
+                        float inc = s2;
+    #pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const float t = __shfl_up_sync(0xffffffffu, inc, o);
+                            if (lane >= o) inc += t;
+                        }
+                        const float ex = carry + inc - s2;
+                        if (inr) {
+                            Q[p] = q0;
+                            PF[p] = ex;
+                            if (even) {
+                                Q[p + 1] = q1;
+                                PF[p + 1] = ex + q0;
+                            }
+                            if (p + RPL >= nr) PF[p + RPL] = ex + s2;   // upper edge of the last row
+                        }
+                        carry += __shfl_sync(0xffffffffu, inc, 31);
+                    }
+
                 }
                 __syncwarp();
                 // (2) active slices (lanes = slices): integral of the row-wise constant Q over
