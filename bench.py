@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--inner", default="sqs", choices=("sqs", "fista"), help="inner solver (NEXT-1: fista)")
     ap.add_argument("--n-inner", type=int, default=1, help="inner FISTA iterations (with --inner fista)")
     ap.add_argument("--bb", action="store_true", help="Barzilai-Borwein scaling of the SQS Hessian (NEXT-2)")
+    ap.add_argument("--zslab", action="store_true",
+                    help="cone beam: z-slab decomposition over the ranks, partial sinograms summed (NEXT-3)")
     ap.add_argument("--init", default="zero", choices=("zero", "fbp"),
                     help="initial image: zero on S (G10) or the FBP/FDK image (NEXT-4, P:586; inside the timed step)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -252,12 +254,19 @@ def main():
     y, w = data["y"].contiguous(), data["w"].contiguous()
     del data
     m0 = I.support_mask(cfg, device=dev)
+    g_full = g
+    if args.zslab:   # NEXT-3: this rank's z-slab of the volume (its own geometry)
+        from paper_1402_4381_b200.host import rank_zslab
+        z0, z1 = rank_zslab(g["nz"], rank, ws)
+        g = I.slab_geom(g, z0, z1)
+        m0 = m0[..., z0:z1].contiguous()
     geo = ctlib.Geometry(g, local)
-    if ws > 1:
+    if ws > 1 or args.zslab:
         import torch.distributed as dist
         uid = [ctlib.ct_comm_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        geo.comm_init(rank, ws, uid[0])
+        if ws > 1:
+            dist.broadcast_object_list(uid, src=0)
+        geo.comm_init(rank, ws, uid[0], zslab=args.zslab)
     mask = m0.clone()
     dl = torch.empty(geo.img_shape, dtype=torch.float32, device=dev)
     scratch = torch.empty(ctlib.ct_sqs_denom_scratch_bytes(geo.h), dtype=torch.uint8, device=dev)
@@ -291,6 +300,12 @@ def main():
     # the first subset of the bit-reversal order is subset 0 (initial G, reading G10)
     Ui = geo.counts(mask, subset_views(g["na"], cfg.M, 0))[0]
     work = 2 * U0 + 2 * Ui + n_iter * 2 * U
+    local_counts = (nnz, U, C)          # this rank's kernels' work (a slab's voxels with --zslab)
+    if args.zslab and ws > 1:           # the slabs partition the voxels: the job's work is their sum
+        import torch.distributed as dist
+        t = torch.tensor([work, U, nnz], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        work, U, nnz = (int(v) for v in t.tolist())
 
     # ---- warm-up (also captures the CUDA graph); the clock sampler starts here so that it is
     # sampling (nvidia-smi needs ~0.3 s to start) when the timed region begins
@@ -335,14 +350,16 @@ def main():
     pk = peaks()
     M = cfg.M
     # algorithmic FLOPs per projection launch: 2 nnz + 15 U + 150 C, per subset = full / M
-    flop_launch = (2 * nnz + 15 * U + 150 * C) / M / ws
+    lnnz, lU, lC = local_counts
+    flop_launch = (2 * lnnz + 15 * lU + 150 * lC) / M / (1 if args.zslab else ws)
     dom = max(("fwd_resid", "back_gupd"), key=lambda k: kt[k][0])
     ms_launch = kt[dom][0] / max(kt[dom][1], 1)
     achieved = flop_launch / (ms_launch / 1e3) / 1e12
     total_kt = sum(v[0] for v in kt.values())
     N = int(np.prod(geo.img_shape))
     upd_ms = kt["sqs_update"][0] / max(kt["sqs_update"][1], 1)
-    upd_bytes = 21 * N        # x, G, g, D_L read (16 B) + mask (1 B) + x' write (4 B) per voxel
+    # x, G, g, D_L read (16 B) + mask (1 B) + x' write (4 B) per updated voxel (row-slab ranks update N/P)
+    upd_bytes = 21 * N / (ws if (ws > 1 and not args.zslab and args.inner == "sqs") else 1)
     traffic = load_traffic(cfg.name)
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / pk["fp32_tflops"], "traffic": traffic.get(dom, {}).get("bytes_per_launch"),
@@ -359,7 +376,7 @@ def main():
     # through L2 once, T = max(T_HBM, 4 B nnz / BW_L2), BW_L2 = L2-resident read bandwidth
     # measured here (no vendor number available)
     l2 = ctlib.ct_peak_l2_read(local)
-    gather_bytes = 4.0 * nnz / M / ws
+    gather_bytes = 4.0 * lnnz / M / (1 if args.zslab else ws)
     roofline_gather = {"bound": "l2-gather", "kernel": dom, "achieved": gather_bytes / (ms_launch / 1e3) / 1e9,
                        "peak": l2, "unit": "GB/s", "frac": gather_bytes / (ms_launch / 1e3) / 1e9 / l2,
                        "bytes_per_launch": gather_bytes, "peak_src": "measured in this run: ct_peak_l2_read (48 MiB buffer streamed 200x, float4 loads)"}
@@ -409,7 +426,9 @@ def main():
                        "views_per_subset": (g["na"] + cfg.M - 1) // cfg.M, "U_full_scan": U,
                        "nnz_full_scan": nnz, "work_per_step": work,
                        "l2": "flushed between steps (512 MiB write, untimed)",
-                       "parallelism": (f"views of each subset split over {ws} GPU(s); NCCL reduce-scatter of G+ "
+                       "parallelism": (f"z-slabs over {ws} GPU(s): partial sinograms all-reduced, slab "
+                                       "back-projection and update, 1-slice halos" if args.zslab else
+                                       f"views of each subset split over {ws} GPU(s); NCCL reduce-scatter of G+ "
                                        "into row slabs, slab update, all-gather of x+" if ws > 1 else "1 GPU")},
             "gpu_launches": int(launches), "roofline": roofline, "roofline_streaming": streaming,
             "roofline_gather": roofline_gather,

@@ -288,6 +288,19 @@ int ct_oslalm_run(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_da
  * NCCL is loaded at run time (libnccl.so.2); CT_ENCCL if unavailable.
  */
 int ct_comm_init(ct_geom* g, int rank, int nranks, const void* nccl_uid);
+/*
+ * z-slab decomposition (NEXT-3; SURVEY §8(e) alternative, "sinogram-domain z-slabs"):
+ * each rank's geometry `g` is its z-slab of the volume (same scan, nz = the slab's slices,
+ * offz placing them; slabs in rank order along z).  A x is separable over voxels, so
+ * the ranks forward-project their slab for every view whose cone meets it and the partial
+ * sinograms are summed (ncclAllReduce of one subset's sinogram instead of an image); each
+ * rank back-projects the full residual onto its own slab (no image exchange), xi and the
+ * BB sums are all-reduced, and the 26-neighbour update takes the neighbours' boundary slices
+ * (ncclSend/ncclRecv of one slice each way).  Cone beam only; SQS inner step only
+ * (CT_EUNSUPPORTED otherwise).  Call before creating OS-LALM states; D_L likewise sums the
+ * slabs' A 1_S.  Same arguments and errors as ct_comm_init.
+ */
+int ct_comm_init_zslab(ct_geom* g, int rank, int nranks, const void* nccl_uid128);
 int ct_comm_get_unique_id(void* nccl_uid_out128);
 
 /* Library identification string (kernel names, target). */

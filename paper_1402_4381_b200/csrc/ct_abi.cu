@@ -69,6 +69,10 @@ struct NcclApi {
     ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                   cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -86,10 +90,15 @@ static bool load_nccl() {
     g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
     g_nccl.ReduceScatter = (decltype(g_nccl.ReduceScatter))dlsym(h, "ncclReduceScatter");
     g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+    g_nccl.Send = (decltype(g_nccl.Send))dlsym(h, "ncclSend");
+    g_nccl.Recv = (decltype(g_nccl.Recv))dlsym(h, "ncclRecv");
+    g_nccl.GroupStart = (decltype(g_nccl.GroupStart))dlsym(h, "ncclGroupStart");
+    g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
     g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
     g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter &&
-                g_nccl.AllGather && g_nccl.CommDestroy;
+                g_nccl.AllGather && g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd &&
+                g_nccl.CommDestroy;
     return g_nccl.ok;
 }
 
@@ -109,6 +118,7 @@ struct ct_geom {
     int2* ext3d = nullptr;                 // cone forward: nonzero column range per image row / column
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
+    int zslab = 0;   // NEXT-3: this geometry is rank `rank`'s z-slab of the volume (sinogram-domain sums)
 };
 
 static int allreduce(const ct_geom* g, float* buf, size_t n, cudaStream_t st) {
@@ -480,6 +490,10 @@ extern "C" int ct_sqs_denom_scratch_bytes(const ct_geom* g, size_t* out) {
     return CT_OK;
 }
 
+static void zslab_window(const ct_geom* g, ct_views v, int* k0, int* k1);
+static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* out, const float* y, const float* w,
+                           float scale, cudaStream_t st);
+
 extern "C" int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask, float* dl, void* scratch, void* stream) {
     if (!g || !w || !mask || !dl || !scratch) return fail(CT_EINVAL, "ct_sqs_denom: null argument");
     DeviceGuard guard(g->d.device);
@@ -492,12 +506,22 @@ extern "C" int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask, flo
     ct_views all{g->rank * base + std::min(g->rank, extra), 1, base + (g->rank < extra ? 1 : 0)};
     mask_to_float_kernel<<<nblk(N), 256, 0, st>>>(mask, one, N);
     CT_LAUNCHED(1);
-    if (int e = launch_fwd<true>(g, all, one, sino, nullptr, w, 1.0f, st)) return e;
     GupdArgs ga{};
     ga.mask = mask;   // D_L is only needed on S (set to 0 elsewhere below)
-    if (int e = launch_back<EPI_STORE>(g, all, sino, dl, ga, st)) return e;
-    if (g->comm)
-        if (int e = allreduce(g, dl, N, st)) return e;
+    if (g->zslab) {
+        // z-slab ranks: A 1_S summed over the slabs (every ray), weighted, back onto the slab
+        const ct_views va{0, 1, g->d.na};
+        if (int e = zslab_fwd_resid(g, va, one, sino, nullptr, w, 1.0f, st)) return e;
+        int k0, k1;
+        zslab_window(g, va, &k0, &k1);
+        if (int e = launch_back<EPI_STORE>(g, ct_views{k0, 1, k1 - k0}, sino + (size_t)k0 * n_cells_view(g), dl, ga, st))
+            return e;
+    } else {
+        if (int e = launch_fwd<true>(g, all, one, sino, nullptr, w, 1.0f, st)) return e;
+        if (int e = launch_back<EPI_STORE>(g, all, sino, dl, ga, st)) return e;
+        if (g->comm)
+            if (int e = allreduce(g, dl, N, st)) return e;
+    }
     mask_finalize_kernel<<<nblk(N), 256, 0, st>>>(mask, dl, N);
     CT_LAUNCHED(1);
     return CT_OK;
@@ -581,6 +605,11 @@ struct ct_oslalm_state {
     float* gbar = nullptr;               // BB: mean subset gradient of the current iteration
     float* gprev = nullptr;              // BB: ... of the previous iteration
     double* bb_part = nullptr;
+    // z-slab ranks (NEXT-3): packed boundary slices sent to / received from the neighbours
+    float* zsend[2] = {nullptr, nullptr};
+    float* zrecv[2] = {nullptr, nullptr};
+    uint8_t* zmask[2] = {nullptr, nullptr};
+    int zmask_ready = 0;
     double* xi_part;
     Scalars* sc;
     double* dlog;        // M x 3 doubles (per iteration)
@@ -659,6 +688,8 @@ static int check_cfg(const ct_geom* g, const ct_oslalm_cfg* c) {
         return fail(CT_EINVAL, "CT_INNER_SQS takes exactly one step (n_inner = %d); use CT_INNER_FISTA", c->n_inner);
     if (c->inner == CT_INNER_FISTA && (c->n_inner < 1 || c->n_inner > 64))
         return fail(CT_EINVAL, "n_inner = %d outside [1, 64]", c->n_inner);
+    if (g->zslab && c->inner == CT_INNER_FISTA)
+        return fail(CT_EUNSUPPORTED, "z-slab ranks support the SQS inner step only (FISTA passes need halos)");
     if (c->bb != 0 && c->bb != 1) return fail(CT_EINVAL, "bb must be 0 or 1");
     if (c->bb && !(c->alpha_min > 0 && c->alpha_min <= 1)) return fail(CT_EINVAL, "alpha_min must be in (0, 1]");
     return check_reg(g, &c->reg);
@@ -674,7 +705,7 @@ static void slab_geometry(const ct_geom* g, int P, int rank, int* iy0, int* iy1,
 
 static bool use_slabs(const ct_geom* g, const ct_oslalm_cfg* c) {
     // FISTA's n stencil passes would need a halo exchange per pass: it keeps the all-reduce path
-    return g->comm != nullptr && c->inner == CT_INNER_SQS;
+    return g->comm != nullptr && !g->zslab && c->inner == CT_INNER_SQS;
 }
 
 static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16], size_t* total) {
@@ -701,6 +732,8 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16
     off[10] = o; o += slab ? 2 * align256(N * 4) : 0;  // slab path: all-gathered full images (ping-pong)
     off[11] = o; o += align256(4 * 8);                 // xi / BB sums exchange
     off[12] = o; o += c->bb ? 3 * align256(N * 4) + align256(2 * 8 * nblk(N)) : 0;   // BB: x_prev, gbar, gbar_prev, partials
+    const size_t ncols = (size_t)g->d.nx * g->d.ny;
+    off[13] = o; o += g->zslab ? 4 * align256(ncols * 4) + 2 * align256(ncols) : 0;   // z-slab halos
     *total = o;
 }
 
@@ -753,6 +786,15 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
         s->xp[1] = (float*)(b + off[10] + align256(s->Npad * 4));
     }
     s->xi_ex = (double*)(b + off[11]);
+    if (g->zslab) {
+        const size_t ncols = (size_t)g->d.nx * g->d.ny, fb = align256(ncols * 4);
+        s->zsend[0] = (float*)(b + off[13]);
+        s->zsend[1] = (float*)(b + off[13] + fb);
+        s->zrecv[0] = (float*)(b + off[13] + 2 * fb);
+        s->zrecv[1] = (float*)(b + off[13] + 3 * fb);
+        s->zmask[0] = (uint8_t*)(b + off[13] + 4 * fb);
+        s->zmask[1] = (uint8_t*)(b + off[13] + 4 * fb + align256(ncols));
+    }
     if (c->bb) {
         s->xprev = (float*)(b + off[12]);
         s->gbar = (float*)(b + off[12] + align256(s->Npad * 4));
@@ -817,10 +859,68 @@ extern "C" int ct_oslalm_state_get(const ct_oslalm_state* s, ct_oslalm_state_vie
 // views of subset m owned by this rank (contiguous block)
 static ct_views rank_views(const ct_geom* g, int M, int m) {
     int count = (g->d.na - m + M - 1) / M;
+    if (g->zslab) return ct_views{m, M, count};   // z-slab ranks project every view onto their slab
     int base = count / g->nranks, extra = count % g->nranks;
     int k0 = g->rank * base + std::min(g->rank, extra);
     int n = base + (g->rank < extra ? 1 : 0);
     return ct_views{m + k0 * M, M, n};
+}
+
+// z-slab ranks (NEXT-3): of views {first + k stride, k < count}, the contiguous range [k0, k1)
+// whose cone can reach this rank's slab (helical: |z - z_s| <= zhalf; axial: all views).
+static void zslab_window(const ct_geom* g, ct_views v, int* k0, int* k1) {
+    *k0 = 0;
+    *k1 = v.count;
+    const DevGeom& dg = g->dg;
+    if (g->d.kind != CT_CONE_HELICAL || !(dg.dzs > 0.0f) || v.count == 0) return;
+    const double zlo = dg.zb0, zhi = (double)dg.zb0 + (double)dg.nz * dg.dz, zh = (double)dg.zhalf + dg.dz;
+    const double vlo = (zlo - zh - dg.zs0) / dg.dzs, vhi = (zhi + zh - dg.zs0) / dg.dzs;
+    *k0 = std::max(0, (int)floor((vlo - v.first) / v.stride) - 1);
+    *k1 = std::min(v.count, (int)ceil((vhi - v.first) / v.stride) + 2);
+    if (*k1 < *k0) *k1 = *k0;
+}
+
+// Forward projection summed over the z-slab ranks: out[k] = sum_slabs A_slab x_slab for
+// views k < v.count (only the rank's view window is projected; other views contribute 0),
+// then s <- scale W (s - y) on every ray (y nullable).
+static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* out, const float* y, const float* w,
+                           float scale, cudaStream_t st) {
+    const size_t cells = n_cells_view(g);
+    int k0, k1;
+    zslab_window(g, v, &k0, &k1);
+    if (k0 > 0) CT_CUDA(cudaMemsetAsync(out, 0, (size_t)k0 * cells * 4, st));
+    if (k1 < v.count) CT_CUDA(cudaMemsetAsync(out + (size_t)k1 * cells, 0, (size_t)(v.count - k1) * cells * 4, st));
+    if (k1 > k0)
+        if (int e = launch_fwd<false>(g, ct_views{v.first + k0 * v.stride, v.stride, k1 - k0}, x, out + (size_t)k0 * cells,
+                                      nullptr, nullptr, 1.0f, st))
+            return e;
+    if (int e = allreduce(g, out, (size_t)v.count * cells, st)) return e;
+    const size_t n = (size_t)v.count * cells;
+    resid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, y, w, v.first, v.stride, v.count, (int)cells, scale);
+    CT_LAUNCHED(1);
+    return CT_OK;
+}
+
+// Boundary slices to / from the neighbouring z-slab ranks (rank - 1 below, rank + 1 above).
+template <class T>
+static int zslab_halo(const ct_geom* g, const T* x, T* send_lo, T* send_hi, T* recv_lo, T* recv_hi, cudaStream_t st) {
+    const int ncols = g->d.nx * g->d.ny, nz = g->d.nz;
+    const ncclDataType_t dt = sizeof(T) == 1 ? ncclUint8 : ncclFloat32;
+    zslice_pack_kernel<T><<<(ncols + 255) / 256, 256, 0, st>>>(x, nz, 0, send_lo, ncols);
+    zslice_pack_kernel<T><<<(ncols + 255) / 256, 256, 0, st>>>(x, nz, nz - 1, send_hi, ncols);
+    CT_LAUNCHED(2);
+    ncclResult_t r = g_nccl.GroupStart();
+    if (g->rank > 0) {
+        if (r == ncclSuccess) r = g_nccl.Send(send_lo, ncols, dt, g->rank - 1, g->comm, st);
+        if (r == ncclSuccess) r = g_nccl.Recv(recv_lo, ncols, dt, g->rank - 1, g->comm, st);
+    }
+    if (g->rank < g->nranks - 1) {
+        if (r == ncclSuccess) r = g_nccl.Send(send_hi, ncols, dt, g->rank + 1, g->comm, st);
+        if (r == ncclSuccess) r = g_nccl.Recv(recv_hi, ncols, dt, g->rank + 1, g->comm, st);
+    }
+    ncclResult_t r2 = g_nccl.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess) return fail(CT_ENCCL, "z-slab halo exchange: %s", nccl_err(r != ncclSuccess ? r : r2));
+    return CT_OK;
 }
 
 
@@ -831,7 +931,11 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
     int M = s->cfg.M;
     ct_views v = rank_views(g, M, m);
     int t0 = tmark(s, st);
-    if (int e = launch_fwd<true>(g, v, x, s->sino, d->y, d->w, (float)M, st)) return e;
+    if (g->zslab) {
+        if (int e = zslab_fwd_resid(g, v, x, s->sino, d->y, d->w, (float)M, st)) return e;
+    } else {
+        if (int e = launch_fwd<true>(g, v, x, s->sino, d->y, d->w, (float)M, st)) return e;
+    }
     tmark_end(s, st, 1, t0);
     GupdArgs ga{};
     ga.mask = d->mask;
@@ -846,6 +950,32 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
     ga.log_slot = s->log_slot;
     ga.gbar = epi == EPI_GUPD ? s->gbar : nullptr;   // BB: accumulate the iteration's mean subset gradient
     ga.inv_M = 1.0f / (float)M;
+    if (g->zslab) {
+        // z-slab rank: the back-projection onto the slab is complete (the residual holds every
+        // ray), so the fused epilogue runs; only xi is a sum over ranks
+        int k0, k1;
+        zslab_window(g, v, &k0, &k1);
+        const ct_views vw{v.first + k0 * v.stride, v.stride, k1 - k0};
+        const float* rsino = s->sino + (size_t)k0 * n_cells_view(g);
+        if (epi == EPI_INIT) {
+            ga.G_new = s->Gbuf[s->curG];
+            return launch_back<EPI_INIT>(g, vw, rsino, nullptr, ga, st);
+        }
+        ga.G_old = s->Gbuf[s->curG];
+        ga.G_new = s->Gbuf[s->curG ^ 1];
+        ga.xi_out = s->xi_ex;
+        int t1 = tmark(s, st);
+        if (int e = launch_back<EPI_GUPD>(g, vw, rsino, nullptr, ga, st)) return e;
+        tmark_end(s, st, 2, t1);
+        int t2 = tmark(s, st);
+        ncclResult_t r = g_nccl.AllReduce(s->xi_ex, s->xi_ex + 1, 1, ncclFloat64, ncclSum, g->comm, st);
+        if (r != ncclSuccess) return fail(CT_ENCCL, "ncclAllReduce(xi): %s", nccl_err(r));
+        ga.xi_out = nullptr;
+        xi_rule_kernel<<<1, 256, 0, st>>>(ga, s->xi_ex + 1);
+        CT_LAUNCHED(1);
+        tmark_end(s, st, 4, t2);
+        return CT_OK;
+    }
     if (g->comm == nullptr) {   // single GPU: fused epilogue
         if (epi == EPI_INIT) {
             ga.G_new = s->Gbuf[s->curG];
@@ -931,11 +1061,19 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
                     sqs_update_kernel<8><<<nblk(rj1 - rj0), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl,
                                                                           d->mask, &s->sc->rho, &s->sc->alpha, (float)c.reg.beta,
                                                                           inv_d, rj0, rj1);
-                else
+                else {
+                    ZHalo hz{nullptr, nullptr, nullptr, nullptr};
+                    if (g->zslab && g->nranks > 1) {   // neighbours' boundary slices of x (and of S, once)
+                        if (int e = zslab_halo<float>(g, xa, s->zsend[0], s->zsend[1], s->zrecv[0], s->zrecv[1], st))
+                            return e;
+                        if (g->rank > 0) { hz.lo = s->zrecv[0]; hz.mlo = s->zmask[0]; }
+                        if (g->rank < g->nranks - 1) { hz.hi = s->zrecv[1]; hz.mhi = s->zmask[1]; }
+                    }
                     sqs_update3d_kernel<<<dim3((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (ry1 - ry0 + kK3Y - 1) / kK3Y),
                                           256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
                                                         &s->sc->rho, &s->sc->alpha, (float)c.reg.beta, inv_d, ry0,
-                                                        ry1);
+                                                        ry1, hz);
+                }
                 CT_LAUNCHED(1);
             }
             if (s->slab) {   // every rank needs the full x+ for its next forward projection
@@ -1007,6 +1145,11 @@ static int ensure_initialised(ct_oslalm_state* s, const ct_oslalm_data* d, float
     zero_offmask_kernel<<<nblk(s->N), 256, 0, st>>>(x, d->mask, s->N);
     CT_LAUNCHED(1);
     if (c.bb) CT_CUDA(cudaMemsetAsync(s->gbar, 0, s->Npad * 4, st));
+    if (s->g->zslab && s->g->nranks > 1) {   // the neighbours' boundary slices of S (static)
+        uint8_t* sb = reinterpret_cast<uint8_t*>(s->zsend[0]);
+        if (int e = zslab_halo<uint8_t>(s->g, d->mask, sb, sb + s->g->d.nx * s->g->d.ny, s->zmask[0], s->zmask[1], st))
+            return e;
+    }
     if (int e = subset_gradient(s, d, x, s->order[0], EPI_INIT, st)) return e;
     s->initialised = 1;
     return CT_OK;
@@ -1144,5 +1287,14 @@ extern "C" int ct_comm_init(ct_geom* g, int rank, int nranks, const void* uid) {
     g->comm = comm;
     g->rank = rank;
     g->nranks = nranks;
+    g->zslab = 0;
+    return CT_OK;
+}
+
+extern "C" int ct_comm_init_zslab(ct_geom* g, int rank, int nranks, const void* uid) {
+    if (!g) return fail(CT_EINVAL, "ct_comm_init_zslab: null argument");
+    if (g->d.kind == CT_FAN2D) return fail(CT_EUNSUPPORTED, "z-slab decomposition needs a cone-beam geometry");
+    if (int e = ct_comm_init(g, rank, nranks, uid)) return e;
+    g->zslab = 1;
     return CT_OK;
 }

@@ -360,6 +360,8 @@ struct GupdArgs {
     int log_slot;
     float* gbar;           // BB (nullable): running mean of the iteration's subset gradients
     float inv_M;
+    double* xi_out;        // z-slab ranks (nullable): the last block stores this rank's xi sum here
+                           // (all-reduced, then xi_rule_kernel applies K4) instead of finalizing
 };
 
 // xi = fixed-order fp64 sum of the partials; l <- (xi > 0) ? 0 : l + 1; rho <- rho_l.
@@ -407,7 +409,23 @@ __device__ __forceinline__ void xi_arrive(const GupdArgs& ga, int nblocks) {
     __syncthreads();
     if (last) {
         __threadfence();
-        xi_finalize_block<NTHR>(ga.xi_part, nblocks, ga);
+        if (ga.xi_out) {
+            __shared__ double red[NTHR];
+            double s = 0.0;
+            for (int i = threadIdx.x; i < nblocks; i += NTHR) s += __ldcg(&ga.xi_part[i]);
+            red[threadIdx.x] = s;
+            __syncthreads();
+            for (int o = NTHR / 2; o > 0; o >>= 1) {
+                if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                *ga.xi_out = red[0];
+                ga.sc->arrive = 0;
+            }
+        } else {
+            xi_finalize_block<NTHR>(ga.xi_part, nblocks, ga);
+        }
     }
 }
 
@@ -855,6 +873,34 @@ __global__ void __launch_bounds__(256) sqs_update_kernel(DevGeom g, const float*
     xn[j] = fmaxf(v, 0.0f);
 }
 
+// Boundary slices of the neighbouring z-slab ranks (nullable pointers: no neighbour).
+struct ZHalo {
+    const float* lo;
+    const float* hi;
+    const uint8_t* mlo;
+    const uint8_t* mhi;
+};
+
+// z-slab ranks: out[c] = x[c nz + z] (one slice of every column; c < ncols).
+template <class T>
+__global__ void zslice_pack_kernel(const T* __restrict__ x, int nz, int z, T* __restrict__ out, int ncols) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < ncols) out[c] = x[(size_t)c * nz + z];
+}
+
+// Sinogram-domain residual (z-slab ranks, after the all-reduce of the partial projections):
+// s <- scale W (s - y) in place (y nullable: s <- scale W s, the D_L setup).
+__global__ void __launch_bounds__(256) resid_kernel(float* __restrict__ s, const float* __restrict__ yobs,
+                                                   const float* __restrict__ wts, int first, int stride, int count,
+                                                   int cells_per_view, float scale) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)count * cells_per_view) return;
+    const int k = (int)(i / cells_per_view);
+    const size_t gi = (size_t)(first + k * stride) * cells_per_view + (i - (size_t)k * cells_per_view);
+    const float yo = yobs ? __ldg(&yobs[gi]) : 0.0f;
+    s[i] = scale * __ldg(&wts[gi]) * (s[i] - yo);
+}
+
 // 3D (26-neighbour) K3 with shared-memory planes: block = 8 (ix) x 32 (z) voxels
 // marching along iy; three planes of x (with a one-voxel halo) rotate through
 // shared memory, voxels outside S (or outside the grid) are stored as NaN so the
@@ -867,8 +913,9 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                                                           const float* __restrict__ dl, const uint8_t* __restrict__ m,
                                                           const double* __restrict__ rho_p,
                                                           const double* __restrict__ alpha_p, float beta, float inv_delta,
-                                                          int iy_begin, int iy_end) {
-    // updates rows [iy_begin, iy_end) (multi-rank: this rank's slab; x is the full image)
+                                                          int iy_begin, int iy_end, ZHalo hz) {
+    // updates rows [iy_begin, iy_end) (multi-rank: this rank's slab; x is the full image).
+    // z-slab ranks: hz holds the neighbours' boundary slices (z = -1, z = nz) and their mask.
     __shared__ float Pl[3][10][34];
     const int tz = threadIdx.x & 31, tx = threadIdx.x >> 5;
     const int ix0 = blockIdx.x * 8, z0 = blockIdx.y * 32, iy0 = iy_begin + blockIdx.z * kK3Y;
@@ -880,9 +927,15 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
             const int a = e / 34, b = e - a * 34;
             const int ix = ix0 - 1 + a, iz = z0 - 1 + b;
             float v = __int_as_float(0x7fc00000);   // NaN: not in S
-            if (iy >= 0 && iy < ny && ix >= 0 && ix < nx && iz >= 0 && iz < nz) {
-                const int j = (iy * nx + ix) * nz + iz;
-                if (__ldg(&m[j])) v = __ldg(&x[j]);
+            if (iy >= 0 && iy < ny && ix >= 0 && ix < nx) {
+                if (iz >= 0 && iz < nz) {
+                    const int j = (iy * nx + ix) * nz + iz;
+                    if (__ldg(&m[j])) v = __ldg(&x[j]);
+                } else {
+                    const int c = iy * nx + ix;
+                    if (iz == -1 && hz.lo && hz.mlo[c]) v = hz.lo[c];
+                    if (iz == nz && hz.hi && hz.mhi[c]) v = hz.hi[c];
+                }
             }
             Pl[slot][a][b] = v;
         }

@@ -29,7 +29,7 @@ EXPORTS = ("ct_geom_create", "ct_geom_destroy", "ct_last_error", "ct_fwd_proj", 
            "ct_sqs_denom_scratch_bytes", "ct_sqs_denom", "ct_reg_grad", "ct_count_vv", "ct_oslalm_state_bytes",
            "ct_oslalm_state_create", "ct_fbp", "ct_fbp_scratch_bytes", "ct_peak_l2_read", "ct_oslalm_state_destroy", "ct_oslalm_state_get", "ct_oslalm_state_reset",
            "ct_oslalm_set_timing", "ct_oslalm_get_timing", "ct_oslalm_iter",
-           "ct_oslalm_run", "ct_comm_init", "ct_comm_get_unique_id", "ct_build_info", "ct_kernel_launches")
+           "ct_oslalm_run", "ct_comm_init", "ct_comm_init_zslab", "ct_comm_get_unique_id", "ct_build_info", "ct_kernel_launches")
 
 
 class CTError(RuntimeError):
@@ -111,6 +111,7 @@ def load():
     L.ct_oslalm_iter.argtypes = [vp, P(ct_oslalm_cfg), P(ct_oslalm_data), vp, vp, vp]
     L.ct_oslalm_run.argtypes = [vp, P(ct_oslalm_cfg), P(ct_oslalm_data), vp, vp, i, P(ct_oslalm_log), vp]
     L.ct_comm_init.argtypes = [vp, i, i, vp]
+    L.ct_comm_init_zslab.argtypes = [vp, i, i, vp]
     L.ct_comm_get_unique_id.argtypes = [vp]
     _lib = L
     return L
@@ -229,9 +230,10 @@ def ct_comm_get_unique_id() -> bytes:
     return buf.raw
 
 
-def ct_comm_init(h, rank, nranks, uid: bytes):
+def ct_comm_init(h, rank, nranks, uid: bytes, zslab=False):
     buf = ctypes.create_string_buffer(bytes(uid), 128)
-    _check(load().ct_comm_init(h, int(rank), int(nranks), buf))
+    f = load().ct_comm_init_zslab if zslab else load().ct_comm_init
+    _check(f(h, int(rank), int(nranks), buf))
 
 
 # ---------------------------------------------------------------------------
@@ -314,8 +316,10 @@ class Geometry:
         scratch = torch.zeros(32, dtype=torch.uint8, device=self.device)
         return ct_count_vv(self.h, views or self.views(), mask, scratch)
 
-    def comm_init(self, rank, nranks, uid):
-        ct_comm_init(self.h, rank, nranks, uid)
+    def comm_init(self, rank, nranks, uid, zslab=False):
+        """Attach an NCCL communicator.  zslab=True: this geometry is rank `rank`'s z-slab of the
+        volume (host.rank_zslab / inputs.slab_geom), partial sinograms are summed (NEXT-3)."""
+        ct_comm_init(self.h, rank, nranks, uid, zslab)
         self.rank, self.nranks = rank, nranks
 
 

@@ -4,6 +4,8 @@
   PAPER.md P:541-559 (eqs. max_M_axial, max_M_helical; s_axial ~ 40, s_helical ~ 24).
 * ``rank_view_block`` — the multi-GPU partition of one subset's views:
   rank p of P owns a contiguous block of the subset's n_m views.
+* ``rank_zslab`` — the z-slab decomposition (NEXT-3): rank p owns slices [z0, z1) of the
+  volume and works on the slab's own geometry (``inputs.slab_geom``).
 * ``rank_slab`` — the multi-GPU partition of the image for the SQS update: rank p owns a
   contiguous block of image rows (iy); buffers are padded to P equal slabs (mirror of
   ``slab_geometry`` in ct_abi.cu).
@@ -39,3 +41,10 @@ def rank_slab(ny: int, rank: int, nranks: int) -> tuple[int, int, int]:
     """Rows [iy0, iy1) of the image owned by `rank`, and the padded rows per slab R (P*R >= ny)."""
     R = (ny + nranks - 1) // nranks
     return min(ny, rank * R), min(ny, (rank + 1) * R), R
+
+
+def rank_zslab(nz: int, rank: int, nranks: int) -> tuple[int, int]:
+    """Slices [z0, z1) of the volume owned by `rank` in the z-slab decomposition (NEXT-3)."""
+    base, extra = divmod(nz, nranks)
+    z0 = rank * base + min(rank, extra)
+    return z0, z0 + base + (1 if rank < extra else 0)

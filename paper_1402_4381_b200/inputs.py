@@ -106,6 +106,14 @@ def scaled(cfg: ScanConfig, name: str, **geom_over) -> ScanConfig:
                       cfg.recipe, cfg.body_z, dict(cfg.extra))
 
 
+def slab_geom(g: dict, z0: int, z1: int) -> dict:
+    """The geometry of slices [z0, z1) of g's volume (same scan; voxel centres on g's grid)."""
+    s = dict(g)
+    s["nz"] = z1 - z0
+    s["offz"] = g.get("offz", 0.0) + ((z0 + z1 - 1) / 2.0 - (g["nz"] - 1) / 2.0) * g["dz"]
+    return s
+
+
 def fov_radius(g: dict) -> float:
     """Radius of the circle every fan covers: dso sin(ns ds / (2 dsd))."""
     return g["dso"] * math.sin(g["ns"] * g["ds"] / (2.0 * g["dsd"]))

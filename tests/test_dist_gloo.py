@@ -100,6 +100,75 @@ def _slab_worker(rank, ws, port, out):
     dist.destroy_process_group()
 
 
+def _zslab_worker(rank, ws, port, out):
+    """z-slab decomposition (NEXT-3) with the oracle as the projector on each rank: partial
+    sinograms of the slabs all-reduced = the full forward projection; the back-projection onto
+    the slab = the full back-projection's slices; the regulariser on the slab with the
+    neighbours' boundary slices (halo) = the full one's slices (what the 26-neighbour update
+    of ct_abi.cu's z-slab path computes)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import oracle as O
+    from paper_1402_4381_b200 import host
+    from paper_1402_4381_b200 import inputs as I
+    from tests import geomutil as GU
+    g = GU.small_geoms()["helical_c5"]
+    rng = np.random.default_rng(2)
+    x = rng.random(O.img_shape(g)) * 0.02          # oracle layout [iz][iy][ix]
+    r = rng.standard_normal(O.sino_shape(g, g["na"]))
+    z0, z1 = host.rank_zslab(g["nz"], rank, ws)
+    gs = I.slab_geom(g, z0, z1)
+    part = torch.from_numpy(O.fwd(gs, x[z0:z1]))
+    dist.all_reduce(part)
+    back_s = O.back(gs, r)
+    # halo: the slab extended by the neighbours' boundary slices, result cropped
+    e0, e1 = max(z0 - 1, 0), min(z1 + 1, g["nz"])
+    ge = I.slab_geom(g, e0, e1)
+    mask = np.ones((e1 - e0,) + O.img_shape(g)[1:], np.uint8)
+    gr_e, cu_e = O.reg_grad(ge, 2.0 ** 10, 2e-4, 26, mask, x[e0:e1])
+    gr_s = gr_e[z0 - e0:z0 - e0 + (z1 - z0)]
+    if rank == 0:
+        full = O.fwd(g, x)
+        bf = O.back(g, r)
+        grf, _ = O.reg_grad(g, 2.0 ** 10, 2e-4, 26, np.ones(O.img_shape(g), np.uint8), x)
+        out.put((float(np.abs(part.numpy() - full).max() / np.abs(full).max()),
+                 float(np.abs(back_s - bf[z0:z1]).max() / np.abs(bf).max()),
+                 float(np.abs(gr_s - grf[z0:z1]).max() / np.abs(grf).max())))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_rank_zslab():
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_zslab_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert max(res) <= 1e-12, res
+
+
+def test_zslab_partition():
+    from paper_1402_4381_b200 import host
+    from paper_1402_4381_b200 import inputs as I
+    g = I.config("c5").geom
+    for ws in (1, 2, 3, 8):
+        sl = [host.rank_zslab(g["nz"], r, ws) for r in range(ws)]
+        assert sl[0][0] == 0 and sl[-1][1] == g["nz"]
+        assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+        for z0, z1 in sl:   # slab voxel centres lie on the full grid
+            gs = I.slab_geom(g, z0, z1)
+            zc_full = (z0 - (g["nz"] - 1) / 2) * g["dz"] + g.get("offz", 0.0)
+            zc_slab = (0 - (gs["nz"] - 1) / 2) * gs["dz"] + gs["offz"]
+            assert abs(zc_full - zc_slab) <= 1e-9
+
+
 def test_slab_partition_covers_rows():
     from paper_1402_4381_b200 import host
     for ny in (1, 20, 64, 512, 513):

@@ -544,3 +544,58 @@ def test_empty_forward_and_one_view_subsets(ct, O):
     rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
     assert rms <= 0.5, rms
     assert np.array_equal(log[:, 2], logo[:, 2])
+
+
+# --------------------------------------------------------------------------- z-slabs (NEXT-3)
+
+@pytest.mark.parametrize("name", ["axial_c3", "helical_c4", "helical_c5"])
+def test_zslab_decomposition(ct, name):
+    """A x is separable over voxels: the slab geometries' forward projections sum to the full
+    one, and their back-projections are the full back-projection's slices (NEXT-3)."""
+    from paper_1402_4381_b200 import host
+    g = geoms_small()[name]
+    geo = ct.Geometry(g)
+    rng = np.random.default_rng(8)
+    x = torch.from_numpy(rng.random(geo.img_shape).astype(np.float32)).cuda()
+    y = torch.from_numpy(rng.random(geo.sino_shape(g["na"])).astype(np.float32)).cuda()
+    yf, bf = geo.fwd(x), geo.back(y)
+    ysum = torch.zeros_like(yf)
+    for r in range(3):
+        z0, z1 = host.rank_zslab(g["nz"], r, 3)
+        gs = ct.Geometry(I.slab_geom(g, z0, z1))
+        ysum += gs.fwd(x[..., z0:z1].contiguous())
+        bs = gs.back(y)
+        assert rel_l2(bs.cpu().numpy(), bf[..., z0:z1].cpu().numpy(), f"zslab back {name} slab {r}") <= 1e-6
+    assert rel_l2(ysum.cpu().numpy(), yf.cpu().numpy(), f"zslab fwd sum {name}") <= 1e-6
+
+
+def test_zslab_path_single_rank(ct, O):
+    """The z-slab exchange path (partial sinograms all-reduced, residual on every ray,
+    back-projection onto the slab, xi all-reduced) on a 1-rank communicator: D_L equals the
+    plain D_L and OS-LALM (26 neighbours, BB on) matches the fp64 oracle."""
+    g = geoms_small()["helical_c4"]
+    base = I.config("c4")
+    ell = [(0.0, 0.0, 0.0, 4.0, 3.5, 2.5, 0.0, 0.02), (1.0, -0.5, 0.3, 1.2, 0.8, 0.9, 0.4, 0.01)]
+    d = I.noisy_data(g, ell, 1e5, 0.0, 79)
+    m0 = torch.ones((g["ny"], g["nx"], g["nz"]), dtype=torch.uint8)
+    plain = ct.Geometry(g)
+    dl0, _ = plain.sqs_denom(d["w"].cuda(), m0.cuda())
+    geo = ct.Geometry(g)
+    geo.comm_init(0, 1, ct.ct_comm_get_unique_id(), zslab=True)
+    dl, S = geo.sqs_denom(d["w"].cuda(), m0.cuda())
+    assert rel_l2(dl.cpu().numpy(), dl0.cpu().numpy(), "zslab D_L") <= 1e-6
+    sol = ct.OSLALM(geo, 4, beta=base.beta, delta=base.delta, nbr=26, bb=True)
+    sol.set_data(d["y"].cuda(), d["w"].cuda(), dl, S)
+    x = torch.zeros(geo.img_shape, device="cuda")
+    log = np.array(sol.run(x, 6, log=True))
+    dlo, So = O.sqs_denom(g, I.to_oracle_sino(d["w"]), I.to_oracle_image(m0).astype(np.uint8))
+    xo, logo, _, _ = O.oslalm_run(g, I.to_oracle_sino(d["y"]), I.to_oracle_sino(d["w"]), dlo, So,
+                                  np.zeros(O.img_shape(g)), M=4, beta=base.beta, delta=base.delta, nbr=26, n_iter=6,
+                                  bb=True)
+    xg = I.to_oracle_image(x.cpu().numpy())
+    rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
+    MARGINS.append({"case": "z-slab path helical_c4 (1 rank, BB) vs oracle", "rms_HU": rms})
+    assert rms <= 0.5, rms
+    assert np.array_equal(log[:, 2], logo[:, 2])
+    with pytest.raises(ct.CTError, match="EUNSUPPORTED"):
+        ct.OSLALM(geo, 4, beta=base.beta, delta=base.delta, nbr=26, inner="fista", n_inner=2)
