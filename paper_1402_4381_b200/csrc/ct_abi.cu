@@ -21,6 +21,28 @@
 
 using namespace ct;
 
+#ifndef CT_PDL
+#define CT_PDL 1   // programmatic dependent launch of the 2D inner-step kernels (A/B: 0 disables)
+#endif
+// Launch with the programmatic-stream-serialization attribute (PDL): the kernel's blocks
+// may start while the previous kernel in the stream finishes; the kernel synchronises with
+// pdl_wait() before it reads the predecessor's output.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = CT_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 #ifndef CT_FWD3D_TC
 #define CT_FWD3D_TC 24   // channels per 3D forward CTA (A/B: 24 beats 16 and 32 by ~10 %)
 #endif
@@ -315,10 +337,10 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
             configured = smem;
         }
         dim3 grid((dg.nx + kF2T - 1) / kF2T, (dg.ny + kF2T - 1) / kF2T, (v.count + kF2VC - 1) / kF2VC);
-        fwd2d_tile_kernel<<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, x, g->acc2d);
+        CT_CUDA(launch_pdl(fwd2d_tile_kernel, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
         const int cells = v.count * dg.ns;
-        fwd2d_finalize_kernel<RESID><<<(cells + 255) / 256, 256, 0, st>>>(dg, v.first, v.stride, v.count, g->acc2d, out,
-                                                                          yobs, w, scale);
+        CT_CUDA(launch_pdl(fwd2d_finalize_kernel<RESID>, dim3((cells + 255) / 256), dim3(256), 0, st, dg, v.first,
+                           v.stride, v.count, g->acc2d, out, yobs, w, scale));
         CT_LAUNCHED(1);
     } else {
         // per line, the columns holding a nonzero voxel of x (trims the wedge walk)
@@ -369,7 +391,7 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
     dim3 grid;
     back_grid(g, grid);
     if (dg.kind == CT_FAN2D)
-        back2d_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+        CT_CUDA(launch_pdl(back2d_kernel<EPI>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
     else if (back3d_use_chunks(g))
         back3d_chunk_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
     else {
@@ -386,6 +408,7 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
 }
 
 static inline unsigned nblk(size_t n) { return (unsigned)((n + 255) / 256); }
+
 
 // ---------------------------------------------------------------------------
 // projections, D_L, regulariser, U
@@ -1054,9 +1077,10 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
         if (c.inner == CT_INNER_SQS) {
             if (ry1 > ry0) {
                 if (c.reg.nbr == 8 && nz_of(g) == 1)
-                    sqs_update2d_kernel<<<dim3((g->dg.nx + 31) / 32, (ry1 - ry0 + 7) / 8), 256, 0, st>>>(
-                        g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask, &s->sc->rho, &s->sc->alpha,
-                        (float)c.reg.beta, inv_d, ry0, ry1);
+                    CT_CUDA(launch_pdl(sqs_update2d_kernel, dim3((g->dg.nx + 31) / 32, (ry1 - ry0 + 7) / 8), dim3(256), 0,
+                                       st, g->dg, (const float*)xa, xb, (const float*)s->Gbuf[s->curG],
+                                       (const float*)s->gs, d->dl, d->mask, (const double*)&s->sc->rho,
+                                       (const double*)&s->sc->alpha, (float)c.reg.beta, inv_d, ry0, ry1));
                 else if (c.reg.nbr == 8)
                     sqs_update_kernel<8><<<nblk(rj1 - rj0), 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl,
                                                                           d->mask, &s->sc->rho, &s->sc->alpha, (float)c.reg.beta,

@@ -221,6 +221,15 @@ __device__ __forceinline__ void voxel_rows(const Axial& ax, const DevGeom& g, in
     r1 = __float2int_rd((zi + 1.0f - ax.qf) * ax.inv_kz + g.rbase + 0.5f);
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the PDL attribute may start
+// while its predecessor in the stream is still running; pdl_wait() blocks until that
+// predecessor has completed and its writes are visible (so code before it may touch only
+// static data: geometry tables, the support mask, shared memory).  pdl_trigger() lets the
+// next kernel's blocks be scheduled once every block of this grid has issued it.
+// Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // Fair potential pieces (reading G3/G14)
 __device__ __forceinline__ void fair(float t, float inv_delta, float& dpsi, float& omega) {
     omega = __frcp_rn(1.0f + fabsf(t) * inv_delta);

@@ -159,6 +159,8 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int vx0 = blockIdx.x * kF2T, vy0 = blockIdx.y * kF2T;
     const int nvx = min(kF2T, g.nx - vx0), nvy = min(kF2T, g.ny - vy0);   // valid pixels in the tile
+    pdl_trigger();
+    pdl_wait();   // x is the previous kernel's output
     bool any = false;
     for (int e = tid; e < kF2T * kF2T; e += 256) {
         const int j = e >> 5, i = e & 31;
@@ -265,6 +267,8 @@ __global__ void __launch_bounds__(256) fwd2d_finalize_kernel(DevGeom g, int firs
                                                             unsigned long long* __restrict__ acc, float* __restrict__ out,
                                                             const float* __restrict__ yobs, const float* __restrict__ wts,
                                                             float scale) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * 256 + threadIdx.x;
     if (i >= count * g.ns) return;
     const long long q = (long long)acc[i];
@@ -299,8 +303,9 @@ __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, 
     const bool valid = ix < g.nx && iy < g.ny;
     const size_t jv = (size_t)(valid ? iy : 0) * g.nx + (valid ? ix : 0);
     // voxels outside the support S are not needed by OS-LALM / D_L: skip their views
-    const bool act = valid && (ga.mask == nullptr || ga.mask[jv]);
+    const bool act = valid && (ga.mask == nullptr || ga.mask[jv]);   // the mask is static
     float acc = 0.0f;
+    pdl_trigger();
     if (__syncthreads_or(act)) {
         const int vx0 = blockIdx.x * 32, vy0 = blockIdx.y * 8;
         const float pxl = vertex_px(g, vx0 + lane), pxe = vertex_px(g, vx0 + 32);
@@ -317,6 +322,7 @@ __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, 
                     if (lane == 0) SC[kk] = make_float2(vw.x, vw.y);
                 }
             }
+            if (kb == 0) pdl_wait();   // the vertex tables depend on the geometry only; y is the predecessor's
             __syncthreads();
             if (act) {
                 for (int kk = 0; kk < nb; kk++) {
@@ -331,6 +337,7 @@ __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, 
             __syncthreads();
         }
     }
+    pdl_wait();   // (tiles outside S skipped the loop) the epilogue writes G+, g
     const size_t j = (size_t)iy * g.nx + ix;
     const double xi = back_epilogue<EPI>(j, valid, acc, x, ga);
     if (EPI == EPI_GUPD) {

@@ -998,6 +998,8 @@ __global__ void __launch_bounds__(256) sqs_update2d_kernel(DevGeom g, const floa
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int ix0 = blockIdx.x * 32, iy0 = iy_begin + blockIdx.y * 8;
     const int nx = g.nx;
+    pdl_trigger();
+    pdl_wait();   // G, g, rho are the previous kernels' outputs
     for (int e = threadIdx.x; e < 340; e += 256) {
         const int a = e / 34, b = e - a * 34;
         const int iy = iy0 - 1 + a, ix = ix0 - 1 + b;
