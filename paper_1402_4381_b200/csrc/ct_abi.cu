@@ -1234,13 +1234,20 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
         if (err) return err;
         if (ce != cudaSuccess) return fail(CT_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
         ce = cudaGraphInstantiate(&ge->exec, graph, 0);
-        size_t nn = 0;
+        // kernel launches per replay = the graph's kernel nodes (exact, for ct_kernel_launches)
+        size_t nn = 0, nkern = 0;
         cudaGraphGetNodes(graph, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+        for (size_t i = 0; i < nn; i++) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) nkern++;
+        }
         cudaGraphDestroy(graph);
         if (ce != cudaSuccess) return fail(CT_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce));
         memcpy(ge->key, key, sizeof(key));
         ge->curG = startG;
-        ge->nodes = (size_t)nk;
+        ge->nodes = nkern ? nkern : (size_t)nk;
     }
     CT_CUDA(cudaEventRecord(s->ev_in, st));
     CT_CUDA(cudaStreamWaitEvent(s->cap, s->ev_in, 0));
