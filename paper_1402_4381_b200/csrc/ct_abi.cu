@@ -361,20 +361,12 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
     return CT_OK;
 }
 
-#ifndef CT_BACK3D_CHUNKS
-#define CT_BACK3D_CHUNKS 0   // 1: axial scans use the 64-slice register-chunk kernel (tuning A/B)
-#endif
-// 3D back-projection variant: axial scans use 64-slice register chunks (every view's
-// cone covers a chunk); helical scans use whole-column shared-memory accumulators so
-// the work follows each view's active slices.
-static bool back3d_use_chunks(const ct_geom* g) { return CT_BACK3D_CHUNKS && g->d.kind == CT_CONE_AXIAL; }
-
+// 3D back-projection: one warp per whole voxel column with shared-memory accumulators, so
+// the work follows each view's active slices (axial and helical scans alike).
 static void back_grid(const ct_geom* g, dim3& grid) {
     const DevGeom& dg = g->dg;
     if (dg.kind == CT_FAN2D)
         grid = dim3((dg.nx + 31) / 32, (dg.ny + 7) / 8, 1);
-    else if (back3d_use_chunks(g))
-        grid = dim3((dg.nx + 3) / 4, (dg.ny + 1) / 2, (dg.nz + 63) / 64);
     else
         grid = dim3((dg.nx + 3) / 4, (dg.ny + 1) / 2, 1);
 }
@@ -392,8 +384,6 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
     back_grid(g, grid);
     if (dg.kind == CT_FAN2D)
         CT_CUDA(launch_pdl(back2d_kernel<EPI>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
-    else if (back3d_use_chunks(g))
-        back3d_chunk_kernel<EPI><<<grid, 256, 0, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
     else {
         const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * (size_t)dg.nz;
         static int configured[4] = {0, 0, 0, 0};

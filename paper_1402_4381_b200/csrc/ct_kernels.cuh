@@ -93,7 +93,7 @@ struct __align__(16) Foot {
     float w[kMaxFoot];      // lphi * F_s(cA + j)
     int cA, n;              // first channel and channel count (n <= 0: misses the detector)
     Axial ax;               // 5 words
-    int rows;               // back3d: first row | (row count << 16) of the warp's z-chunk
+    int rows;               // back3d: first active slice | (slice count << 16); fwd3d: 32-bit column base
 };
 static_assert(sizeof(Foot) == 64, "Foot must be 64 bytes");
 
@@ -464,143 +464,6 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
         if (ga.mask[j]) return (double)(gg - Gp) * (double)(Gp - G);
     }
     return 0.0;
-}
-
-// ---------------------------------------------------------------------------
-// K2 (3D cone, axial): voxel-driven back projection; warp = one column x 64 slices
-// ---------------------------------------------------------------------------
-// Block = 4x2 columns (8 warps); lane l owns slices zlo + l and zlo + 32 + l.
-// Views are processed in batches of 32: lane l computes the column's footprint
-// for view vb + l into the warp's shared table.  For each view the warp then
-//  (1) forms the transaxially filtered detector rows of its z-chunk
-//        Q(r) = sum_c lphi F_s(c) y[k][c][r]
-//      (lanes = rows: unit-stride loads, warp-uniform loop over the channels)
-//      and their prefix sums (warp scan), and
-//  (2) for each slice, sum_r F_t(iz, r) Q(r) is the integral of the row-wise
-//      constant Q over the slice's extent on the detector (in row units):
-//      PF(u1) - PF(u0) with PF the piecewise-linear cumulative sum.
-// Used for axial scans, where every view's cone covers the whole chunk; helical scans
-// use the column kernel below, whose work follows each view's active slices.
-template <int EPI>
-__global__ void __launch_bounds__(256, 3) back3d_chunk_kernel(DevGeom g, int first, int stride, int count,
-                                                       const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
-    constexpr int kRows = 128;                 // >= nt (validated)
-    __shared__ Foot table[8][32];
-    __shared__ float Qs[8][kRows];
-    __shared__ float Pf[8][kRows + 1];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ix = blockIdx.x * 4 + (wid & 3);
-    const int iy = blockIdx.y * 2 + (wid >> 2);
-    const int zlo = blockIdx.z * 64;
-    const bool colok = ix < g.nx && iy < g.ny;
-    const int nt = g.nt, ns = g.ns, nz = g.nz;
-    const size_t col = (size_t)(colok ? iy : 0) * g.nx + (colok ? ix : 0);
-    bool valid[2], act[2];
-    size_t jv[2];
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-        const int iz = zlo + 32 * h + lane;
-        valid[h] = colok && iz < nz;
-        jv[h] = col * nz + (valid[h] ? iz : 0);
-        // voxels outside the support S are not needed by OS-LALM / D_L
-        act[h] = valid[h] && (ga.mask == nullptr || ga.mask[jv[h]]);
-    }
-    const bool warp_act = __ballot_sync(0xffffffffu, act[0] || act[1]) != 0u;
-    Foot* tab = table[wid];
-    float* Q = Qs[wid];
-    float* PF = Pf[wid];
-    float acc[2] = {0.0f, 0.0f};
-    if (warp_act) {
-        const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
-        const int zhi = min(nz, zlo + 64) - 1;
-        // helical: only the views whose source is within zhalf of the chunk can reach it
-        int k_lo = 0, k_hi = count - 1;
-        if (g.dzs != 0.0f) {
-            const float za = g.zb0 + zlo * g.dz - g.zhalf, zb = g.zb0 + (zhi + 1) * g.dz + g.zhalf;
-            float va = (za - g.zs0) / g.dzs, vbnd = (zb - g.zs0) / g.dzs;
-            if (va > vbnd) { float t = va; va = vbnd; vbnd = t; }
-            k_lo = max(0, (int)floorf((va - first) / stride) - 1);
-            k_hi = min(count - 1, (int)ceilf((vbnd - first) / stride) + 1);
-        }
-        for (int vb = k_lo; vb <= k_hi; vb += 32) {
-            const int kk = vb + lane;
-            if (kk <= k_hi) {
-                Foot f;
-                column_footprint(g, g.views[first + kk * stride], xc, yc, f);
-                int ra, rb, rc, rd;
-                voxel_rows(f.ax, g, zlo, ra, rb);
-                voxel_rows(f.ax, g, zhi, rc, rd);
-                ra = max(ra, 0);
-                rd = min(rd, nt - 1);
-                if (!(f.n > 0 && rd >= ra)) f.n = 0;   // the chunk's rows miss the detector
-                f.rows = ra | ((rd - ra + 1) << 16);
-                tab[lane] = f;
-            }
-            __syncwarp();
-            const int nb = min(32, k_hi + 1 - vb);
-            for (int j = 0; j < nb; j++) {
-                Foot f;
-                load_foot(&tab[j], f);
-                if (f.n <= 0) continue;
-                const int ra = f.rows & 0xffff, nr = f.rows >> 16;
-                const float* yv = y + (size_t)(vb + j) * ns * nt;     // this view's sinogram
-                const int off0 = f.cA * nt + ra;                        // 32-bit offsets below
-                // (1) filtered rows and their prefix sums (lanes = rows)
-                float carry = 0.0f;
-                for (int p0 = 0; p0 < nr; p0 += 32) {
-                    const int p = p0 + lane;
-                    const bool inr = p < nr;
-                    const float* yr = yv + (off0 + (inr ? p : 0));
-                    float q;
-                    if (f.n <= 4) {   // warp-uniform: issue all loads first, then the FMAs
-                        float v[4];
-#pragma unroll
-                        for (int c = 0; c < 4; c++) v[c] = (inr && c < f.n) ? __ldg(yr + c * nt) : 0.0f;
-                        q = f.w[0] * v[0] + f.w[1] * v[1] + f.w[2] * v[2] + f.w[3] * v[3];
-                    } else {
-                        float v[kMaxFoot];
-#pragma unroll
-                        for (int c = 0; c < kMaxFoot; c++) v[c] = (inr && c < f.n) ? __ldg(yr + c * nt) : 0.0f;
-                        q = 0.0f;
-#pragma unroll
-                        for (int c = 0; c < kMaxFoot; c++) q += f.w[c] * v[c];
-                    }
-                    if (inr) Q[p] = q;
-                    float inc = q;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        float t = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (lane >= o) inc += t;
-                    }
-                    if (p < nr) PF[p + 1] = carry + inc;
-                    carry += __shfl_sync(0xffffffffu, inc, 31);
-                }
-                if (lane == 0) PF[0] = 0.0f;
-                __syncwarp();
-                // (2) lanes = slices: integral of the row-wise constant Q over each slice
-                const float fnr = (float)nr;
-                const float ubase = g.rbase + 0.5f - (float)ra;
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    if (!act[h]) continue;
-                    const int iz = zlo + 32 * h + lane;
-                    const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
-                    float u0 = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubase), 0.0f), fnr);
-                    float u1 = fminf(fmaxf(fmaf(zi + 1.0f, f.ax.inv_kz, ubase), 0.0f), fnr);
-                    int p0 = min(__float2int_rd(u0), nr - 1), p1 = min(__float2int_rd(u1), nr - 1);
-                    float s0 = PF[p0] + (u0 - (float)p0) * Q[p0];
-                    float s1 = PF[p1] + (u1 - (float)p1) * Q[p1];
-                    acc[h] += ltheta(f.ax, iz) * (s1 - s0);
-                }
-                __syncwarp();
-            }
-        }
-    }
-    double xi = back_epilogue<EPI>(jv[0], valid[0], acc[0], x, ga) + back_epilogue<EPI>(jv[1], valid[1], acc[1], x, ga);
-    if (EPI == EPI_GUPD) {
-        block_sum_store<256>(xi, &ga.xi_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x]);
-        xi_arrive<256>(ga, gridDim.x * gridDim.y * gridDim.z);
-    }
 }
 
 // ---------------------------------------------------------------------------

@@ -1,3 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()"
 timeout 600 python -m pytest tests -m gpu -x -q -k "helical or axial or c3 or c4 or c5 or exchange or determinism or 3d" > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -4 gpurun_out/pytest_gpu.log
-for c in c3 c4 c5; do python tools/time_proj.py $c 3; done; python -m paper_1402_4381_b200.build --out paper_1402_4381_b200/tune_chunk.so -DCT_BACK3D_CHUNKS=1 >/dev/null; CT_OSLALM_LIB=paper_1402_4381_b200/tune_chunk.so python tools/time_proj.py c3 3
+for c in c3 c4 c5; do python tools/time_proj.py $c 3; done
