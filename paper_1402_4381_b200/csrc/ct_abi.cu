@@ -21,6 +21,9 @@
 
 using namespace ct;
 
+#ifndef CT_VREL
+#define CT_VREL 1   // fan 2D: vertex positions relative to per-block reference rays (A/B: 0 = absolute)
+#endif
 #ifndef CT_PDL
 #define CT_PDL 1   // programmatic dependent launch of the 2D inner-step kernels (A/B: 0 disables)
 #endif
@@ -194,7 +197,7 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     if (wmax > kMaxFoot - 1)
         return fail(CT_EUNSUPPORTED, "voxel footprint may be %.2f channels wide (> %d)", wmax, kMaxFoot - 1);
 
-    int dg_fpar = 1, dg_fspan = 1;
+    int dg_fpar = 1, dg_fspan = 1, dg_vrel = 0;
     if (is2d) {
         // fwd2d_tile_kernel: (1) lanes l and l + P must hit different first channels: a pixel
         // step along the warp's line moves the footprint by >= dx sin(pi/4 - delta) mag_min / ds
@@ -210,6 +213,13 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
                         span);
         dg_fpar = P;
         dg_fspan = span;
+        // relative vertex positions: |cross/dot| <= tan(asin(|offset| / distance)) over the 32-vertex
+        // block grid (offsets up to 16 sqrt(2) pixels from the block's reference vertex)
+        const double bx = 0.5 * 32.0 * ceil(d->nx / 32.0) * d->dx + fabs(d->offx) + d->dx;
+        const double by = 0.5 * 32.0 * ceil(d->ny / 32.0) * d->dy + fabs(d->offy) + d->dy;
+        const double dist = d->dso - sqrt(bx * bx + by * by);
+        const double off = 16.0 * sqrt(2.0) * d->dx;
+        dg_vrel = (dist > off && tan(asin(off / dist)) <= 0.4) ? 1 : 0;
     }
     int dev = d->device;
     DeviceGuard guard(dev);
@@ -286,6 +296,7 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     dg.views = g->d_views;
     dg.fpar = dg_fpar;
     dg.fspan = dg_fspan;
+    dg.vrel = CT_VREL ? dg_vrel : 0;
     gd.vz = g->d_vz;
     *out = g;
     return CT_OK;

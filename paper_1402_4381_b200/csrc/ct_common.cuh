@@ -36,6 +36,7 @@ struct DevGeom {
     float zs0, dzs;           // helical source height z_s(v) = zs0 + v dzs (dzs = 0: axial)
     float zhalf;              // bound on |z - z_s| of any voxel a view can see (mm)
     int fpar, fspan;          // fan 2D forward: lane-parity buffers P and tile channel-span bound
+    int vrel;                 // fan 2D: vertex positions relative to a per-block reference ray (1) or absolute (0)
     const float4* views;      // per view: (sin beta, cos beta, qi, qf) with
                               // (z_s - zb0)/dz = qi + qf, qi integer (exact in fp32)
 };
