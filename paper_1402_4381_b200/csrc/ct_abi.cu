@@ -344,11 +344,15 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         const size_t smem = sizeof(float) * 8 * dg.fpar * dg.fspan;
         static size_t configured = 0;
         if (smem > 48 * 1024 && configured < smem) {
-            cudaFuncSetAttribute(fwd2d_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(fwd2d_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(fwd2d_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             configured = smem;
         }
         dim3 grid((dg.nx + kF2T - 1) / kF2T, (dg.ny + kF2T - 1) / kF2T, (v.count + kF2VC - 1) / kF2VC);
-        CT_CUDA(launch_pdl(fwd2d_tile_kernel, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
+        if (dg.vrel)
+            CT_CUDA(launch_pdl(fwd2d_tile_kernel<true>, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
+        else
+            CT_CUDA(launch_pdl(fwd2d_tile_kernel<false>, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
         const int cells = v.count * dg.ns;
         CT_CUDA(launch_pdl(fwd2d_finalize_kernel<RESID>, dim3((cells + 255) / 256), dim3(256), 0, st, dg, v.first,
                            v.stride, v.count, g->acc2d, out, yobs, w, scale));
@@ -394,7 +398,10 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
     dim3 grid;
     back_grid(g, grid);
     if (dg.kind == CT_FAN2D)
-        CT_CUDA(launch_pdl(back2d_kernel<EPI>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
+        if (dg.vrel)
+            CT_CUDA(launch_pdl(back2d_kernel<EPI, true>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
+        else
+            CT_CUDA(launch_pdl(back2d_kernel<EPI, false>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
     else {
         const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * (size_t)dg.nz;
         static int configured[4] = {0, 0, 0, 0};

@@ -188,6 +188,7 @@ constexpr int kF2T = 32;      // tile edge (pixels)
 constexpr int kF2VC = 8;      // views per CTA
 constexpr float kFix = 4294967296.0f;   // 2^32
 
+template <bool VREL>
 __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom g, int first, int stride, int count,
                                                         const float* __restrict__ x,
                                                         unsigned long long* __restrict__ acc) {
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
     // the tile's last vertex column / row) for every view of the chunk: warp 0, lane = view x 4
     __shared__ VRef RF[kF2VC][4];
     const int k0 = blockIdx.z * kF2VC, k1 = min(count, k0 + kF2VC);
-    if (g.vrel && tid < 4 * kF2VC && k0 + (tid >> 2) < k1) {
+    if (VREL && tid < 4 * kF2VC && k0 + (tid >> 2) < k1) {
         const float4 vw = __ldg(&g.views[first + (k0 + (tid >> 2)) * stride]);
         RF[tid >> 2][tid & 3] = make_vref(g, vw.x, vw.y, blockIdx.x + (tid & 1), blockIdx.y + ((tid >> 1) & 1));
     }
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
     for (int k = k0; k < k1; k++) {
         const float4 vw = __ldg(&g.views[first + k * stride]);
         const float sb = vw.x, cb = vw.y;
-        if (g.vrel) {   // relative to the owner blocks' reference rays (no per-vertex atan)
+        if (VREL) {   // relative to the owner blocks' reference rays (no per-vertex atan)
             const VRef* R = RF[k - k0];
             const float dil = (float)(lane - 16), dil2 = -16.0f;
 #pragma unroll
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(256) fwd2d_finalize_kernel(DevGeom g, int firs
 // view kk by warp kk % 8), then thread = pixel walks the batch's views.
 constexpr int kB2VB = 16;   // views per vertex-table batch
 
-template <int EPI>
+template <int EPI, bool VREL>
 __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, int first, int stride, int count,
                                                     const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     __shared__ float V[kB2VB][9][33];
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, 
         const float djt = top_next ? -16.0f : (float)(yoff + 8 - 16), djl = (float)(yoff + min(lane, 8) - 16);
         for (int kb = 0; kb < count; kb += kB2VB) {
             const int nb = min(kB2VB, count - kb);
-            if (g.vrel) {
+            if (VREL) {
                 if (threadIdx.x < 4 * nb) {
                     const int kk = threadIdx.x >> 2, q = threadIdx.x & 3;
                     const float4 vw = __ldg(&g.views[first + (kb + kk) * stride]);
