@@ -90,7 +90,10 @@ typedef struct {
 } ct_views;
 
 /* Validate the description and build per-view tables on the device.
- * The geometry is immutable afterwards and may be shared between streams.
+ * The geometry tables are immutable afterwards.  Fan-beam (2D) forward projections
+ * accumulate into a geometry-owned 64-bit fixed-point buffer (kept zero between
+ * calls), so 2D projections with one geometry must be ordered on one stream (or by
+ * events); cone-beam geometries may be used from several streams at once.
  * Returns CT_EINVAL for inconsistent sizes, CT_EUNSUPPORTED if some voxel's
  * transaxial footprint could span more than 7 channels (kernel window limit). */
 int ct_geom_create(const ct_geom_desc* desc, ct_geom** out);
@@ -101,7 +104,8 @@ const char* ct_last_error(void);
  * Forward projection y = A_v x over the view list v ("one multiplication
  * by A"; system matrix A = separable-footprint SF-TR with A1 amplitude, reading
  * O2 / G1):  a_ij = l_phi * l_theta * F_s(c) * F_t(r).
- * x: [ny][nx][nz]; y: [count][ns][nt], overwritten.  Deterministic, no atomics.
+ * x: [ny][nx][nz]; y: [count][ns][nt], overwritten.  Deterministic: no floating-point
+ * atomics (the 2D tile sums meet in exact 64-bit integer adds, order-independent).
  */
 int ct_fwd_proj(const ct_geom* g, ct_views v, const float* x, float* y, void* stream);
 

@@ -181,7 +181,7 @@ __host__ __device__ constexpr int fwd3d_tcp() { return TC + 2 * kMaxFoot - 2; }
 #define CT_FWD3D_MINB 4   // min resident CTAs per SM for the register budget (A/B: 4 beats 1 by 1.3-1.5x)
 #endif
 #ifndef CT_BACK3D_MINB
-#define CT_BACK3D_MINB 4
+#define CT_BACK3D_MINB 5   // A/B (c3, c5): 5 beats 4 by 2-3% despite a few spilled bytes; 3 is 12% slower
 #endif
 
 template <int TC, int NTP, int NTHR, bool RESID>

@@ -1,10 +1,13 @@
-# A/B timing of 2D tuning variants (same box, same call)
+# A/B timing of 2D tuning variants (same box, same call): projector pair and the c2 bench step
 python -c "import __graft_entry__ as g; g.build()"
-timeout 400 python -m pytest tests -m gpu -x -q -k "fan or c1 or c2 or adjoint or determinism or small or exchange or bb or axis" > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
-for v in "base:" "abs:-DCT_VREL=0"; do
+VARS=${VARS:-"base: S1:-DCT_BACK2D_SPLIT=1 S3:-DCT_BACK2D_SPLIT=3"}
+for v in $VARS; do
   name=${v%%:*}; flags=${v#*:}
-  python -m paper_1402_4381_b200.build --out paper_1402_4381_b200/tune_$name.so $flags > /dev/null
+  [ "$name" = base ] || python -m paper_1402_4381_b200.build --out paper_1402_4381_b200/tune_$name.so $flags > /dev/null
 done
-for r in 1 2; do for name in base abs; do
-  CT_OSLALM_LIB=paper_1402_4381_b200/tune_$name.so python tools/time_proj.py c2 30
+lib() { [ "$1" = base ] && echo paper_1402_4381_b200/libct_oslalm.so || echo paper_1402_4381_b200/tune_$1.so; }
+for r in 1 2; do for v in $VARS; do name=${v%%:*}
+  CT_OSLALM_LIB=$(lib $name) python tools/time_proj.py c2 30
+  CT_OSLALM_LIB=$(lib $name) python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernel_ms']; print('$name', 'bench', f\"{d['value']:.4g}\", {s: round(v['ms_total']/v['launches']*1e3, 1) for s, v in k.items()})"
 done; done

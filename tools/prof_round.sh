@@ -12,8 +12,9 @@ ncu --set full --clock-control none --import-source on -k regex:"fwd2d_tile|fwd2
 python tools/ncu_traffic.py gpurun_out/full_c2.ncu-rep c2 gpurun_out/traffic.json
 for c in c3 c4 c5; do python bench.py --config $c --iters 2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_c2_reference.json 2> gpurun_out/bench_ref.err
-# c5: one full capture of each projector inside an OS-LALM iteration + traffic
+# c5: one full capture of each step kernel inside an OS-LALM iteration + traffic (76 matching
+# launches per step: setup fwd/back, init fwd/back, 24 x (sqs, fwd, back); -s 98 lands in step 2)
 F5="python bench.py --config c5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --iters 1"
 $F5 > gpurun_out/plain_f5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"fwd3d_kernel|back3d_kernel|sqs_update3d" -s 75 -c 3 -o gpurun_out/full_c5 $F5 > gpurun_out/ncu_full5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"fwd3d_kernel|back3d_kernel|sqs_update3d" -s 98 -c 3 -o gpurun_out/full_c5 $F5 > gpurun_out/ncu_full5.log 2>&1
 python tools/ncu_traffic.py gpurun_out/full_c5.ncu-rep c5 gpurun_out/traffic.json
