@@ -46,6 +46,15 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+#ifndef CT_FWD3D_PAIR
+#define CT_FWD3D_PAIR 1   // 32 < nt <= 64: pair-row forward kernel (fwd3d2_kernel)
+#endif
+#ifndef CT_FWD3D2_TC
+#define CT_FWD3D2_TC 22   // A/B (c3, c5): 22 beats 16, 18, 20, 24 by 2-10 %
+#endif
+#ifndef CT_FWD3D2_NW
+#define CT_FWD3D2_NW 4    // warps (row groups) per CTA (8: c3 -1 %, c5 +12 %)
+#endif
 #ifndef CT_FWD3D_TC
 #define CT_FWD3D_TC 24   // channels per 3D forward CTA (A/B: 24 beats 16 and 32 by ~10 %)
 #endif
@@ -335,6 +344,19 @@ static void launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const float* 
     fwd3d_kernel<TC, NTP, 256, RESID><<<grid, 256, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
 }
 
+template <int TC, int NW, bool RESID>
+static void launch_fwd3d2(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs, const float* w,
+                          float scale, const int2* ext, cudaStream_t st) {
+    constexpr size_t smem = fwd3d2_smem<TC, NW>();
+    static bool configured = false;   // per template instance
+    if (!configured) {
+        cudaFuncSetAttribute(fwd3d2_kernel<TC, NW, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    dim3 grid((dg.ns + TC - 1) / TC, v.count);
+    fwd3d2_kernel<TC, NW, RESID><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
+}
+
 template <bool RESID>
 static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, const float* yobs, const float* w,
                       float scale, cudaStream_t st) {
@@ -366,6 +388,8 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32)
             launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
+        else if (dg.nt <= 64 && CT_FWD3D_PAIR)
+            launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st);
         else if (dg.nt <= 64)
             launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
         else

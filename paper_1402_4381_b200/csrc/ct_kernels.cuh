@@ -295,6 +295,188 @@ constexpr size_t fwd3d_smem() {
     return sizeof(float) * (NTHR / NTP) * fwd3d_tcp<TC>() * NTP + sizeof(Foot) * NTHR;
 }
 
+// ---------------------------------------------------------------------------
+// K1 (3D cone), pair-row form for 32 < nt <= 64 (c3, c5): warp = one group of
+// fwd3d_kernel, lane l owns detector rows 2l and 2l + 1.
+// ---------------------------------------------------------------------------
+// Same wedge walk, column trimming and per-group shared accumulators as fwd3d_kernel;
+// the per-column work that does not depend on the row (table loads, branches,
+// accumulator addressing) is shared by two rows, the accumulator update is one float2
+// read-modify-write, and the two rows' slices are formed once: rows 2l, 2l + 1 cover
+// [lo, lo + 2 kz] (voxel units), i.e. slices z0 .. z0 + 4 when kz < 2.
+// Table fields (footprint phase): w[j] = lphi F_s(cA + j) / kz (F_t = overlap / kz folded
+// in); ax.qf = lower edge of row 0 relative to qi; ax.inv_kz holds tzc, the l_theta
+// offset tz(slice qi + m) = m dz_rho + tzc; rows = 32-bit index of (column, slice qi).
+#ifndef CT_FWD3D2_MINB
+#define CT_FWD3D2_MINB 1
+#endif
+
+__device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __restrict__ x, int l, int nz) {
+    const float kz = f.ax.kz;
+    const float lo = fmaf((float)(2 * l), kz, f.ax.qf);
+    const float mid = lo + kz, hi = mid + kz;
+    const int i0 = __float2int_rd(lo);
+    const float z0 = (float)i0;
+    const float tz0 = fmaf(z0, f.ax.dz_rho, f.ax.inv_kz);
+    const int iz0 = i0 + f.ax.qi;
+    const float* xp = x + (f.rows + i0);
+    float xl[5];   // x l_theta of slices z0 .. z0 + 4 (0 outside the volume)
+#pragma unroll
+    for (int m = 0; m < 5; m++) {
+        const float tz = fmaf((float)m, f.ax.dz_rho, tz0);
+        const bool in = (unsigned)(iz0 + m) < (unsigned)nz && (m < 2 || z0 + (float)m < hi);
+        const float v = in ? __ldg(xp + m) : 0.0f;
+        xl[m] = v * sqrt_approx(fmaf(tz, tz, 1.0f));
+    }
+    // row 2l: [lo, mid] meets slices z0 .. z0 + 2 (lo >= z0, kz < 2)
+    const float a1 = fminf(z0 + 1.0f, mid), a2 = fminf(z0 + 2.0f, mid);
+    float A = xl[0] * (a1 - lo);
+    A = fmaf(xl[1], a2 - a1, A);
+    A = fmaf(xl[2], mid - a2, A);
+    // row 2l + 1: [mid, hi], clamped slice boundaries b(m) = clamp(z0 + m, mid, hi)
+    float B = 0.0f, pb = mid;
+#pragma unroll
+    for (int m = 0; m < 5; m++) {
+        const float nb = m < 4 ? fminf(fmaxf(z0 + (float)(m + 1), mid), hi) : hi;
+        B = fmaf(xl[m], nb - pb, B);
+        pb = nb;
+    }
+    return make_float2(A, B);
+}
+
+// General form (kz >= 2, rarely: very fine slices): one row [lo, hi].
+__device__ __forceinline__ float fwd_axial_row(const Foot& f, const float* __restrict__ x, float lo, float hi, int nz) {
+    float A = 0.0f;
+    const int m0 = max(__float2int_rd(lo), -f.ax.qi), m1 = min(__float2int_rd(hi), nz - 1 - f.ax.qi);
+    for (int m = m0; m <= m1; m++) {
+        const float tz = fmaf((float)m, f.ax.dz_rho, f.ax.inv_kz);
+        const float ov = fminf((float)m + 1.0f, hi) - fmaxf((float)m, lo);
+        A = fmaf(__ldg(x + f.rows + m) * sqrt_approx(fmaf(tz, tz, 1.0f)), fmaxf(ov, 0.0f), A);
+    }
+    return A;
+}
+
+template <int TC, int NW, bool RESID>
+__global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom g, int first, int stride,
+                                                                     const float* __restrict__ x, float* __restrict__ out,
+                                                                     const float* __restrict__ yobs,
+                                                                     const float* __restrict__ wts, float scale,
+                                                                     const int2* __restrict__ ext) {
+    constexpr int TCP = fwd3d_tcp<TC>();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* Pacc = reinterpret_cast<float2*>(smem_raw);                                   // [NW][TCP][32]
+    Foot* table = reinterpret_cast<Foot*>(smem_raw + sizeof(float2) * NW * TCP * 32);     // [NW][32]
+    const int c0 = blockIdx.x * TC;
+    const int k = blockIdx.y;
+    const int v = first + k * stride;
+    const float4 vw = g.views[v];
+    const int gi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Foot* tab = table + gi * 32;
+    float2* Pg = Pacc + gi * TCP * 32 + lane;   // lane owns rows 2 lane, 2 lane + 1
+#pragma unroll
+    for (int c = 0; c < TCP; c++) Pg[c * 32] = make_float2(0.0f, 0.0f);
+    const Wedge w = make_wedge(g, vw.x, vw.y, c0, TC);
+    const int nz = g.nz;
+    for (int L = gi; L < w.nlines; L += NW) {
+        int lo, hi;
+        wedge_line(g, w, L, lo, hi);
+        if (ext) {
+            const int2 e = __ldg(&ext[w.rows ? L : g.ny + L]);
+            lo = max(lo, e.x);
+            hi = min(hi, e.y);
+        }
+        if (lo > hi) continue;
+        const int n_in = hi - lo + 1;
+        for (int cb0 = 0; cb0 < n_in; cb0 += 32) {
+            const int q = cb0 + lane;
+            if (q < n_in) {
+                const int u = lo + q;
+                const int ix = w.rows ? u : L, iy = w.rows ? L : u;
+                Foot f;
+                column_footprint(g, vw, g.x0 + ix * g.dx, g.y0 + iy * g.dy, f);
+                if (!(f.n > 0 && f.cA + f.n > c0 && f.cA < c0 + TC)) f.n = 0;   // misses the tile
+#pragma unroll
+                for (int j = 0; j < kMaxFoot; j++) f.w[j] *= f.ax.inv_kz;
+                const float qf = f.ax.qf;
+                f.ax.qf = qf - 0.5f * f.ax.kz - g.rbase * f.ax.kz;
+                f.ax.inv_kz = (0.5f - qf) * f.ax.dz_rho;   // tzc
+                f.rows = (iy * g.nx + ix) * nz + f.ax.qi;
+                tab[lane] = f;
+            }
+            __syncwarp();
+            const int nq = min(32, n_in - cb0);
+            for (int j = 0; j < nq; j += 2) {
+                Foot f0, f1;
+                load_foot(&tab[j], f0);
+                if (j + 1 < nq) load_foot(&tab[j + 1], f1); else f1.n = 0;
+                if (f0.n <= 0 && f1.n <= 0) continue;
+                float2 A0 = make_float2(0.0f, 0.0f), A1 = A0;
+                if (f0.ax.kz < 2.0f && f1.ax.kz < 2.0f) {
+                    if (f0.n > 0) A0 = fwd_axial_pair(f0, x, lane, nz);
+                    if (f1.n > 0) A1 = fwd_axial_pair(f1, x, lane, nz);
+                } else {
+                    if (f0.n > 0) {
+                        const float l0 = fmaf((float)(2 * lane), f0.ax.kz, f0.ax.qf);
+                        A0 = make_float2(fwd_axial_row(f0, x, l0, l0 + f0.ax.kz, nz),
+                                         fwd_axial_row(f0, x, l0 + f0.ax.kz, l0 + 2.0f * f0.ax.kz, nz));
+                    }
+                    if (f1.n > 0) {
+                        const float l1 = fmaf((float)(2 * lane), f1.ax.kz, f1.ax.qf);
+                        A1 = make_float2(fwd_axial_row(f1, x, l1, l1 + f1.ax.kz, nz),
+                                         fwd_axial_row(f1, x, l1 + f1.ax.kz, l1 + 2.0f * f1.ax.kz, nz));
+                    }
+                }
+                if (f0.n > 0) {
+                    float2* p = Pg + (f0.cA - c0 + kMaxFoot - 1) * 32;
+#pragma unroll
+                    for (int jj = 0; jj < kMaxFoot; jj++) {
+                        if (jj >= f0.n) break;
+                        float2 t = p[jj * 32];
+                        t.x = fmaf(f0.w[jj], A0.x, t.x);
+                        t.y = fmaf(f0.w[jj], A0.y, t.y);
+                        p[jj * 32] = t;
+                    }
+                }
+                if (f1.n > 0) {
+                    float2* p = Pg + (f1.cA - c0 + kMaxFoot - 1) * 32;
+#pragma unroll
+                    for (int jj = 0; jj < kMaxFoot; jj++) {
+                        if (jj >= f1.n) break;
+                        float2 t = p[jj * 32];
+                        t.x = fmaf(f1.w[jj], A1.x, t.x);
+                        t.y = fmaf(f1.w[jj], A1.y, t.y);
+                        p[jj * 32] = t;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // fixed-order sum over the NW groups; (c, r) pairs cover the tile, r fastest
+    const float* Pf = reinterpret_cast<const float*>(Pacc);
+    for (int idx = threadIdx.x; idx < TC * 64; idx += NW * 32) {
+        const int c = idx >> 6, rr = idx & 63;
+        if (rr >= g.nt || c0 + c >= g.ns) continue;
+        float s = 0.0f;
+#pragma unroll
+        for (int q = 0; q < NW; q++) s += Pf[(q * TCP + c + kMaxFoot - 1) * 64 + rr];
+        const size_t oi = ((size_t)k * g.ns + c0 + c) * g.nt + rr;
+        if (RESID) {
+            const size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
+            const float yo = yobs ? __ldg(&yobs[gidx]) : 0.0f;
+            out[oi] = scale * __ldg(&wts[gidx]) * (s - yo);
+        } else {
+            out[oi] = s;
+        }
+    }
+}
+
+template <int TC, int NW>
+constexpr size_t fwd3d2_smem() {
+    return sizeof(float2) * NW * fwd3d_tcp<TC>() * 32 + sizeof(Foot) * NW * 32;
+}
+
 // Per image line, the range of columns holding a nonzero voxel (forward-projection
 // trimming): ext[iy] = [min ix, max ix] over row iy, ext[ny + ix] = [min iy, max iy].
 // Integer atomics: order-independent.  Warp = one column (lanes walk z, coalesced).

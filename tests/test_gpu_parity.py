@@ -64,6 +64,12 @@ def geoms_small():
                                 start=11.0)
     gs["axial_offsets"] = GU.geom("cone_axial", nx=14, ny=11, nz=9, dx=1.5, dz=1.1, ns=37, ds=1.9, nt=13, dt=1.3,
                                   na=30, offx=-0.7, offz=0.4, offs=-0.21, offt=0.33)
+    # 32 < nt <= 64: the pair-row forward kernel (odd nt: the last lane's second row is off
+    # the detector); fine slices (kz >= 2): its general axial form
+    gs["axial_rows41"] = GU.geom("cone_axial", nx=11, ny=9, nz=28, dx=0.9766, dz=0.625, ns=23, ds=1.0239, nt=41,
+                                 dt=1.0964, na=20, offz=0.3, offt=0.4)
+    gs["helical_fine_kz"] = GU.geom("cone_helical", nx=10, nz=40, dx=0.9766, dz=0.25, ns=21, ds=1.0239, nt=36,
+                                    dt=1.0964, na=30, turns=2.0, pitch=0.7, start=5.0)
     return gs
 
 

@@ -1,9 +1,12 @@
-# A/B of 3D variants on one box (same call)
+# A/B of 3D variants on one box (same call): VARS="name:-DFLAG=V ..." (base = default build)
 python -c "import __graft_entry__ as g; g.build()"
-for v in "base:" "F3:-DCT_FWD3D_MINB=3" "F5:-DCT_FWD3D_MINB=5" "B3:-DCT_BACK3D_MINB=3" "B5:-DCT_BACK3D_MINB=5"; do
-  name=${v%%:*}; flags=${v#*:}
-  python -m paper_1402_4381_b200.build --out paper_1402_4381_b200/tune_$name.so $flags > /dev/null
+VARS=${VARS:-"base: P0:-DCT_FWD3D_PAIR=0"}
+CFGS=${CFGS:-"c3 c5"}
+for v in $VARS; do
+  name=${v%%:*}; flags=${v#*:}; flags=${flags//_-D/ -D}
+  [ "$name" = base ] || python -m paper_1402_4381_b200.build --out paper_1402_4381_b200/tune_$name.so $flags > /dev/null
 done
-for c in c3 c5; do for name in base F3 F5 B3 B5; do
-  CT_OSLALM_LIB=paper_1402_4381_b200/tune_$name.so python tools/time_proj.py $c 3
+lib() { [ "$1" = base ] && echo paper_1402_4381_b200/libct_oslalm.so || echo paper_1402_4381_b200/tune_$1.so; }
+for c in $CFGS; do for v in $VARS; do name=${v%%:*}
+  CT_OSLALM_LIB=$(lib $name) python tools/time_proj.py $c 3
 done; done

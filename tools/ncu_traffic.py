@@ -14,8 +14,8 @@ import sys
 from collections import defaultdict
 
 STEPS = {   # bench step -> kernel-name prefixes
-    "fwd_resid": ("fwd2d_tile_kernel", "fwd2d_finalize_kernel", "fwd3d_kernel"),
-    "back_gupd": ("back2d_kernel", "back3d_kernel", "back3d_chunk_kernel"),
+    "fwd_resid": ("fwd2d_tile_kernel", "fwd2d_finalize_kernel", "fwd3d_kernel", "fwd3d2_kernel"),
+    "back_gupd": ("back2d_kernel", "back3d_kernel"),
     "sqs_update": ("sqs_update_kernel", "sqs_update2d_kernel", "sqs_update3d_kernel"),
 }
 

@@ -16,5 +16,5 @@ python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_c2_refe
 # launches per step: setup fwd/back, init fwd/back, 24 x (sqs, fwd, back); -s 98 lands in step 2)
 F5="python bench.py --config c5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --iters 1"
 $F5 > gpurun_out/plain_f5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"fwd3d_kernel|back3d_kernel|sqs_update3d" -s 98 -c 3 -o gpurun_out/full_c5 $F5 > gpurun_out/ncu_full5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"fwd3d_kernel|fwd3d2_kernel|back3d_kernel|sqs_update3d" -s 98 -c 3 -o gpurun_out/full_c5 $F5 > gpurun_out/ncu_full5.log 2>&1
 python tools/ncu_traffic.py gpurun_out/full_c5.ncu-rep c5 gpurun_out/traffic.json
