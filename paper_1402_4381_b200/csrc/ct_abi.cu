@@ -47,7 +47,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 #ifndef CT_FWD3D_PAIR
-#define CT_FWD3D_PAIR 1   // 32 < nt <= 64: pair-row forward kernel (fwd3d2_kernel)
+#define CT_FWD3D_PAIR 1   // nt <= 64: pair-row forward kernel (fwd3d2_kernel); 0: fwd3d_kernel
 #endif
 #ifndef CT_FWD3D2_TC
 #define CT_FWD3D2_TC 22   // A/B (c3, c5): 22 beats 16, 18, 20, 24 by 2-10 %
@@ -344,17 +344,17 @@ static void launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const float* 
     fwd3d_kernel<TC, NTP, 256, RESID><<<grid, 256, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
 }
 
-template <int TC, int NW, bool RESID>
+template <int TC, int NW, int H, bool RESID>
 static void launch_fwd3d2(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs, const float* w,
                           float scale, const int2* ext, cudaStream_t st) {
     constexpr size_t smem = fwd3d2_smem<TC, NW>();
     static bool configured = false;   // per template instance
     if (!configured) {
-        cudaFuncSetAttribute(fwd3d2_kernel<TC, NW, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(fwd3d2_kernel<TC, NW, H, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     dim3 grid((dg.ns + TC - 1) / TC, v.count);
-    fwd3d2_kernel<TC, NW, RESID><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
+    fwd3d2_kernel<TC, NW, H, RESID><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
 }
 
 template <bool RESID>
@@ -386,10 +386,12 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         fwd3d_extent_kernel<<<(dg.nx * dg.ny + 7) / 8, 256, 0, st>>>(dg, x, g->ext3d);
         constexpr int TC = CT_FWD3D_TC;
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
-        if (dg.nt <= 32)
+        if (dg.nt <= 32 && CT_FWD3D_PAIR)
+            launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 2, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st);
+        else if (dg.nt <= 32)
             launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
         else if (dg.nt <= 64 && CT_FWD3D_PAIR)
-            launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st);
+            launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 1, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st);
         else if (dg.nt <= 64)
             launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
         else

@@ -296,8 +296,10 @@ constexpr size_t fwd3d_smem() {
 }
 
 // ---------------------------------------------------------------------------
-// K1 (3D cone), pair-row form for 32 < nt <= 64 (c3, c5): warp = one group of
-// fwd3d_kernel, lane l owns detector rows 2l and 2l + 1.
+// K1 (3D cone), pair-row form for nt <= 64: lane l of a column's LW = 32 / H lanes owns
+// detector rows 2l and 2l + 1.  H = 1 (32 < nt <= 64, c3 / c5): warp = one group of
+// fwd3d_kernel; H = 2 (nt <= 32, c4): each half-warp is a group with its own accumulator,
+// and both halves walk the same line (two columns per half per step).
 // ---------------------------------------------------------------------------
 // Same wedge walk, column trimming and per-group shared accumulators as fwd3d_kernel;
 // the per-column work that does not depend on the row (table loads, branches,
@@ -356,25 +358,27 @@ __device__ __forceinline__ float fwd_axial_row(const Foot& f, const float* __res
     return A;
 }
 
-template <int TC, int NW, bool RESID>
+template <int TC, int NW, int H, bool RESID>
 __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom g, int first, int stride,
                                                                      const float* __restrict__ x, float* __restrict__ out,
                                                                      const float* __restrict__ yobs,
                                                                      const float* __restrict__ wts, float scale,
                                                                      const int2* __restrict__ ext) {
     constexpr int TCP = fwd3d_tcp<TC>();
+    constexpr int LW = 32 / H;   // lanes per column (row pairs)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2* Pacc = reinterpret_cast<float2*>(smem_raw);                                   // [NW][TCP][32]
+    float2* Pacc = reinterpret_cast<float2*>(smem_raw);                                   // [NW][H][TCP][LW]
     Foot* table = reinterpret_cast<Foot*>(smem_raw + sizeof(float2) * NW * TCP * 32);     // [NW][32]
     const int c0 = blockIdx.x * TC;
     const int k = blockIdx.y;
     const int v = first + k * stride;
     const float4 vw = g.views[v];
     const int gi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hf = lane / LW, ll = lane % LW;   // half (column stream) and row pair
     Foot* tab = table + gi * 32;
-    float2* Pg = Pacc + gi * TCP * 32 + lane;   // lane owns rows 2 lane, 2 lane + 1
+    float2* Pg = Pacc + (gi * H + hf) * TCP * LW + ll;   // rows 2 ll, 2 ll + 1 of stream hf
 #pragma unroll
-    for (int c = 0; c < TCP; c++) Pg[c * 32] = make_float2(0.0f, 0.0f);
+    for (int c = 0; c < TCP; c++) Pg[c * LW] = make_float2(0.0f, 0.0f);
     const Wedge w = make_wedge(g, vw.x, vw.y, c0, TC);
     const int nz = g.nz;
     for (int L = gi; L < w.nlines; L += NW) {
@@ -405,47 +409,48 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
             }
             __syncwarp();
             const int nq = min(32, n_in - cb0);
-            for (int j = 0; j < nq; j += 2) {
+            for (int j0 = 0; j0 < nq; j0 += 2 * H) {
+                const int j = j0 + 2 * hf;   // this stream's two columns
                 Foot f0, f1;
-                load_foot(&tab[j], f0);
+                if (j < nq) load_foot(&tab[j], f0); else f0.n = 0;
                 if (j + 1 < nq) load_foot(&tab[j + 1], f1); else f1.n = 0;
                 if (f0.n <= 0 && f1.n <= 0) continue;
                 float2 A0 = make_float2(0.0f, 0.0f), A1 = A0;
                 if (f0.ax.kz < 2.0f && f1.ax.kz < 2.0f) {
-                    if (f0.n > 0) A0 = fwd_axial_pair(f0, x, lane, nz);
-                    if (f1.n > 0) A1 = fwd_axial_pair(f1, x, lane, nz);
+                    if (f0.n > 0) A0 = fwd_axial_pair(f0, x, ll, nz);
+                    if (f1.n > 0) A1 = fwd_axial_pair(f1, x, ll, nz);
                 } else {
                     if (f0.n > 0) {
-                        const float l0 = fmaf((float)(2 * lane), f0.ax.kz, f0.ax.qf);
+                        const float l0 = fmaf((float)(2 * ll), f0.ax.kz, f0.ax.qf);
                         A0 = make_float2(fwd_axial_row(f0, x, l0, l0 + f0.ax.kz, nz),
                                          fwd_axial_row(f0, x, l0 + f0.ax.kz, l0 + 2.0f * f0.ax.kz, nz));
                     }
                     if (f1.n > 0) {
-                        const float l1 = fmaf((float)(2 * lane), f1.ax.kz, f1.ax.qf);
+                        const float l1 = fmaf((float)(2 * ll), f1.ax.kz, f1.ax.qf);
                         A1 = make_float2(fwd_axial_row(f1, x, l1, l1 + f1.ax.kz, nz),
                                          fwd_axial_row(f1, x, l1 + f1.ax.kz, l1 + 2.0f * f1.ax.kz, nz));
                     }
                 }
                 if (f0.n > 0) {
-                    float2* p = Pg + (f0.cA - c0 + kMaxFoot - 1) * 32;
+                    float2* p = Pg + (f0.cA - c0 + kMaxFoot - 1) * LW;
 #pragma unroll
                     for (int jj = 0; jj < kMaxFoot; jj++) {
                         if (jj >= f0.n) break;
-                        float2 t = p[jj * 32];
+                        float2 t = p[jj * LW];
                         t.x = fmaf(f0.w[jj], A0.x, t.x);
                         t.y = fmaf(f0.w[jj], A0.y, t.y);
-                        p[jj * 32] = t;
+                        p[jj * LW] = t;
                     }
                 }
                 if (f1.n > 0) {
-                    float2* p = Pg + (f1.cA - c0 + kMaxFoot - 1) * 32;
+                    float2* p = Pg + (f1.cA - c0 + kMaxFoot - 1) * LW;
 #pragma unroll
                     for (int jj = 0; jj < kMaxFoot; jj++) {
                         if (jj >= f1.n) break;
-                        float2 t = p[jj * 32];
+                        float2 t = p[jj * LW];
                         t.x = fmaf(f1.w[jj], A1.x, t.x);
                         t.y = fmaf(f1.w[jj], A1.y, t.y);
-                        p[jj * 32] = t;
+                        p[jj * LW] = t;
                     }
                 }
             }
@@ -453,14 +458,15 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
         }
     }
     __syncthreads();
-    // fixed-order sum over the NW groups; (c, r) pairs cover the tile, r fastest
+    // fixed-order sum over the NW * H groups; (c, r) pairs cover the tile, r fastest
+    constexpr int RW = 2 * LW;   // rows per group
     const float* Pf = reinterpret_cast<const float*>(Pacc);
-    for (int idx = threadIdx.x; idx < TC * 64; idx += NW * 32) {
-        const int c = idx >> 6, rr = idx & 63;
+    for (int idx = threadIdx.x; idx < TC * RW; idx += NW * 32) {
+        const int c = idx / RW, rr = idx % RW;
         if (rr >= g.nt || c0 + c >= g.ns) continue;
         float s = 0.0f;
 #pragma unroll
-        for (int q = 0; q < NW; q++) s += Pf[(q * TCP + c + kMaxFoot - 1) * 64 + rr];
+        for (int q = 0; q < NW * H; q++) s += Pf[(q * TCP + c + kMaxFoot - 1) * RW + rr];
         const size_t oi = ((size_t)k * g.ns + c0 + c) * g.nt + rr;
         if (RESID) {
             const size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
