@@ -188,6 +188,26 @@ constexpr int kF2T = 32;      // tile edge (pixels)
 constexpr int kF2VC = 8;      // views per CTA
 constexpr float kFix = 4294967296.0f;   // 2^32
 
+// NR rounds of the forward tile (NR = warp max of the lanes' bin counts n): round j adds
+// lane's bin cA + j.  Bins j >= n add exactly 0 (Fn = Fp = mass); the last round needs no CDF
+// (every lane is at or past its right edge).  The CDF is evaluated on every lane and
+// selected, so the rounds are branch-free.
+template <int NR>
+__device__ __forceinline__ void fwd_rounds(float* bp, const Trap2& T, float koff, int n, bool act, float lx) {
+    float Fp = 0.0f;   // unclipped: F = 0 at the left edge of bin cA
+#pragma unroll
+    for (int j = 0; j < NR; j++) {
+        float Fn = T.mass;
+        if (j + 1 < NR) {
+            const float Fv = T.F(__fadd_rn(T.u0, koff + (float)(j + 1)));
+            Fn = (j + 1 < n) ? Fv : T.mass;
+        }
+        if (act) bp[j] += lx * __fsub_rn(Fn, Fp);
+        Fp = Fn;
+        __syncwarp();   // round j's stores are visible to round j + 1's loads
+    }
+}
+
 template <bool VREL>
 __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom g, int first, int stride, int count,
                                                         const float* __restrict__ x,
@@ -284,17 +304,16 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
                 // u = u0 + k rounds exactly as in the back-projector (edges left of channel 0
                 // only feed dropped bins)
                 const float koff = (float)(f.cA - T.c0);
-                float Fp = 0.0f;   // unclipped: F = 0 at the left edge of bin cA
-#pragma unroll
-                for (int j = 0; j < kMaxFoot; j++) {
-                    if (j >= nmax) break;
-                    // bins j >= n add exactly 0 (Fn = Fp = mass) to distinct addresses
-                    // the warp's last round needs no CDF (every lane is at or past its right edge)
-                    float Fn = T.mass;
-                    if (j + 1 < nmax) Fn = (j + 1 < n) ? T.F(__fadd_rn(T.u0, koff + (float)(j + 1))) : T.mass;
-                    if (act) bp[j] += lx * __fsub_rn(Fn, Fp);
-                    Fp = Fn;
-                    __syncwarp();   // round j's stores are visible to round j + 1's loads
+                // warp-uniform round count: straight-line rounds, no per-round branches
+                switch (nmax) {
+                    case 1: fwd_rounds<1>(bp, T, koff, n, act, lx); break;
+                    case 2: fwd_rounds<2>(bp, T, koff, n, act, lx); break;
+                    case 3: fwd_rounds<3>(bp, T, koff, n, act, lx); break;
+                    case 4: fwd_rounds<4>(bp, T, koff, n, act, lx); break;
+                    case 5: fwd_rounds<5>(bp, T, koff, n, act, lx); break;
+                    case 6: fwd_rounds<6>(bp, T, koff, n, act, lx); break;
+                    case 7: fwd_rounds<7>(bp, T, koff, n, act, lx); break;
+                    default: fwd_rounds<kMaxFoot>(bp, T, koff, n, act, lx); break;
                 }
             }
         }

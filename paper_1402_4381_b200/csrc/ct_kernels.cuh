@@ -310,7 +310,7 @@ constexpr size_t fwd3d_smem() {
 // in); ax.qf = lower edge of row 0 relative to qi; ax.inv_kz holds tzc, the l_theta
 // offset tz(slice qi + m) = m dz_rho + tzc; rows = 32-bit index of (column, slice qi).
 #ifndef CT_FWD3D2_MINB
-#define CT_FWD3D2_MINB 1
+#define CT_FWD3D2_MINB 5   // 5 CTAs of 4 warps per SM (A/B: c3 2.32 -> 2.12, c5 15.2 -> 13.3 ms vs 4)
 #endif
 
 __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __restrict__ x, int l, int nz) {
