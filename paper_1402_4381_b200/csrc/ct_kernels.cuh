@@ -672,7 +672,7 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 constexpr int kBackRows = 128;   // >= nt (validated)
 
 __host__ __device__ constexpr size_t back3d_smem_fixed() {
-    return sizeof(Foot) * 8 * 32 + sizeof(float) * 8 * kBackRows + sizeof(float) * 8 * (kBackRows + 4);
+    return sizeof(Foot) * 8 * 32 + sizeof(float2) * 8 * (kBackRows + 4);
 }
 
 // Two filtered detector rows (float2) of one view: q = sum_{c < n} w[c] y[c][r..r+1].
@@ -703,9 +703,8 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                                                     const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     Foot* table = reinterpret_cast<Foot*>(sm_raw);
-    float* Qs = reinterpret_cast<float*>(sm_raw + sizeof(Foot) * 8 * 32);
-    float* Ps = Qs + 8 * kBackRows;
-    float* ACC = Ps + 8 * (kBackRows + 4);
+    float2* QPs = reinterpret_cast<float2*>(sm_raw + sizeof(Foot) * 8 * 32);
+    float* ACC = reinterpret_cast<float*>(QPs + 8 * (kBackRows + 4));
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ix = blockIdx.x * 4 + (wid & 3);
     const int iy = blockIdx.y * 2 + (wid >> 2);
@@ -713,8 +712,9 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
     const int nt = g.nt, ns = g.ns, nz = g.nz;
     const int col = ((colok ? iy : 0) * g.nx + (colok ? ix : 0)) * nz;
     Foot* tab = table + wid * 32;
-    float* Q = Qs + wid * kBackRows;
-    float* PF = Ps + wid * (kBackRows + 4);
+    // QP[k] = (PF[k], Q(r_lo + k)): prefix sum of the filtered rows below row r_lo + k and the
+    // row itself (one 8-byte load per slice edge); QP[nr] = (total, 0)
+    float2* QP = QPs + wid * (kBackRows + 4);
     float* acc = ACC + wid * nz;
     bool any = false;
     for (int iz = lane; iz < nz; iz += 32) {
@@ -764,11 +764,8 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                         if (lane >= o) inc += t;
                     }
                     const float ex = inc - s2;
-                    Q[2 * lane] = q0;
-                    Q[2 * lane + 1] = q1;
-                    PF[2 * lane] = ex;
-                    PF[2 * lane + 1] = ex + q0;
-                    if (lane == 31) PF[64] = inc;
+                    reinterpret_cast<float4*>(QP)[lane] = make_float4(ex, q0, ex + q0, q1);
+                    if (lane == 31) QP[64] = make_float2(inc, 0.0f);
                 } else if (nt == 32) {
                     // 32-row detector: one pass over every row, one row per lane
                     const float* yr = y + ((vb + j) * ns + f.cA) * 32 + lane;
@@ -782,9 +779,8 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                         const float t = __shfl_up_sync(0xffffffffu, inc, o);
                         if (lane >= o) inc += t;
                     }
-                    Q[lane] = q0;
-                    PF[lane] = inc - q0;
-                    if (lane == 31) PF[32] = inc;
+                    QP[lane] = make_float2(inc - q0, q0);
+                    if (lane == 31) QP[32] = make_float2(inc, 0.0f);
                 } else {
                     // rows met by the active slices, from an even row (float2 loads)
                     const float zq = (float)(za - f.ax.qi) - f.ax.qf;
@@ -824,13 +820,9 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                         }
                         const float ex = carry + inc - s2;
                         if (inr) {
-                            Q[p] = q0;
-                            PF[p] = ex;
-                            if (even) {
-                                Q[p + 1] = q1;
-                                PF[p + 1] = ex + q0;
-                            }
-                            if (p + RPL >= nr) PF[p + RPL] = ex + s2;   // upper edge of the last row
+                            QP[p] = make_float2(ex, q0);
+                            if (even) QP[p + 1] = make_float2(ex + q0, q1);
+                            if (p + RPL >= nr) QP[p + RPL] = make_float2(ex + s2, 0.0f);   // upper edge of the last row
                         }
                         carry += __shfl_sync(0xffffffffu, inc, 31);
                     }
@@ -841,15 +833,19 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 //     the slice's extent on the detector, PF(u(iz + 1)) - PF(u(iz))
                 //     Lanes evaluate PF at consecutive slice edges; slice iz takes its upper edge
                 //     from the next lane, so a pass of 32 edges completes 31 slices.
-                const float fnr = (float)nr, ubl = ub - (float)r_lo;
+                //     (u = nr, the top edge, reads QP[nr] = (total, 0); l_theta of slice iz from
+                //     its lower edge's zi: tz = (zi + 1/2) dz / rho)
+                const float fnr = (float)nr, ubl = ub - (float)r_lo, hdz = 0.5f * f.ax.dz_rho;
                 for (int s0 = 0; s0 < nzs; s0 += 31) {
                     const int iz = za + s0 + lane;   // lower edge of slice iz (lane 31: upper edge of iz - 1)
                     const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
                     const float u = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubl), 0.0f), fnr);
-                    const int k = min(__float2int_rd(u), nr - 1);
-                    const float pf = fmaf(u - (float)k, Q[k], PF[k]);
+                    const int k = __float2int_rd(u);
+                    const float2 qp = QP[k];
+                    const float pf = fmaf(u - (float)k, qp.y, qp.x);
                     const float up = __shfl_down_sync(0xffffffffu, pf, 1);
-                    if (lane < 31 && s0 + lane < nzs) acc[iz] = fmaf(ltheta(f.ax, iz), up - pf, acc[iz]);
+                    const float tz = fmaf(zi, f.ax.dz_rho, hdz);
+                    if (lane < min(nzs - s0, 31)) acc[iz] = fmaf(sqrt_approx(fmaf(tz, tz, 1.0f)), up - pf, acc[iz]);
                 }
                 __syncwarp();
             }
