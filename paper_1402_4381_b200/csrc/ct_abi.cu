@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -332,29 +333,43 @@ static int check_views(const ct_geom* g, ct_views v) {
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
+// Dynamic shared memory above 48 KB must be opted into per kernel and per device: remember
+// the largest size set for each (kernel, device) pair (calls may come from several threads
+// and devices of one process).
+static cudaError_t ensure_dyn_smem(const void* func, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{func, dev}];
+    if (have >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
 template <int TC, int NTP, bool RESID>
-static void launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const float* x, float* out, const float* yobs,
-                         const float* w, float scale, const int2* ext, cudaStream_t st) {
+static cudaError_t launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const float* x, float* out, const float* yobs,
+                                const float* w, float scale, const int2* ext, cudaStream_t st) {
     constexpr size_t smem = fwd3d_smem<TC, NTP, 256>();
-    static bool configured = false;   // per template instance
-    if (!configured) {
-        cudaFuncSetAttribute(fwd3d_kernel<TC, NTP, 256, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    cudaError_t e = ensure_dyn_smem((const void*)fwd3d_kernel<TC, NTP, 256, RESID>, smem);
+    if (e != cudaSuccess) return e;
     fwd3d_kernel<TC, NTP, 256, RESID><<<grid, 256, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
+    return cudaSuccess;
 }
 
 template <int TC, int NW, int H, bool RESID>
-static void launch_fwd3d2(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs, const float* w,
-                          float scale, const int2* ext, cudaStream_t st) {
+static cudaError_t launch_fwd3d2(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
+                                 const float* w, float scale, const int2* ext, cudaStream_t st) {
     constexpr size_t smem = fwd3d2_smem<TC, NW>();
-    static bool configured = false;   // per template instance
-    if (!configured) {
-        cudaFuncSetAttribute(fwd3d2_kernel<TC, NW, H, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    cudaError_t e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, RESID>, smem);
+    if (e != cudaSuccess) return e;
     dim3 grid((dg.ns + TC - 1) / TC, v.count);
     fwd3d2_kernel<TC, NW, H, RESID><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
+    return cudaSuccess;
 }
 
 template <bool RESID>
@@ -364,12 +379,8 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
     const DevGeom& dg = g->dg;
     if (dg.kind == CT_FAN2D) {
         const size_t smem = sizeof(float) * 8 * dg.fpar * dg.fspan;
-        static size_t configured = 0;
-        if (smem > 48 * 1024 && configured < smem) {
-            cudaFuncSetAttribute(fwd2d_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaFuncSetAttribute(fwd2d_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured = smem;
-        }
+        CT_CUDA(ensure_dyn_smem(dg.vrel ? (const void*)fwd2d_tile_kernel<true> : (const void*)fwd2d_tile_kernel<false>,
+                                smem));
         dim3 grid((dg.nx + kF2T - 1) / kF2T, (dg.ny + kF2T - 1) / kF2T, (v.count + kF2VC - 1) / kF2VC);
         if (dg.vrel)
             CT_CUDA(launch_pdl(fwd2d_tile_kernel<true>, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
@@ -385,17 +396,24 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         fwd3d_extent_init<<<(next + 255) / 256, 256, 0, st>>>(g->ext3d, next);
         fwd3d_extent_kernel<<<(dg.nx * dg.ny + 7) / 8, 256, 0, st>>>(dg, x, g->ext3d);
         constexpr int TC = CT_FWD3D_TC;
+        if (v.count > 65535) {   // gridDim.y limit: launch the view list in chunks
+            for (int c0 = 0; c0 < v.count; c0 += 65535) {
+                const ct_views vc{v.first + c0 * v.stride, v.stride, std::min(65535, v.count - c0)};
+                if (int e = launch_fwd<RESID>(g, vc, x, out + (size_t)c0 * dg.ns * dg.nt, yobs, w, scale, st)) return e;
+            }
+            return CT_OK;
+        }
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32 && CT_FWD3D_PAIR)
-            launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 2, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st);
+            CT_CUDA((launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 2, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st)));
         else if (dg.nt <= 32)
-            launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
+            CT_CUDA((launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st)));
         else if (dg.nt <= 64 && CT_FWD3D_PAIR)
-            launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 1, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st);
+            CT_CUDA((launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 1, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st)));
         else if (dg.nt <= 64)
-            launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
+            CT_CUDA((launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st)));
         else
-            launch_fwd3d<TC, 128, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st);
+            CT_CUDA((launch_fwd3d<TC, 128, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st)));
         CT_LAUNCHED(2);
     }
     CT_LAUNCHED(1);
@@ -430,11 +448,7 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
             CT_CUDA(launch_pdl(back2d_kernel<EPI, false>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
     else {
         const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * (size_t)dg.nz;
-        static int configured[4] = {0, 0, 0, 0};
-        if (smem > 48 * 1024 && configured[EPI] < (int)smem) {
-            cudaFuncSetAttribute(back3d_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured[EPI] = (int)smem;
-        }
+        CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI>, smem));
         back3d_kernel<EPI><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
     }
     CT_LAUNCHED(1);
@@ -534,7 +548,7 @@ extern "C" int ct_fbp(const ct_geom* g, const float* y, float* x, void* scratch,
     const DevGeom& dg = g->dg;
     float* q = (float*)scratch;
     const size_t smem = sizeof(float) * 2 * dg.ns;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fbp_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    CT_CUDA(ensure_dyn_smem((const void*)fbp_filter_kernel, smem));
     fbp_filter_kernel<<<dim3(dg.na, dg.nt), 256, smem, st>>>(dg, y, q);
     fbp_back_kernel<<<nblk(n_vox(g)), 256, 0, st>>>(dg, q, x, dg.na);
     CT_LAUNCHED(2);

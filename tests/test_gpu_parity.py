@@ -605,3 +605,18 @@ def test_zslab_path_single_rank(ct, O):
     assert np.array_equal(log[:, 2], logo[:, 2])
     with pytest.raises(ct.CTError, match="EUNSUPPORTED"):
         ct.OSLALM(geo, 4, beta=base.beta, delta=base.delta, nbr=26, inner="fista", n_inner=2)
+
+
+def test_fwd_more_views_than_grid_rows(ct, O):
+    """A 3D forward projection of > 65535 views (the CUDA grid's y limit) is launched in view
+    chunks: every view matches the oracle (tiny image and detector, 70000-view helix)."""
+    g = GU.geom("cone_helical", nx=4, nz=6, dx=0.9766, dz=0.625, ns=6, ds=1.0239, nt=4, dt=1.0964, na=70000,
+                turns=20.0, pitch=1.0)
+    geo = ct.Geometry(g)
+    x = rand_image(g, 5, geo.img_shape)
+    yg = geo.fwd(torch.from_numpy(x).cuda()).cpu().numpy()
+    yo = O.fwd(g, I.to_oracle_image(x), 0, 1, g["na"])
+    assert rel_l2(I.to_oracle_sino(yg), yo, "fwd 70000 views") <= 1e-4
+    tail = (65530, 1, 12)   # a view list straddling the chunk boundary
+    yt = geo.fwd(torch.from_numpy(x).cuda(), tail).cpu().numpy()
+    assert np.array_equal(yt, yg[65530:65542])
