@@ -95,7 +95,10 @@ typedef struct {
  * calls), so 2D projections with one geometry must be ordered on one stream (or by
  * events); cone-beam geometries may be used from several streams at once.
  * Returns CT_EINVAL for inconsistent sizes, CT_EUNSUPPORTED if some voxel's
- * transaxial footprint could span more than 7 channels (kernel window limit). */
+ * transaxial footprint could span more than 7 channels (kernel window limit), or,
+ * for fan beams, if consecutive pixels can be less than 1/8 channel apart on the
+ * detector (forward tile kernel's lane-parity buffers) or a 32x32 pixel tile's
+ * channel span does not fit its shared-memory buffers. */
 int ct_geom_create(const ct_geom_desc* desc, ct_geom** out);
 void ct_geom_destroy(ct_geom* g);
 const char* ct_last_error(void);

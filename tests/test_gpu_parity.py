@@ -620,3 +620,41 @@ def test_fwd_more_views_than_grid_rows(ct, O):
     tail = (65530, 1, 12)   # a view list straddling the chunk boundary
     yt = geo.fwd(torch.from_numpy(x).cuda(), tail).cpu().numpy()
     assert np.array_equal(yt, yg[65530:65542])
+
+
+DEGENERATE = {
+    # one slice, one detector row: the cone path reduces to a single-row fan
+    "axial_nz1_nt1": GU.geom("cone_axial", nx=9, nz=1, dx=1.2, dz=1.0, ns=17, ds=1.7, nt=1, dt=1.1, na=14),
+    # one slice seen by many rows (kz small) and a thick-slice stack (one row per slice pair)
+    "axial_nz1_nt64": GU.geom("cone_axial", nx=7, nz=1, dx=1.0, dz=3.0, ns=13, ds=1.4, nt=64, dt=0.3, na=10),
+    "axial_nz3_nt2": GU.geom("cone_axial", nx=8, ny=5, nz=3, dx=1.0, dz=0.4, ns=11, ds=1.6, nt=2, dt=2.0, na=12),
+    # helical with two slices and two rows; one-channel detector
+    "helical_nz2_nt2": GU.geom("cone_helical", nx=6, nz=2, dx=1.0, dz=0.7, ns=9, ds=1.5, nt=2, dt=1.0, na=40,
+                               turns=2.0, pitch=1.0),
+    "fan_ns1": GU.geom("fan2d", nx=6, dx=0.8, ns=1, ds=4.0, na=25),
+    "axial_ns1": GU.geom("cone_axial", nx=5, nz=4, dx=0.8, dz=0.8, ns=1, ds=9.0, nt=3, dt=1.0, na=16),
+}
+
+
+@pytest.mark.parametrize("name", list(DEGENERATE))
+def test_degenerate_shapes(ct, O, name):
+    """Single slice / row / channel geometries and tiny volumes: forward and back match the
+    oracle and stay adjoint (every kernel's tile is almost entirely ragged)."""
+    g = DEGENERATE[name]
+    geo = ct.Geometry(g)
+    x = rand_image(g, 11, geo.img_shape)
+    yg = geo.fwd(torch.from_numpy(x).cuda()).cpu().numpy()
+    yo = O.fwd(g, I.to_oracle_image(x), 0, 1, g["na"])
+    assert np.isfinite(yg).all()
+    assert rel_l2(I.to_oracle_sino(yg), yo, f"fwd degenerate {name}") <= 1e-4
+    p = np.random.default_rng(12).random(yg.shape).astype(np.float32)
+    bg = geo.back(torch.from_numpy(p).cuda()).cpu().numpy()
+    bo = O.back(g, I.to_oracle_sino(p), 0, 1, g["na"])
+    assert rel_l2(I.to_oracle_image(bg), bo, f"back degenerate {name}") <= 1e-4
+
+
+def test_fan_pixel_much_finer_than_channel_is_rejected(ct):
+    """The fan forward tile kernel needs consecutive pixels >= 1/8 channel apart (lane-parity
+    buffers): a finer grid is refused at create with CT_EUNSUPPORTED, not run."""
+    with pytest.raises(ct.CTError, match="CT_EUNSUPPORTED"):
+        ct.Geometry(GU.geom("fan2d", nx=6, dx=0.8, ns=1, ds=9.0, na=25))
