@@ -128,7 +128,9 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _ptr(t, dtype, name):
+def _ptr(t, dtype, name, numel=None):
+    """Device pointer of a contiguous CUDA tensor; `numel`: the element count the call reads or
+    writes through it (the C ABI takes bare pointers, so sizes are checked here)."""
     if t is None:
         return None
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
@@ -137,7 +139,25 @@ def _ptr(t, dtype, name):
         raise CTError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise CTError(f"{name} must be contiguous")
+    if numel is not None and t.numel() < numel:
+        raise CTError(f"{name} has {t.numel()} elements, the call needs {numel}")
     return ctypes.c_void_p(t.data_ptr())
+
+
+# element counts per geometry handle (image, cells per view, views), for the size checks
+_SIZES = {}
+
+
+def _img(h):
+    return _SIZES[h.value][0] if h.value in _SIZES else None
+
+
+def _cells(h, count):
+    return _SIZES[h.value][1] * count if h.value in _SIZES else None
+
+
+def _na(h):
+    return _SIZES[h.value][2] if h.value in _SIZES else 0
 
 
 # ---------------------------------------------------------------------------
@@ -156,16 +176,20 @@ def ct_geom_create(geom: dict, device: int = 0):
     d.device = int(device)
     h = ctypes.c_void_p()
     _check(L.ct_geom_create(ctypes.byref(d), ctypes.byref(h)))
+    is2d = geom["kind"] == "fan2d"
+    _SIZES[h.value] = (int(geom["nx"]) * int(geom["ny"]) * (1 if is2d else int(geom["nz"])),
+                       int(geom["ns"]) * (1 if is2d else int(geom["nt"])), int(geom["na"]))
     return h
 
 
 def ct_geom_destroy(h):
+    _SIZES.pop(h.value, None)
     load().ct_geom_destroy(h)
 
 
 def ct_fwd_proj(h, views, x, y, stream=None):
-    _check(load().ct_fwd_proj(h, ct_views(*views), _ptr(x, torch.float32, "x"), _ptr(y, torch.float32, "y"),
-                              _stream(stream)))
+    _check(load().ct_fwd_proj(h, ct_views(*views), _ptr(x, torch.float32, "x", _img(h)),
+                              _ptr(y, torch.float32, "y", _cells(h, views[2])), _stream(stream)))
 
 
 def ct_peak_l2_read(device=0, mib=48, reps=200):
@@ -182,13 +206,13 @@ def ct_fbp_scratch_bytes(h):
 
 
 def ct_fbp(h, y, x, scratch, stream=None):
-    _check(load().ct_fbp(h, _ptr(y, torch.float32, "y"), _ptr(x, torch.float32, "x"),
-                         ctypes.c_void_p(scratch.data_ptr()), _stream(stream)))
+    _check(load().ct_fbp(h, _ptr(y, torch.float32, "y", _cells(h, _na(h))), _ptr(x, torch.float32, "x", _img(h)),
+                         _ptr(scratch, torch.uint8, "scratch", ct_fbp_scratch_bytes(h)), _stream(stream)))
 
 
 def ct_back_proj(h, views, y, x, accumulate=False, stream=None):
-    _check(load().ct_back_proj(h, ct_views(*views), _ptr(y, torch.float32, "y"), _ptr(x, torch.float32, "x"),
-                               1 if accumulate else 0, _stream(stream)))
+    _check(load().ct_back_proj(h, ct_views(*views), _ptr(y, torch.float32, "y", _cells(h, views[2])),
+                               _ptr(x, torch.float32, "x", _img(h)), 1 if accumulate else 0, _stream(stream)))
 
 
 def ct_sqs_denom_scratch_bytes(h):
@@ -198,20 +222,23 @@ def ct_sqs_denom_scratch_bytes(h):
 
 
 def ct_sqs_denom(h, w, mask, dl, scratch, stream=None):
-    _check(load().ct_sqs_denom(h, _ptr(w, torch.float32, "w"), _ptr(mask, torch.uint8, "mask"),
-                               _ptr(dl, torch.float32, "dl"), _ptr(scratch, torch.uint8, "scratch"), _stream(stream)))
+    _check(load().ct_sqs_denom(h, _ptr(w, torch.float32, "w", _cells(h, _na(h))), _ptr(mask, torch.uint8, "mask", _img(h)),
+                               _ptr(dl, torch.float32, "dl", _img(h)),
+                               _ptr(scratch, torch.uint8, "scratch", ct_sqs_denom_scratch_bytes(h)), _stream(stream)))
 
 
 def ct_reg_grad(h, reg, mask, x, grad, curv=None, stream=None):
     r = ct_reg(float(reg[0]), float(reg[1]), int(reg[2]))
-    _check(load().ct_reg_grad(h, ctypes.byref(r), _ptr(mask, torch.uint8, "mask"), _ptr(x, torch.float32, "x"),
-                              _ptr(grad, torch.float32, "grad"), _ptr(curv, torch.float32, "curv"), _stream(stream)))
+    n = _img(h)
+    _check(load().ct_reg_grad(h, ctypes.byref(r), _ptr(mask, torch.uint8, "mask", n), _ptr(x, torch.float32, "x", n),
+                              _ptr(grad, torch.float32, "grad", n), _ptr(curv, torch.float32, "curv", n),
+                              _stream(stream)))
 
 
 def ct_count_vv(h, views, mask, scratch, stream=None):
     """Returns (U, nnz, C) of the view list (see the header)."""
     out = (ctypes.c_longlong * 3)()
-    _check(load().ct_count_vv(h, ct_views(*views), _ptr(mask, torch.uint8, "mask"),
+    _check(load().ct_count_vv(h, ct_views(*views), _ptr(mask, torch.uint8, "mask", _img(h)),
                               _ptr(scratch, torch.uint8, "scratch"), out, _stream(stream)))
     return tuple(int(v) for v in out)
 
@@ -297,7 +324,7 @@ class Geometry:
         _check(L.ct_fbp_scratch_bytes(self.h, ctypes.byref(n)))
         scratch = torch.empty(n.value, dtype=torch.uint8, device=self.device)
         x = torch.empty(self.img_shape, dtype=torch.float32, device=self.device)
-        _check(L.ct_fbp(self.h, _ptr(y, torch.float32, "y"), _ptr(x, torch.float32, "x"),
+        _check(L.ct_fbp(self.h, _ptr(y, torch.float32, "y", _cells(self.h, self.na)), _ptr(x, torch.float32, "x"),
                         ctypes.c_void_p(scratch.data_ptr()), _stream(stream)))
         return x
 
@@ -352,12 +379,13 @@ class OSLALM:
 
     def set_data(self, y, w, dl, mask):
         self._keep = (y, w, dl, mask)
-        self._data = ct_oslalm_data(_ptr(y, torch.float32, "y"), _ptr(w, torch.float32, "w"),
-                                    _ptr(dl, torch.float32, "dl"), _ptr(mask, torch.uint8, "mask"))
+        h, na = self.geo.h, self.geo.na
+        self._data = ct_oslalm_data(_ptr(y, torch.float32, "y", _cells(h, na)), _ptr(w, torch.float32, "w", _cells(h, na)),
+                                    _ptr(dl, torch.float32, "dl", _img(h)), _ptr(mask, torch.uint8, "mask", _img(h)))
 
     def iterate(self, x, stream=None):
         _check(load().ct_oslalm_iter(self.geo.h, ctypes.byref(self.cfg), ctypes.byref(self._data), self.h,
-                                     _ptr(x, torch.float32, "x"), _stream(stream)))
+                                     _ptr(x, torch.float32, "x", _img(self.geo.h)), _stream(stream)))
 
     def reset(self):
         _check(load().ct_oslalm_state_reset(self.h))
@@ -380,7 +408,7 @@ class OSLALM:
             rho = (ctypes.c_double * cap)(); xi = (ctypes.c_double * cap)(); rs = (ctypes.c_int * cap)()
             lg = ct_oslalm_log(rho, xi, rs, cap, 0)
         _check(L.ct_oslalm_run(self.geo.h, ctypes.byref(self.cfg), ctypes.byref(self._data), self.h,
-                               _ptr(x, torch.float32, "x"), int(n_iter), ctypes.byref(lg) if lg else None,
+                               _ptr(x, torch.float32, "x", _img(self.geo.h)), int(n_iter), ctypes.byref(lg) if lg else None,
                                _stream(stream)))
         if log:
             n = lg.count

@@ -658,3 +658,22 @@ def test_fan_pixel_much_finer_than_channel_is_rejected(ct):
     buffers): a finer grid is refused at create with CT_EUNSUPPORTED, not run."""
     with pytest.raises(ct.CTError, match="CT_EUNSUPPORTED"):
         ct.Geometry(GU.geom("fan2d", nx=6, dx=0.8, ns=1, ds=9.0, na=25))
+
+
+def test_binding_rejects_short_buffers(ct):
+    """The C ABI takes bare pointers; the binding checks every buffer's size against the
+    geometry before the call (no out-of-bounds device writes from a short tensor)."""
+    g = geoms_small()["axial_c3"]
+    geo = ct.Geometry(g)
+    x = torch.zeros(geo.img_shape, device="cuda")
+    y = torch.zeros(geo.sino_shape(4), device="cuda")
+    ct.ct_fwd_proj(geo.h, (0, 1, 4), x, y)
+    with pytest.raises(ct.CTError, match="elements"):
+        ct.ct_fwd_proj(geo.h, (0, 1, 5), x, y)            # 5 views into a 4-view sinogram
+    with pytest.raises(ct.CTError, match="elements"):
+        ct.ct_back_proj(geo.h, (0, 1, 4), y, x[:-1])     # image one row short
+    w = torch.ones(geo.sino_shape(g["na"] - 1), device="cuda")
+    mask = torch.ones(geo.img_shape, dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(ct.ct_sqs_denom_scratch_bytes(geo.h), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ct.CTError, match="elements"):
+        ct.ct_sqs_denom(geo.h, w, mask, x, scratch)       # weights one view short
