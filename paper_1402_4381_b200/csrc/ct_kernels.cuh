@@ -836,16 +836,19 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 //     (u = nr, the top edge, reads QP[nr] = (total, 0); l_theta of slice iz from
                 //     its lower edge's zi: tz = (zi + 1/2) dz / rho)
                 const float fnr = (float)nr, ubl = ub - (float)r_lo, hdz = 0.5f * f.ax.dz_rho;
-                for (int s0 = 0; s0 < nzs; s0 += 31) {
-                    const int iz = za + s0 + lane;   // lower edge of slice iz (lane 31: upper edge of iz - 1)
-                    const float zi = (float)(iz - f.ax.qi) - f.ax.qf;
+                const float zl = (float)(za + lane - f.ax.qi) - f.ax.qf;   // this lane's edge in pass 0
+                float* accl = acc + za + lane;
+                float sf = 0.0f;   // (float)s0
+                for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) {
+                    // lower edge of slice za + s0 + lane (lane 31: upper edge of the pass's last slice)
+                    const float zi = zl + sf;
                     const float u = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubl), 0.0f), fnr);
                     const int k = __float2int_rd(u);
                     const float2 qp = QP[k];
                     const float pf = fmaf(u - (float)k, qp.y, qp.x);
                     const float up = __shfl_down_sync(0xffffffffu, pf, 1);
                     const float tz = fmaf(zi, f.ax.dz_rho, hdz);
-                    if (lane < min(nzs - s0, 31)) acc[iz] = fmaf(sqrt_approx(fmaf(tz, tz, 1.0f)), up - pf, acc[iz]);
+                    if (lane < nzs - s0 && lane < 31) accl[s0] = fmaf(sqrt_approx(fmaf(tz, tz, 1.0f)), up - pf, accl[s0]);
                 }
                 __syncwarp();
             }
