@@ -448,8 +448,16 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
             CT_CUDA(launch_pdl(back2d_kernel<EPI, false>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
     else {
         const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * (size_t)dg.nz;
-        CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI>, smem));
-        back3d_kernel<EPI><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+        if (dg.nt == 64) {
+            CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 64>, smem));
+            back3d_kernel<EPI, 64><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+        } else if (dg.nt == 32) {
+            CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 32>, smem));
+            back3d_kernel<EPI, 32><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+        } else {
+            CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 0>, smem));
+            back3d_kernel<EPI, 0><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+        }
     }
     CT_LAUNCHED(1);
     return CT_OK;

@@ -698,7 +698,9 @@ __device__ __forceinline__ void filt_rows1(const float* __restrict__ yr, int pit
     for (int c = 0; c < NC; c++) q0 = fmaf(f.w[c], vv[c], q0);
 }
 
-template <int EPI>
+// NTM: detector-row specialisation, 64 or 32 (every row in one pass, nt a compile-time
+// constant) or 0 (general nt: the rows the active slices meet).
+template <int EPI, int NTM>
 __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, int first, int stride, int count,
                                                     const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
     const int ix = blockIdx.x * 4 + (wid & 3);
     const int iy = blockIdx.y * 2 + (wid >> 2);
     const bool colok = ix < g.nx && iy < g.ny;
-    const int nt = g.nt, ns = g.ns, nz = g.nz;
+    const int nt = NTM ? NTM : g.nt, ns = g.ns, nz = g.nz;
     const int col = ((colok ? iy : 0) * g.nx + (colok ? ix : 0)) * nz;
     Foot* tab = table + wid * 32;
     // QP[k] = (PF[k], Q(r_lo + k)): prefix sum of the filtered rows below row r_lo + k and the
@@ -748,7 +750,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 if (f.n <= 0) continue;
                 const int za = f.rows & 0xffff, nzs = f.rows >> 16;
                 int r_lo = 0, nr = nt;
-                if (nt == 64) {
+                if (NTM == 64) {
                     // the common 64-row detector: one pass over every row, two rows per lane
                     // (the rows the active slices miss are cheap to include)
                     const float2* yr = reinterpret_cast<const float2*>(y + ((vb + j) * ns + f.cA) * 64) + lane;
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                     const float ex = inc - s2;
                     reinterpret_cast<float4*>(QP)[lane] = make_float4(ex, q0, ex + q0, q1);
                     if (lane == 31) QP[64] = make_float2(inc, 0.0f);
-                } else if (nt == 32) {
+                } else if (NTM == 32) {
                     // 32-row detector: one pass over every row, one row per lane
                     const float* yr = y + ((vb + j) * ns + f.cA) * 32 + lane;
                     float q0 = 0.0f;
