@@ -229,6 +229,29 @@ __device__ __forceinline__ void voxel_rows(const Axial& ax, const DevGeom& g, in
 // next kernel's blocks be scheduled once every block of this grid has issued it.
 // Both are no-ops for a normal launch.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The compiler treats read-only (ld.global.nc) loads as invariant and may hoist them above
+// griddepcontrol.wait despite its memory clobber.  A pointer to data a predecessor kernel
+// writes is passed through pdl_after() after the wait: the loads through the returned
+// pointer depend on an opaque asm output that follows the wait (volatile asms keep order).
+template <typename T>
+__device__ __forceinline__ T* pdl_after(T* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
+// Loads of data a PDL predecessor writes use coherent ld.global (L1-cached): ld.global.nc
+// (__ldg, or what nvcc emits for const __restrict__ pointers) promises the data is read-only
+// for the kernel's whole lifetime, which a predecessor still running before the wait breaks,
+// and ptxas does hoist .nc loads above griddepcontrol.wait.
+__device__ __forceinline__ float ld_dep(const float* p) {
+    float v;
+    asm("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_dep(const double* p) {
+    double v;
+    asm("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 // Fair potential pieces (reading G3/G14)

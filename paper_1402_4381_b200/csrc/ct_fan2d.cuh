@@ -146,8 +146,8 @@ __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, cons
     // issue the bin loads before the CDF arithmetic (latency hiding)
     float yv[kPre];
 #pragma unroll
-    for (int j = 0; j < kPre; j++) yv[j] = (j + 1 < f.n) ? __ldg(&yk[j]) : 0.0f;
-    const float ylast = __ldg(&yk[f.n - 1]);
+    for (int j = 0; j < kPre; j++) yv[j] = (j + 1 < f.n) ? ld_dep(&yk[j]) : 0.0f;
+    const float ylast = ld_dep(&yk[f.n - 1]);
     const Trap2 T(g, f);   // clamped footprint: c0 = cA
     // F = 0 left of t0 and F = mass right of t3: only clipped ends need an evaluation
     float Fp = f.clL ? T.F(T.u0) : 0.0f, s = 0.0f;
@@ -155,7 +155,7 @@ __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, cons
     for (int j = 0; j < kMaxFoot - 1; j++) {
         if (j + 1 >= f.n) break;
         const float Fn = T.F(__fadd_rn(T.u0, (float)(j + 1)));
-        s = fmaf(__fsub_rn(Fn, Fp), j < kPre ? yv[j < kPre ? j : 0] : __ldg(&yk[j]), s);
+        s = fmaf(__fsub_rn(Fn, Fp), j < kPre ? yv[j < kPre ? j : 0] : ld_dep(&yk[j]), s);
         Fp = Fn;
     }
     const float Fend = f.clR ? T.F(__fadd_rn(T.u0, (float)f.n)) : T.mass;
@@ -221,10 +221,11 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
     const int nvx = min(kF2T, g.nx - vx0), nvy = min(kF2T, g.ny - vy0);   // valid pixels in the tile
     pdl_trigger();
     pdl_wait();   // x is the previous kernel's output
+    x = pdl_after(x);
     bool any = false;
     for (int e = tid; e < kF2T * kF2T; e += 256) {
         const int j = e >> 5, i = e & 31;
-        const float v = (i < nvx && j < nvy) ? __ldg(&x[(vy0 + j) * g.nx + vx0 + i]) : 0.0f;
+        const float v = (i < nvx && j < nvy) ? ld_dep(&x[(vy0 + j) * g.nx + vx0 + i]) : 0.0f;
         xs[j][i] = v;
         any |= v != 0.0f;
     }
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(256) fwd2d_finalize_kernel(DevGeom g, int firs
                                                             float scale) {
     pdl_trigger();
     pdl_wait();
+    acc = pdl_after(acc);
     const int i = blockIdx.x * 256 + threadIdx.x;
     if (i >= count * g.ns) return;
     const long long q = (long long)acc[i];
@@ -427,6 +429,7 @@ __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, 
                 }
             }
             if (kb == 0) pdl_wait();   // the vertex tables depend on the geometry only; y is the predecessor's
+            y = pdl_after(y);
             __syncthreads();
             if (act) {
                 for (int kk = 0; kk < nb; kk++) {
@@ -442,6 +445,10 @@ __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, 
         }
     }
     pdl_wait();   // (tiles outside S skipped the loop) the epilogue writes G+, g
+    ga.G_old = pdl_after(ga.G_old);
+    ga.gs = pdl_after(ga.gs);
+    ga.rho = pdl_after(ga.rho);
+    ga.gbar = pdl_after(ga.gbar);
     const size_t j = (size_t)iy * g.nx + ix;
     const double xi = back_epilogue<EPI>(j, valid, acc, x, ga);
     if (EPI == EPI_GUPD) {

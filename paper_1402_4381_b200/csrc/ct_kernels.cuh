@@ -1050,22 +1050,44 @@ __global__ void __launch_bounds__(256) sqs_update2d_kernel(DevGeom g, const floa
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int ix0 = blockIdx.x * 32, iy0 = iy_begin + blockIdx.y * 8;
     const int nx = g.nx;
-    pdl_trigger();
-    pdl_wait();   // G, g, rho are the previous kernels' outputs
-    for (int e = threadIdx.x; e < 340; e += 256) {
+    const int ix = ix0 + tx, iy = iy0 + ty;
+    const bool own = ix < nx && iy < iy_end;
+    const int j = own ? iy * nx + ix : 0;
+    // halo tile elements e0 = tid, e1 = tid + 256 (< 340); the mask and D_L are static, so
+    // they are read before the wait for the previous kernels, and x is read unconditionally
+    // next to its mask bit (two independent loads instead of a dependent pair)
+    int je[2];
+    bool ok[2], me[2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+        const int e = threadIdx.x + 256 * q;
         const int a = e / 34, b = e - a * 34;
-        const int iy = iy0 - 1 + a, ix = ix0 - 1 + b;
-        float v = __int_as_float(0x7fc00000);   // NaN: not in S
-        if (iy >= 0 && iy < g.ny && ix >= 0 && ix < nx) {
-            const int j = iy * nx + ix;
-            if (__ldg(&m[j])) v = __ldg(&x[j]);
-        }
-        T[a][b] = v;
+        const int ey = iy0 - 1 + a, ex = ix0 - 1 + b;
+        ok[q] = e < 340 && ey >= 0 && ey < g.ny && ex >= 0 && ex < nx;
+        je[q] = ok[q] ? ey * nx + ex : 0;
+        me[q] = ok[q] && __ldg(&m[je[q]]);
+    }
+    const float dlj = own ? __ldg(&dl[j]) : 0.0f;
+    pdl_trigger();
+    pdl_wait();   // x, G, g, rho are the previous kernels' outputs
+    x = pdl_after(x);
+    G = pdl_after(G);
+    gs = pdl_after(gs);
+    rho_p = pdl_after(rho_p);
+    alpha_p = pdl_after(alpha_p);
+    float xe[2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) xe[q] = ok[q] ? ld_dep(&x[je[q]]) : 0.0f;
+    const float Gj = own ? ld_dep(&G[j]) : 0.0f, gj = own ? ld_dep(&gs[j]) : 0.0f;
+    const float rho = (float)ld_dep(rho_p);
+    const float ra = rho * (float)ld_dep(alpha_p);   // rho alpha: H = alpha D_L (BB; alpha = 1 otherwise)
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+        const int e = threadIdx.x + 256 * q;
+        if (e < 340) (&T[0][0])[e] = me[q] ? xe[q] : __int_as_float(0x7fc00000);   // NaN: not in S
     }
     __syncthreads();
-    const int ix = ix0 + tx, iy = iy0 + ty;
-    if (ix >= nx || iy >= iy_end) return;
-    const int j = iy * nx + ix;
+    if (!own) return;
     const float xj = T[ty + 1][tx + 1];
     if (xj != xj) {
         xn[j] = 0.0f;   // off S
@@ -1087,10 +1109,8 @@ __global__ void __launch_bounds__(256) sqs_update2d_kernel(DevGeom g, const floa
                 cu += wgt * om;
             }
         }
-    const float rho = (float)*rho_p;
-    const float ra = rho * (float)*alpha_p;   // rho alpha: H = alpha D_L (BB; alpha = 1 otherwise)
-    const float sdir = rho * __ldg(&G[j]) + (1.0f - rho) * __ldg(&gs[j]);
-    const float den = ra * __ldg(&dl[j]) + 2.0f * beta * cu;
+    const float sdir = rho * Gj + (1.0f - rho) * gj;
+    const float den = ra * dlj + 2.0f * beta * cu;
     xn[j] = fmaxf(xj - (sdir + beta * gr) / den, 0.0f);
 }
 
