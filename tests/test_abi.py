@@ -50,6 +50,36 @@ def test_library_targets_sm100a_only():
     assert "sm_90" not in out and "sm_80" not in out
 
 
+def test_pdl_kernels_read_no_predecessor_data_before_the_wait():
+    """In every kernel that waits on its PDL predecessor (griddepcontrol.wait = SASS ACQBULK),
+    the loads scheduled before the wait are static data only: the uint8 support mask, the
+    view table (64/128-bit .nc loads) and, in the 2D K3, D_L (one 32-bit .nc load per
+    thread).  Any other load there is a predecessor output hoisted above the wait (DESIGN §6,
+    launch chain; a hoisted x load in a K3 variant gave a 63 HU error)."""
+    from paper_1402_4381_b200 import build
+    import re
+    import subprocess
+    sass = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True).stdout
+    n_pdl = 0
+    for func in re.split(r"\n\s*Function : ", sass)[1:]:
+        name = func.split("\n", 1)[0].strip()
+        lines = func.split("\n")
+        waits = [i for i, l in enumerate(lines) if "ACQBULK" in l]
+        if not waits:
+            continue
+        n_pdl += 1
+        f32_nc = 0
+        for l in lines[:waits[0]]:
+            if "LDG" not in l:
+                continue
+            if ".U8" in l or ".64.CONSTANT" in l or ".128.CONSTANT" in l:
+                continue
+            assert "LDG.E.CONSTANT" in l, (name, l.strip())   # a coherent load before the wait
+            f32_nc += 1
+        assert f32_nc <= (1 if "sqs_update2d" in name else 0), (name, f32_nc)
+    assert n_pdl >= 4   # fwd2d tile + finalize, back2d, 2D K3
+
+
 @pytest.mark.parametrize("bad,code", [
     (dict(dy=1.0), "CT_EINVAL"),            # non-square voxels
     (dict(nx=0), "CT_EINVAL"),
