@@ -255,8 +255,18 @@ __device__ __forceinline__ double ld_dep(const double* p) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 // Fair potential pieces (reading G3/G14)
+#ifndef CT_FAIR_RCP_APPROX
+#define CT_FAIR_RCP_APPROX 1
+#endif
 __device__ __forceinline__ void fair(float t, float inv_delta, float& dpsi, float& omega) {
-    omega = __frcp_rn(1.0f + fabsf(t) * inv_delta);
+    const float v = fmaf(fabsf(t), inv_delta, 1.0f);   // >= 1
+#if CT_FAIR_RCP_APPROX
+    // MUFU reciprocal (max error ~1 ulp on [1, inf)): one instruction instead of the
+    // correctly rounded sequence; the 26-neighbour stencil evaluates it 26 times per voxel
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(omega) : "f"(v));
+#else
+    omega = __frcp_rn(v);
+#endif
     dpsi = t * omega;
 }
 
