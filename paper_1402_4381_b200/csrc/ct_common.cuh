@@ -181,8 +181,8 @@ __device__ __forceinline__ void axial(const DevGeom& g, float4 view, float rho, 
     ax.qi = (int)view.z;
     ax.qf = view.w;
     ax.kz = g.dt * rho / (g.dsd * g.dz);
-    ax.inv_kz = 1.0f / ax.kz;
-    ax.dz_rho = g.dz / rho;
+    ax.inv_kz = __fdividef(g.dsd * g.dz, g.dt * rho);   // MUFU reciprocal paths (~2 ulp)
+    ax.dz_rho = __fdividef(g.dz, rho);
 }
 
 __device__ __forceinline__ float sqrt_approx(float v) {

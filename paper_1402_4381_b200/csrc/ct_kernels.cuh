@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(256) sqs_update_kernel(DevGeom g, const float*
     const float ra = rho * (float)*alpha_p;   // rho alpha: H = alpha D_L (BB; alpha = 1 otherwise)
     float s = rho * G[j] + (1.0f - rho) * gs[j];
     float den = ra * dl[j] + 2.0f * beta * cu;
-    float v = xj - (s + beta * gr) / den;
+    float v = xj - __fdividef(s + beta * gr, den);
     xn[j] = fmaxf(v, 0.0f);
 }
 
@@ -1030,7 +1030,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                 }
                 const float sdir = rho * __ldg(&G[j]) + (1.0f - rho) * __ldg(&gs[j]);
                 const float den = ra * __ldg(&dl[j]) + 2.0f * beta * cu;
-                xn[j] = fmaxf(xj - (sdir + beta * gr) / den, 0.0f);
+                xn[j] = fmaxf(xj - __fdividef(sdir + beta * gr, den), 0.0f);
             }
         }
         __syncthreads();
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(256) sqs_update2d_kernel(DevGeom g, const floa
         }
     const float sdir = rho * Gj + (1.0f - rho) * gj;
     const float den = ra * dlj + 2.0f * beta * cu;
-    xn[j] = fmaxf(xj - (sdir + beta * gr) / den, 0.0f);
+    xn[j] = fmaxf(xj - __fdividef(sdir + beta * gr, den), 0.0f);
 }
 
 // One FISTA iteration of the inner denoising problem (NEXT-1):
@@ -1162,7 +1162,7 @@ __global__ void __launch_bounds__(256) fista_step_kernel(DevGeom g, const float*
     const float s = rho * G[j] + (1.0f - rho) * gs[j];
     const float grad = beta * gr + rdl * (vj - xk[j]) + s;
     const float xp = xprev[j];
-    const float xn = fmaxf(vj - grad / (rdl + 2.0f * beta * sw), 0.0f);
+    const float xn = fmaxf(vj - __fdividef(grad, rdl + 2.0f * beta * sw), 0.0f);
     xout[j] = xn;
     if (!LAST) vout[j] = xn + mom * (xn - xp);
 }
