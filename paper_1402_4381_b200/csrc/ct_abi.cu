@@ -447,7 +447,7 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
         else
             CT_CUDA(launch_pdl(back2d_kernel<EPI, false>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
     else {
-        const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * (size_t)dg.nz;
+        const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * ((size_t)dg.nz + kBackPad);
         if (dg.nt == 64) {
             CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 64>, smem));
             back3d_kernel<EPI, 64><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);

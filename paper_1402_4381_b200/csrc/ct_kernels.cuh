@@ -670,6 +670,7 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 // Work per (column, view) is proportional to the slices the cone actually meets,
 // which matters for helical scans (a view sees ~20-30 % of a long volume).
 constexpr int kBackRows = 128;   // >= nt (validated)
+constexpr int kBackPad = 32;     // per-warp accumulator padding past nz (slice-loop tail lanes add 0 there)
 
 __host__ __device__ constexpr size_t back3d_smem_fixed() {
     return sizeof(Foot) * 8 * 32 + sizeof(float2) * 8 * (kBackRows + 4);
@@ -717,7 +718,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
     // QP[k] = (PF[k], Q(r_lo + k)): prefix sum of the filtered rows below row r_lo + k and the
     // row itself (one 8-byte load per slice edge); QP[nr] = (total, 0)
     float2* QP = QPs + wid * (kBackRows + 4);
-    float* acc = ACC + wid * nz;
+    float* acc = ACC + wid * (nz + kBackPad);   // + kBackPad: the slice loop's unpredicated tail
     bool any = false;
     for (int iz = lane; iz < nz; iz += 32) {
         acc[iz] = 0.0f;
@@ -850,7 +851,9 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                     const float pf = fmaf(u - (float)k, qp.y, qp.x);
                     const float up = __shfl_down_sync(0xffffffffu, pf, 1);
                     const float tz = fmaf(zi, f.ax.dz_rho, hdz);
-                    if (lane < nzs - s0 && lane < 31) accl[s0] = fmaf(sqrt_approx(fmaf(tz, tz, 1.0f)), up - pf, accl[s0]);
+                    // no predicate: lanes past the active window (and lane 31, whose up = pf) add
+                    // exactly 0 (both edges clamp to the same u), into slots < nz + kBackPad
+                    accl[s0] = fmaf(sqrt_approx(fmaf(tz, tz, 1.0f)), up - pf, accl[s0]);
                 }
                 __syncwarp();
             }
