@@ -1,5 +1,5 @@
 """Multi-GPU decomposition checked on CPU with torch.distributed/gloo,
-world size 2: each rank back-projects its contiguous block of a subset's views (the same
+world sizes 2 and 3: each rank back-projects its contiguous block of a subset's views (the same
 partition the C library's rank_views uses, mirrored by host.rank_view_block), the partial
 images are summed with all_reduce, and the result must equal the full subset back-projection.
 The oracle supplies the projector on both ranks; the NCCL path itself needs GPUs."""
@@ -138,13 +138,14 @@ def _zslab_worker(rank, ws, port, out):
     dist.destroy_process_group()
 
 
-def test_gloo_two_rank_zslab():
+@pytest.mark.parametrize("ws", [2, 3])   # 3: uneven view blocks / slabs
+def test_gloo_two_rank_zslab(ws):
     import oracle
     oracle.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_zslab_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_zslab_worker, args=(r, ws, port, q)) for r in range(ws)]
     for p in procs:
         p.start()
     res = q.get(timeout=120)
@@ -180,13 +181,14 @@ def test_slab_partition_covers_rows():
             assert ws * slabs[0][2] >= ny
 
 
-def test_gloo_two_rank_slab_update():
+@pytest.mark.parametrize("ws", [2, 3])   # 3: uneven view blocks / slabs
+def test_gloo_two_rank_slab_update(ws):
     import oracle
     oracle.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_slab_worker, args=(r, ws, port, q)) for r in range(ws)]
     for p in procs:
         p.start()
     res = q.get(timeout=120)
@@ -208,13 +210,14 @@ def test_view_block_partition_covers_subset():
             assert max(n for _, n in blocks) - min(n for _, n in blocks) <= 1
 
 
-def test_gloo_two_rank_back_projection_sum():
+@pytest.mark.parametrize("ws", [2, 3])   # 3: uneven view blocks / slabs
+def test_gloo_two_rank_back_projection_sum(ws):
     import oracle
     oracle.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, ws, port, q)) for r in range(ws)]
     for p in procs:
         p.start()
     res = q.get(timeout=120)
