@@ -47,6 +47,9 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+#ifndef CT_FWD2D_PT
+#define CT_FWD2D_PT 1     // compile-time lane-parity buffer count for P = 1, 2
+#endif
 #ifndef CT_FWD3D_PAIR
 #define CT_FWD3D_PAIR 1   // nt <= 64: pair-row forward kernel (fwd3d2_kernel); 0: fwd3d_kernel
 #endif
@@ -379,13 +382,14 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
     const DevGeom& dg = g->dg;
     if (dg.kind == CT_FAN2D) {
         const size_t smem = sizeof(float) * 8 * dg.fpar * dg.fspan;
-        CT_CUDA(ensure_dyn_smem(dg.vrel ? (const void*)fwd2d_tile_kernel<true> : (const void*)fwd2d_tile_kernel<false>,
-                                smem));
+        // P = 2 (c1, c2 and most fan geometries) and P = 1 get compile-time instances
+        auto kern = dg.vrel ? (dg.fpar == 2 && CT_FWD2D_PT ? fwd2d_tile_kernel<true, 2>
+                               : dg.fpar == 1 && CT_FWD2D_PT ? fwd2d_tile_kernel<true, 1> : fwd2d_tile_kernel<true, 0>)
+                            : (dg.fpar == 2 && CT_FWD2D_PT ? fwd2d_tile_kernel<false, 2>
+                               : dg.fpar == 1 && CT_FWD2D_PT ? fwd2d_tile_kernel<false, 1> : fwd2d_tile_kernel<false, 0>);
+        CT_CUDA(ensure_dyn_smem((const void*)kern, smem));
         dim3 grid((dg.nx + kF2T - 1) / kF2T, (dg.ny + kF2T - 1) / kF2T, (v.count + kF2VC - 1) / kF2VC);
-        if (dg.vrel)
-            CT_CUDA(launch_pdl(fwd2d_tile_kernel<true>, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
-        else
-            CT_CUDA(launch_pdl(fwd2d_tile_kernel<false>, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
+        CT_CUDA(launch_pdl(kern, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
         const int cells = v.count * dg.ns;
         CT_CUDA(launch_pdl(fwd2d_finalize_kernel<RESID>, dim3((cells + 255) / 256), dim3(256), 0, st, dg, v.first,
                            v.stride, v.count, g->acc2d, out, yobs, w, scale));

@@ -208,14 +208,15 @@ __device__ __forceinline__ void fwd_rounds(float* bp, const Trap2& T, float koff
     }
 }
 
-template <bool VREL>
+// PT: the lane-parity buffer count P as a compile-time constant (0: runtime g.fpar)
+template <bool VREL, int PT>
 __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom g, int first, int stride, int count,
                                                         const float* __restrict__ x,
                                                         unsigned long long* __restrict__ acc) {
     extern __shared__ float wb[];                 // [8 warps][P][SPAN]
     __shared__ float xs[kF2T][kF2T + 1];
     __shared__ float V[kF2T + 1][kF2T + 1];
-    const int P = g.fpar, SPAN = g.fspan;
+    const int P = PT ? PT : g.fpar, SPAN = g.fspan;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int vx0 = blockIdx.x * kF2T, vy0 = blockIdx.y * kF2T;
     const int nvx = min(kF2T, g.nx - vx0), nvy = min(kF2T, g.ny - vy0);   // valid pixels in the tile
