@@ -518,11 +518,15 @@ void or_inner_fista(const or_geom* g, double beta, double delta, int nbr, const 
  * alpha <= 1 (eq. scale_factor_alpha_k):
  *     alpha_k = min(1, max(alpha_min, (y_k' s_k) / (s_k' D_L s_k)))   (sums over S),
  *     s_k = x^k - x^{k-1},  y_k = grad l(x^k) - grad l(x^{k-1}).
- * OS reading (DESIGN.md B-BB): k counts outer iterations; x^k is the image after outer
- * iteration k and grad l(x^k) is approximated by the mean of the M subset gradients
- * M grad l_m computed during iteration k.  alpha = 1 for iterations 1 and 2 (no secant
- * pair yet); alpha_k (from iterations k-1, k) is used in iteration k + 1.  alpha_log
- * (nullable) receives the alpha used in each outer iteration.
+ * OS reading (DESIGN.md B-BB): k counts outer iterations; grad l is approximated by the
+ * mean gbar_k of the M subset gradients M grad l_m computed during iteration k, and the
+ * secant pair uses the points where those gradients were evaluated: s_k = xbar_k -
+ * xbar_{k-1}, xbar_k = mean of the M inner iterates x^{k,j} (the image after inner step j,
+ * at which the next subset gradient is computed), y_k = gbar_k - gbar_{k-1}.  With M = 1
+ * xbar_k = x^k (the paper's s_k).  (Pairing gbar_k with the end point x^k instead makes
+ * y_k's' <= 0 common with OS and collapses the iteration.)  alpha = 1 for iterations 1
+ * and 2 (no secant pair yet); alpha_k (from iterations k-1, k) is used in iteration k + 1.
+ * alpha_log (nullable) receives the alpha used in each outer iteration.
  */
 void or_oslalm_run(const or_geom* g, const double* y, const double* w, const double* dl, const uint8_t* mask,
                    int M, int mode, double rho_fixed, double rho_min, double beta, double delta, int nbr,
@@ -548,7 +552,8 @@ void or_oslalm_run(const or_geom* g, const double* y, const double* w, const dou
     /* Barzilai-Borwein state: H = alpha D_L (alpha = 1: the plain SQS Hessian) */
     double alpha = 1.0;
     double* hd = (double*)malloc(N * sizeof(double));        /* alpha D_L */
-    double* xprev = bb ? (double*)malloc(N * sizeof(double)) : NULL;
+    double* xprev = bb ? (double*)malloc(N * sizeof(double)) : NULL;   /* xbar_{k-1} */
+    double* xbar = bb ? (double*)calloc(N, sizeof(double)) : NULL;
     double* gbar = bb ? (double*)calloc(N, sizeof(double)) : NULL;
     double* gprev = bb ? (double*)malloc(N * sizeof(double)) : NULL;
     for (int k = 1; k <= n_iter; k++) {
@@ -585,29 +590,33 @@ void or_oslalm_run(const or_geom* g, const double* y, const double* w, const dou
             if (mode == 1) l = restart ? 0 : l + 1;
             if (log) { log[3 * step + 1] = xi; log[3 * step + 2] = restart; }
             if (bb)
-                for (size_t q = 0; q < N; q++) gbar[q] += G[q] / M;   /* mean of the iteration's M grad l_m */
+                for (size_t q = 0; q < N; q++) {
+                    gbar[q] += G[q] / M;   /* mean of the iteration's M grad l_m ... */
+                    xbar[q] += x[q] / M;   /* ... and of the points they were evaluated at */
+                }
         }
         if (bb && step < n_iter * M) {   /* end of outer iteration k (completed) */
             if (k >= 2) {
                 double num = 0.0, den = 0.0;
                 for (size_t q = 0; q < N; q++)
                     if (mask[q]) {
-                        double sq = x[q] - xprev[q];
+                        double sq = xbar[q] - xprev[q];
                         num += (gbar[q] - gprev[q]) * sq;
                         den += dl[q] * sq * sq;
                     }
                 double a = den > 0.0 ? num / den : 1.0;
                 alpha = a > 1.0 ? 1.0 : (a < alpha_min ? alpha_min : a);
             }
-            memcpy(xprev, x, N * sizeof(double));
+            memcpy(xprev, xbar, N * sizeof(double));
             memcpy(gprev, gbar, N * sizeof(double));
             memset(gbar, 0, N * sizeof(double));
+            memset(xbar, 0, N * sizeof(double));
         }
     }
     if (g_out) memcpy(g_out, sg, N * sizeof(double));
     if (G_out) memcpy(G_out, G, N * sizeof(double));
     free(order); free(G); free(Gp); free(sg); free(gr); free(cu); free(pbuf); free(hd);
-    free(xprev); free(gbar); free(gprev);
+    free(xprev); free(xbar); free(gbar); free(gprev);
 }
 
 /* ---------------- NEXT-4: FBP / FDK initial image ---------------- */

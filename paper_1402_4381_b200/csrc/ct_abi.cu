@@ -684,7 +684,8 @@ struct ct_oslalm_state {
     size_t S = 0, off0 = 0, Npad = 0;
     float* xp[2] = {nullptr, nullptr};   // full images (all-gathered), ping-pong
     double* xi_ex = nullptr;             // [0] this rank's xi, [1] all-reduced xi, [2..3] BB sums
-    float* xprev = nullptr;              // BB: x after the previous outer iteration
+    float* xprev = nullptr;              // BB: xbar of the previous outer iteration
+    float* xbar = nullptr;               // BB: mean of the current iteration's inner iterates
     float* gbar = nullptr;               // BB: mean subset gradient of the current iteration
     float* gprev = nullptr;              // BB: ... of the previous iteration
     double* bb_part = nullptr;
@@ -814,7 +815,7 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16
     const bool slab = use_slabs(g, c);
     off[10] = o; o += slab ? 2 * align256(N * 4) : 0;  // slab path: all-gathered full images (ping-pong)
     off[11] = o; o += align256(4 * 8);                 // xi / BB sums exchange
-    off[12] = o; o += c->bb ? 3 * align256(N * 4) + align256(2 * 8 * nblk(N)) : 0;   // BB: x_prev, gbar, gbar_prev, partials
+    off[12] = o; o += c->bb ? 4 * align256(N * 4) + align256(2 * 8 * nblk(N)) : 0;   // BB: xbar_prev, gbar, gbar_prev, xbar, partials
     const size_t ncols = (size_t)g->d.nx * g->d.ny;
     off[13] = o; o += g->zslab ? 4 * align256(ncols * 4) + 2 * align256(ncols) : 0;   // z-slab halos
     *total = o;
@@ -882,7 +883,8 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
         s->xprev = (float*)(b + off[12]);
         s->gbar = (float*)(b + off[12] + align256(s->Npad * 4));
         s->gprev = (float*)(b + off[12] + 2 * align256(s->Npad * 4));
-        s->bb_part = (double*)(b + off[12] + 3 * align256(s->Npad * 4));
+        s->xbar = (float*)(b + off[12] + 3 * align256(s->Npad * 4));
+        s->bb_part = (double*)(b + off[12] + 4 * align256(s->Npad * 4));
     }
     cudaError_t e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
@@ -1192,6 +1194,11 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
         }
         tmark_end(s, st, 0, t0);
         std::swap(xa, xb);
+        if (c.bb) {   // BB (reading B-BB): mean of the points where this iteration's gradients are taken
+            const size_t bj0 = s->slab ? s->off0 : 0, bj1 = s->slab ? std::min(s->N, s->off0 + s->S) : s->N;
+            xbar_acc_kernel<<<nblk(std::max(bj1, bj0 + 1) - bj0), 256, 0, st>>>(s->xbar, xa, 1.0f / (float)M, bj0, bj1);
+            kernels += 1;
+        }
         s->log_slot = j;
         if (int e = subset_gradient(s, d, xa, s->order[(j + 1) % M], EPI_GUPD, st)) return e;
         s->log_slot = -1;
@@ -1202,7 +1209,7 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
         // Barzilai-Borwein scale for the next outer iteration (reading B-BB), over this rank's
         // rows (all rows on one rank; gbar is valid on the rank's slab in the slab path)
         const size_t bj0 = s->slab ? s->off0 : 0, bj1 = s->slab ? std::min(s->N, s->off0 + s->S) : s->N;
-        BBArgs bbA{xa, s->xprev, s->gbar, s->gprev, d->dl, d->mask, s->bb_part, g->comm ? s->xi_ex + 2 : nullptr,
+        BBArgs bbA{s->xbar, s->xprev, s->gbar, s->gprev, d->dl, d->mask, s->bb_part, g->comm ? s->xi_ex + 2 : nullptr,
                    s->sc, c.alpha_min};
         bb_alpha_kernel<<<nblk(std::max(bj1, bj0 + 1) - bj0), 256, 0, st>>>(bbA, bj0, bj1);
         kernels += 1;
@@ -1229,6 +1236,7 @@ static int ensure_initialised(ct_oslalm_state* s, const ct_oslalm_data* d, float
     zero_offmask_kernel<<<nblk(s->N), 256, 0, st>>>(x, d->mask, s->N);
     CT_LAUNCHED(1);
     if (c.bb) CT_CUDA(cudaMemsetAsync(s->gbar, 0, s->Npad * 4, st));
+    if (c.bb) CT_CUDA(cudaMemsetAsync(s->xbar, 0, s->Npad * 4, st));
     if (s->g->zslab && s->g->nranks > 1) {   // the neighbours' boundary slices of S (static)
         uint8_t* sb = reinterpret_cast<uint8_t*>(s->zsend[0]);
         if (int e = zslab_halo<uint8_t>(s->g, d->mask, sb, sb + s->g->d.nx * s->g->d.ny, s->zmask[0], s->zmask[1], st))

@@ -1273,12 +1273,12 @@ __global__ void __launch_bounds__(256) gupd_slab_kernel(GupdArgs ga, size_t j0, 
 // Barzilai-Borwein scale (NEXT-2, reading B-BB): at the end of outer
 // iteration k, over S and voxels [j0, j1) (this rank's rows):
 //   num = sum (gbar_k - gbar_{k-1})(x^k - x^{k-1}),  den = sum D_L (x^k - x^{k-1})^2,
-// then x_prev <- x, gbar_prev <- gbar, gbar <- 0.  The last block (single rank) sets
+// then x_prev <- xbar, gbar_prev <- gbar, gbar <- 0, xbar <- 0.  The last block (single rank) sets
 // alpha = clip(num / den, alpha_min, 1) once two iterations are complete; with several
 // ranks it stores (num, den) for an all-reduce and bb_rule_kernel applies the rule.
 struct BBArgs {
-    const float* x;
-    float* xprev;
+    float* xbar;           // mean of the iteration's inner iterates (reset here)
+    float* xprev;          // xbar of the previous iteration
     float* gbar;
     float* gprev;
     const float* dl;
@@ -1288,6 +1288,14 @@ struct BBArgs {
     Scalars* sc;
     double alpha_min;
 };
+
+// xbar += x / M over [j0, j1): the mean of the points at which an iteration's subset
+// gradients are evaluated (the secant pair of reading B-BB)
+__global__ void __launch_bounds__(256) xbar_acc_kernel(float* __restrict__ xbar, const float* __restrict__ x,
+                                                       float inv_M, size_t j0, size_t j1) {
+    const size_t j = j0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < j1) xbar[j] = fmaf(x[j], inv_M, xbar[j]);
+}
 
 __device__ __forceinline__ void bb_rule(Scalars* sc, double num, double den, double alpha_min) {
     sc->kiter += 1;
@@ -1301,7 +1309,7 @@ __global__ void __launch_bounds__(256) bb_alpha_kernel(BBArgs b, size_t j0, size
     const size_t j = j0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     double num = 0.0, den = 0.0;
     if (j < j1) {
-        const float xj = b.x[j], gj = b.gbar[j];
+        const float xj = b.xbar[j], gj = b.gbar[j];
         if (b.mask[j]) {
             const double sq = (double)xj - (double)b.xprev[j];
             num = ((double)gj - (double)b.gprev[j]) * sq;
@@ -1310,6 +1318,7 @@ __global__ void __launch_bounds__(256) bb_alpha_kernel(BBArgs b, size_t j0, size
         b.xprev[j] = xj;
         b.gprev[j] = gj;
         b.gbar[j] = 0.0f;
+        b.xbar[j] = 0.0f;
     }
     block_sum_store<256>(num, &b.part[2 * blockIdx.x]);
     __syncthreads();   // block_sum_store's shared scratch is reused
