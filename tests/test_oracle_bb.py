@@ -71,3 +71,48 @@ def test_bb_converges_to_bruteforce_minimiser_16x16():
     assert (a[2:] < 1.0).all() and (a > 0).all()
     x_c, _, _ = _run(g, y, w, dl, S, 4000, bb=True, **kw)
     assert err(x_c) <= 1e-6, err(x_c)
+
+
+def test_bb_os_bookkeeping_matches_python_transcription_M4():
+    """OS reading B-BB: alpha_k = clip(y's / s'D_L s, alpha_min, 1) with
+    y = gbar_k - gbar_{k-1} (mean subset gradients of iterations k, k-1) and s = xbar_k -
+    xbar_{k-1} (mean of the inner iterates those gradients were taken at); alpha_k is used
+    in iteration k + 1.  A separately written Python loop (plain SQS inner step, fixed rho)
+    must reproduce the oracle's alpha sequence and image."""
+    from tests.test_oracle_algorithm import _subset_grad_py
+    g, y, w, mask = _small_problem(seed=3)
+    dl, S = O.sqs_denom(g, w, mask)
+    beta, delta, M, K, rho, amin = 2.0 ** 11, 2e-4, 4, 7, 0.5, 1e-6
+    x0 = np.zeros(O.img_shape(g))
+    a_or = np.zeros(K)
+    xo, _, _, _ = O.oslalm_run(g, y, w, dl, S, x0, M=M, mode="fixed", rho_fixed=rho, beta=beta, delta=delta,
+                               nbr=8, n_iter=K, trailing=True, bb=True, alpha_min=amin, alpha_out=a_or)
+    order = O.bit_reversal(M)
+    Sm = S > 0
+    x = x0.copy()
+    G = _subset_grad_py(g, M, order[0], y, w, x)
+    gs = G.copy()
+    alpha, alphas = 1.0, []
+    gbar_prev = xbar_prev = None
+    for k in range(1, K + 1):
+        alphas.append(alpha)
+        gbar = np.zeros_like(x)
+        xbar = np.zeros_like(x)
+        for j in range(M):
+            s = rho * G + (1 - rho) * gs
+            gr, cu = O.reg_grad(g, beta, delta, 8, S, x)
+            x = np.where(Sm, np.maximum(0.0, x - (s + gr) / np.where(Sm, rho * alpha * dl + cu, 1.0)), 0.0)
+            Gp = _subset_grad_py(g, M, order[(j + 1) % M], y, w, x)
+            gs = (rho * Gp + gs) / (1 + rho)
+            G = Gp
+            gbar += G / M
+            xbar += x / M
+        if k >= 2:
+            sv = (xbar - xbar_prev)[Sm]
+            num = ((gbar - gbar_prev)[Sm] * sv).sum()
+            den = (dl[Sm] * sv * sv).sum()
+            alpha = min(1.0, max(amin, num / den if den > 0 else 1.0))
+        gbar_prev, xbar_prev = gbar, xbar
+    assert np.allclose(alphas, a_or, rtol=1e-9, atol=0), (alphas, a_or)
+    assert (np.array(alphas[2:]) < 1.0).any()
+    assert np.abs(x - xo).max() <= 1e-9 * np.abs(x).max()
