@@ -226,13 +226,14 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
                         span);
         dg_fpar = P;
         dg_fspan = span;
-        // relative vertex positions: |cross/dot| <= tan(asin(|offset| / distance)) over the 32-vertex
-        // block grid (offsets up to 16 sqrt(2) pixels from the block's reference vertex)
-        const double bx = 0.5 * 32.0 * ceil(d->nx / 32.0) * d->dx + fabs(d->offx) + d->dx;
-        const double by = 0.5 * 32.0 * ceil(d->ny / 32.0) * d->dy + fabs(d->offy) + d->dy;
+        // relative vertex positions: |cross/dot| <= tan(asin(|offset| / distance)) over the kVB-vertex
+        // block grid (offsets up to kVB/2 sqrt(2) pixels from the block's reference vertex; the
+        // tiles' reference tables reach one block past the image)
+        const double bx = 0.5 * 32.0 * ceil(d->nx / 32.0) * d->dx + fabs(d->offx) + 2.0 * kVB * d->dx;
+        const double by = 0.5 * 32.0 * ceil(d->ny / 32.0) * d->dy + fabs(d->offy) + 2.0 * kVB * d->dy;
         const double dist = d->dso - sqrt(bx * bx + by * by);
-        const double off = 16.0 * sqrt(2.0) * d->dx;
-        dg_vrel = (dist > off && tan(asin(off / dist)) <= 0.4) ? 1 : 0;
+        const double off = 0.5 * kVB * sqrt(2.0) * d->dx;
+        dg_vrel = (dist > off && tan(asin(off / dist)) <= 0.1) ? 1 : 0;
     }
     int dev = d->device;
     DeviceGuard guard(dev);

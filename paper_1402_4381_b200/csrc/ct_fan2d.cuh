@@ -32,21 +32,25 @@ __device__ __forceinline__ float vertex_ch(const DevGeom& g, float sb, float cb,
 }
 
 // Vertex positions relative to a reference ray (vrel = 1).  The vertex grid is cut into
-// 32x32 blocks; vertices (32 bx + i, 32 by + j), i, j in [0, 32), belong to block (bx, by),
-// whose reference is the ray through its vertex (32 bx + 16, 32 by + 16).  For a vertex at
-// index offset (di, dj) from the reference, the angle between the two source rays is
-// atan(cross / dot) with cross = di Cx + dj Cy and dot = r2 + di Cy - dj Cx (square pixels),
-// |cross / dot| <= 0.4 (validated at create), so an odd series to q^15 (error < 1e-7 rad at
-// the bound) replaces the full atan: one reference atan per (block, view).  Forward and
-// back use the same owner block for every vertex, so both see identical vertex values.
+// kVB x kVB blocks; vertices (kVB bx + i, kVB by + j), i, j in [0, kVB), belong to block
+// (bx, by), whose reference is the ray through its vertex (kVB bx + kVB/2, kVB by + kVB/2).
+// For a vertex at index offset (di, dj) from the reference, the angle between the two
+// source rays is atan(cross / dot) with cross = di Cx + dj Cy and dot = r2 + di Cy - dj Cx
+// (square pixels), |cross / dot| <= 0.1 (validated at create; c2: 0.03), so the odd series
+// q - q^3/3 + q^5/5 (error < 1.5e-8 rad at the bound) replaces the full atan: one
+// reference atan per (block, view).  Forward and back use the same owner block for every
+// vertex, so both see identical vertex values.
+constexpr int kVB = 8;   // reference block edge (vertices)
+
 struct VRef {
     float G;                  // reference arc position (centred channel units)
     float Cx, Cy, r2;
 };
 
 __device__ __forceinline__ VRef make_vref(const DevGeom& g, float sb, float cb, int bx, int by) {
-    const float A = fmaf(vertex_px(g, 32 * bx + 16), sb, fmaf(-vertex_py(g, 32 * by + 16), cb, g.dso));
-    const float P = fmaf(vertex_px(g, 32 * bx + 16), cb, __fmul_rn(vertex_py(g, 32 * by + 16), sb));
+    const float px = vertex_px(g, kVB * bx + kVB / 2), py = vertex_py(g, kVB * by + kVB / 2);
+    const float A = fmaf(px, sb, fmaf(-py, cb, g.dso));
+    const float P = fmaf(px, cb, __fmul_rn(py, sb));
     VRef R;
     R.G = __fmul_rn(fast_atan(__fdividef(P, A)), g.dsd_ds);
     R.Cx = __fmul_rn(g.dx, fmaf(cb, A, -__fmul_rn(sb, P)));
@@ -59,15 +63,16 @@ __device__ __forceinline__ float vertex_rel(const DevGeom& g, const VRef& R, flo
     const float cross = fmaf(di, R.Cx, __fmul_rn(dj, R.Cy));
     const float dot = fmaf(di, R.Cy, fmaf(-dj, R.Cx, R.r2));
     const float q = __fdividef(cross, dot), t = __fmul_rn(q, q);
-    float p = -1.0f / 15.0f;
-    p = fmaf(p, t, 1.0f / 13.0f);
-    p = fmaf(p, t, -1.0f / 11.0f);
-    p = fmaf(p, t, 1.0f / 9.0f);
-    p = fmaf(p, t, -1.0f / 7.0f);
-    p = fmaf(p, t, 1.0f / 5.0f);
-    p = fmaf(p, t, -1.0f / 3.0f);
-    p = fmaf(p, t, 1.0f);
+    const float p = fmaf(fmaf(t, 1.0f / 5.0f, -1.0f / 3.0f), t, 1.0f);
     return fmaf(__fmul_rn(q, p), g.dsd_ds, R.G);
+}
+
+// Vertex (vx, vy) (global vertex indices) from the reference table of a tile whose first
+// block is (bx0, by0); RT[(by - by0) * NBX + (bx - bx0)].
+template <int NBX>
+__device__ __forceinline__ float vertex_tab(const DevGeom& g, const VRef* RT, int bx0, int by0, int vx, int vy) {
+    const VRef& R = RT[((vy >> 3) - by0) * NBX + ((vx >> 3) - bx0)];
+    return vertex_rel(g, R, (float)((vx & (kVB - 1)) - kVB / 2), (float)((vy & (kVB - 1)) - kVB / 2));
 }
 
 // Footprint of one pixel for one view (centred channel units).
@@ -230,14 +235,18 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
         xs[j][i] = v;
         any |= v != 0.0f;
     }
-    // reference rays of this block and its right / upper / upper-right neighbours (which own
-    // the tile's last vertex column / row) for every view of the chunk: warp 0, lane = view x 4
-    __shared__ VRef RF[kF2VC][4];
+    // reference rays of the 5 x 5 vertex blocks that own the tile's 33 x 33 vertices, for
+    // every view of the chunk
+    constexpr int NBF = kF2T / kVB + 1;
+    __shared__ VRef RF[kF2VC][NBF * NBF];
     const int k0 = blockIdx.z * kF2VC, k1 = min(count, k0 + kF2VC);
-    if (VREL && tid < 4 * kF2VC && k0 + (tid >> 2) < k1) {
-        const float4 vw = __ldg(&g.views[first + (k0 + (tid >> 2)) * stride]);
-        RF[tid >> 2][tid & 3] = make_vref(g, vw.x, vw.y, blockIdx.x + (tid & 1), blockIdx.y + ((tid >> 1) & 1));
-    }
+    const int bx0 = vx0 / kVB, by0 = vy0 / kVB;
+    if (VREL)
+        for (int e = tid; e < (k1 - k0) * NBF * NBF; e += 256) {
+            const int kk = e / (NBF * NBF), b = e - kk * (NBF * NBF);
+            const float4 vw = __ldg(&g.views[first + (k0 + kk) * stride]);
+            RF[kk][b] = make_vref(g, vw.x, vw.y, bx0 + b % NBF, by0 + b / NBF);
+        }
     if (!__syncthreads_or(any)) return;   // nothing to project from this tile
     for (int e = tid; e < 8 * P * SPAN; e += 256) wb[e] = 0.0f;
     float* mybuf = wb + (w * P + lane % P) * SPAN;
@@ -253,13 +262,14 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
         const float sb = vw.x, cb = vw.y;
         if (VREL) {   // relative to the owner blocks' reference rays (no per-vertex atan)
             const VRef* R = RF[k - k0];
-            const float dil = (float)(lane - 16), dil2 = -16.0f;
 #pragma unroll
             for (int r = 0; r < 4; r++)
-                if (lane <= nvx && w + 8 * r <= nvy) V[w + 8 * r][lane] = vertex_rel(g, R[0], dil, (float)(w + 8 * r - 16));
-            if (w == 0 && lane <= nvx && nvy == kF2T) V[kF2T][lane] = vertex_rel(g, R[2], dil, dil2);   // top row
-            else if (w == 1 && lane <= nvy && nvx == kF2T) V[lane][kF2T] = vertex_rel(g, R[1], dil2, (float)(lane - 16));
-            else if (w == 2 && lane == 0 && nvx == kF2T && nvy == kF2T) V[kF2T][kF2T] = vertex_rel(g, R[3], dil2, dil2);
+                if (lane <= nvx && w + 8 * r <= nvy)
+                    V[w + 8 * r][lane] = vertex_tab<NBF>(g, R, bx0, by0, vx0 + lane, vy0 + w + 8 * r);
+            if (w == 0 && lane <= nvx && nvy == kF2T) V[kF2T][lane] = vertex_tab<NBF>(g, R, bx0, by0, vx0 + lane, vy0 + kF2T);
+            else if (w == 1 && lane <= nvy && nvx == kF2T) V[lane][kF2T] = vertex_tab<NBF>(g, R, bx0, by0, vx0 + kF2T, vy0 + lane);
+            else if (w == 2 && lane == 0 && nvx == kF2T && nvy == kF2T)
+                V[kF2T][kF2T] = vertex_tab<NBF>(g, R, bx0, by0, vx0 + kF2T, vy0 + kF2T);
         } else if (nvx == kF2T && nvy == kF2T) {   // full tile (uniform branch): no bounds checks
 #pragma unroll
             for (int r = 0; r < 4; r++) V[w + 8 * r][lane] = vertex_ch(g, sb, cb, pxl, pyr[r]);
@@ -375,7 +385,8 @@ __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, 
                                                     const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     __shared__ float V[kB2VB][9][33];
     __shared__ float2 SC[kB2VB];
-    __shared__ VRef RB[kB2VB][4];   // vrel: reference rays of the owner blocks (see VRef)
+    constexpr int NBB = 32 / kVB + 1;   // vertex blocks across the tile's 33 vertex columns
+    __shared__ VRef RB[kB2VB][2 * NBB];   // vrel: reference rays of the owner blocks (see VRef)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ix = blockIdx.x * 32 + lane;
     const int iy = blockIdx.y * 8 + w;
@@ -390,28 +401,24 @@ __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, 
         const float pxl = vertex_px(g, vx0 + lane), pxe = vertex_px(g, vx0 + 32);
         const float pyw = vertex_py(g, vy0 + w), pye = vertex_py(g, vy0 + 8), pyl = vertex_py(g, vy0 + min(lane, 8));
         const float xc = fmaf((float)ix, g.dx, g.x0), yc = fmaf((float)iy, g.dy, g.y0);
-        // vrel: this tile's rows lie in 32-block row by32; the top vertex row may be the next's
-        const int by32 = vy0 >> 5, yoff = vy0 & 31;
-        const bool top_next = yoff + 8 == 32;
-        const float dil = (float)(lane - 16), djw = (float)(yoff + w - 16);
-        const float djt = top_next ? -16.0f : (float)(yoff + 8 - 16), djl = (float)(yoff + min(lane, 8) - 16);
+        // vrel: the tile's 9 vertex rows lie in vertex-block rows by0 (rows 0-7) and by0 + 1 (row 8)
+        const int bx0 = vx0 / kVB, by0 = vy0 / kVB;
         for (int kb = 0; kb < count; kb += kB2VB) {
             const int nb = min(kB2VB, count - kb);
             if (VREL) {
-                if (threadIdx.x < 4 * nb) {
-                    const int kk = threadIdx.x >> 2, q = threadIdx.x & 3;
+                if (threadIdx.x < 2 * NBB * nb) {
+                    const int kk = threadIdx.x / (2 * NBB), q = threadIdx.x - kk * (2 * NBB);
                     const float4 vw = __ldg(&g.views[first + (kb + kk) * stride]);
-                    RB[kk][q] = make_vref(g, vw.x, vw.y, blockIdx.x + (q & 1), by32 + (q >> 1));
+                    RB[kk][q] = make_vref(g, vw.x, vw.y, bx0 + q % NBB, by0 + q / NBB);
                 }
                 __syncthreads();
                 for (int kk = 0; kk < nb; kk++) {
                     const VRef* R = RB[kk];
-                    V[kk][w][lane] = vertex_rel(g, R[0], dil, djw);
+                    V[kk][w][lane] = vertex_tab<NBB>(g, R, bx0, by0, vx0 + lane, vy0 + w);
                     if ((kk & 7) == w) {
-                        V[kk][8][lane] = vertex_rel(g, R[top_next ? 2 : 0], dil, djt);   // top row
-                        if (lane <= 8)                                                    // right column
-                            V[kk][lane][32] = vertex_rel(g, R[(lane == 8 && top_next) ? 3 : 1], -16.0f,
-                                                         lane == 8 ? djt : djl);
+                        V[kk][8][lane] = vertex_tab<NBB>(g, R, bx0, by0, vx0 + lane, vy0 + 8);   // top row
+                        if (lane <= 8)                                                            // right column
+                            V[kk][lane][32] = vertex_tab<NBB>(g, R, bx0, by0, vx0 + 32, vy0 + lane);
                         if (lane == 0) {
                             const float4 vw = __ldg(&g.views[first + (kb + kk) * stride]);
                             SC[kk] = make_float2(vw.x, vw.y);
