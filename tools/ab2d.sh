@@ -1,6 +1,6 @@
 # A/B timing of 2D tuning variants (same box, same call): projector pair and the c2 bench step
 python -c "import __graft_entry__ as g; g.build()"
-VARS=${VARS:-"base: S1:-DCT_BACK2D_SPLIT=1 S3:-DCT_BACK2D_SPLIT=3"}
+VARS=${VARS:-"base: F5:-DCT_FWD2D_MINB=5 B5:-DCT_BACK2D_MINB=5"}
 for v in $VARS; do
   name=${v%%:*}; flags=${v#*:}
   [ "$name" = base ] || python -m paper_1402_4381_b200.build --out paper_1402_4381_b200/tune_$name.so $flags > /dev/null
