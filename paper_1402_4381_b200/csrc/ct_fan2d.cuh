@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(256) fwd2d_finalize_kernel(DevGeom g, int firs
 // vertex table for every view (warp w: vertex row w; the top row and right column of
 // view kk by warp kk % 8), then thread = pixel walks the batch's views.
 constexpr int kB2VB = 16;   // views per vertex-table batch
+static_assert(2 * (32 / kVB + 1) * kB2VB <= 256, "back2d: one thread per (view, reference block) of a batch");
 
 template <int EPI, bool VREL>
 __global__ void __launch_bounds__(256, CT_BACK2D_MINB) back2d_kernel(DevGeom g, int first, int stride, int count,
