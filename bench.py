@@ -1,20 +1,23 @@
 #!/usr/bin/env python
 """bench.py — OS-LALM CT hot path on B200 (BASELINE.json metric).
 
-A step = one complete reconstruction job of the chosen config (default c2 = BASELINE
-configs[1]): the SQS denominator D_L = A'WA1 (one full forward/back pair, S8), then
-n_iter OS-LALM iterations (M inner steps each: K3 update, K1 forward + fused residual,
-K2 back-projection + fused g-update/xi, K4 rho continuation).  Inputs are synthetic
-(seeded phantom, Poisson noise) and resident in HBM when the timed region starts.
+A step = one OS-LALM outer iteration (BASELINE.md T_iter) of the chosen config (default c5 =
+BASELINE configs[4], the helical scaling config the metric is quoted on at 1/2/4/8 GPUs):
+M inner steps, each K3 update, K1 forward projection + fused weighted residual, K2
+back-projection + fused g-update / xi, K4 rho continuation.  The setup (D_L = A'WA1, the
+support, the initial image) runs once before the warm-up and is reported as setup_ms.
+The W warm-up and K timed steps are iterations 1..W and W+1..W+K of one reconstruction.
+Inputs are synthetic (seeded phantom, Poisson noise) and resident in HBM.
 
-value  = voxel-ray updates/s = (work of every projection in the step, counted as U per
-         projection, U = #(view, voxel in S) pairs with a non-empty footprint) / time.
-iters_per_s = n_iter / (time of the n_iter iterations, D_L excluded).
+value  = voxel-ray updates/s = 2 U (one forward and one back-projection of every view per
+         iteration, U = #(view, voxel in S) pairs with a non-empty footprint) / T_iter.
+iters_per_s = 1 / T_iter.
 
-Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
-For N > 1 launch with torch.distributed.run (one rank per GPU); views of every subset
-are split into contiguous blocks per rank and the partial back-projections are summed
-with NCCL (strong scaling).
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+--gpus N > 1 launches itself under torch.distributed.run when WORLD_SIZE is unset (one rank
+per GPU); views of every subset are split into contiguous blocks per rank and the partial
+back-projections are reduce-scattered with NCCL (strong scaling); --zslab selects the
+z-slab decomposition instead.
 """
 from __future__ import annotations
 
@@ -135,105 +138,124 @@ def barrier(ws):
     torch.cuda.synchronize()
 
 
-def workload_name(cfg):
+def workload_name(cfg, n_iter=None):
     g = cfg.geom
     shape = f"{g['nx']}x{g['ny']}" + ("" if cfg.is2d else f"x{g['nz']}")
     det = f"{g['ns']}ch" + ("" if cfg.is2d else f"x{g['nt']}rows")
-    return (f"{cfg.name}: {g['kind']} {shape} image, {det}, {g['na']} views, M={cfg.M}, "
-            f"{cfg.n_iter} OS-LALM iterations + D_L setup")
+    return (f"{cfg.name}: {g['kind']} {shape} image, {det}, {g['na']} views, M={cfg.M}; "
+            f"one step = one OS-LALM outer iteration (M subset fwd/back pairs + M updates), "
+            f"the config's reconstruction is {n_iter or cfg.n_iter} iterations")
 
 
-def cpu_oracle_sample(cfg, budget_s=10.0):
-    """The fp64 oracle as it stands, on whole subsets of the workload (fwd + back)."""
+# views per reference-arm step: a bounded block of one subset (whole subsets for the small configs)
+REF_VIEWS = {"c1": 30, "c2": 41, "c3": 41, "c4": 64, "c5": 48}
+
+
+def oracle_chunk(cfg, x, mo, i, nv):
+    """One bounded oracle sample: forward + back projection of the first nv views of subset
+    pi[i mod M] (fp64, OpenMP over the host cores).  Returns the voxel-ray updates done."""
+    import oracle as O
+    g = cfg.geom
+    sub = O.bit_reversal(cfg.M)[i % cfg.M]
+    cnt = min(nv, O.nviews(g, sub, cfg.M))
+    p = O.fwd(g, x, sub, cfg.M, cnt)
+    O.back(g, p, sub, cfg.M, cnt)
+    return 2 * O.count_vv(g, mo, sub, cfg.M, cnt), cnt
+
+
+def oracle_inputs(cfg):
     import oracle as O
     from paper_1402_4381_b200 import inputs as I
-    g = cfg.geom
+    O.build()
     m = I.support_mask(cfg)
     mo = I.to_oracle_image(m).astype(np.uint8)
-    rng = np.random.default_rng(0)
-    x = rng.random(O.img_shape(g)) * 0.02 * mo
-    order = O.bit_reversal(cfg.M)
-    done, work, t0 = 0, 0, time.perf_counter()
+    x = np.random.default_rng(0).random(O.img_shape(cfg.geom)) * 0.02 * mo
+    return x, mo
+
+
+def cpu_oracle_sample(cfg, budget_s=15.0):
+    """The fp64 oracle as it stands, timed on bounded samples of the same workload."""
+    x, mo = oracle_inputs(cfg)
+    nv = REF_VIEWS.get(cfg.name, 32)
+    done, work, views, t0 = 0, 0, 0, time.perf_counter()
     while True:
-        sub = order[done % cfg.M]
-        cnt = O.nviews(g, sub, cfg.M)
-        p = O.fwd(g, x, sub, cfg.M, cnt)
-        O.back(g, p, sub, cfg.M, cnt)
-        work += 2 * O.count_vv(g, mo, sub, cfg.M, cnt)
-        done += 1
+        w, c = oracle_chunk(cfg, x, mo, done, nv)
+        work += w; views += c; done += 1
         if time.perf_counter() - t0 >= budget_s:
             break
     el = time.perf_counter() - t0
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": work / el, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{done} whole subset(s) of {cfg.name} (forward + back projection, fp64, OpenMP), {el:.1f} s"}
+            "sample": f"{done} block(s) of <= {nv} views of one subset each ({views} views) of {cfg.name}: "
+                      f"forward + back projection, fp64, OpenMP; {el:.1f} s"}
 
 
 def run_reference(args):
     """--impl reference: the oracle is this tier's reference arm (CPU, rank 0 only)."""
-    ws, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from paper_1402_4381_b200 import inputs as I
-    import oracle as O
-    O.build()
     cfg = I.config(args.config)
-    g = cfg.geom
-    m = I.support_mask(cfg)
-    mo = I.to_oracle_image(m).astype(np.uint8)
-    x = np.random.default_rng(0).random(O.img_shape(g)) * 0.02 * mo
-    order = O.bit_reversal(cfg.M)
-
-    def step(i):
-        sub = order[i % cfg.M]
-        cnt = O.nviews(g, sub, cfg.M)
-        p = O.fwd(g, x, sub, cfg.M, cnt)
-        O.back(g, p, sub, cfg.M, cnt)
-        return 2 * O.count_vv(g, mo, sub, cfg.M, cnt)
-
+    x, mo = oracle_inputs(cfg)
+    nv = REF_VIEWS.get(cfg.name, 32)
     for i in range(args.warmup):
-        step(i)
+        oracle_chunk(cfg, x, mo, i, nv)
     times, work = [], 0
     for i in range(args.steps):
         t0 = time.perf_counter()
-        w = step(args.warmup + i)
+        w, _ = oracle_chunk(cfg, x, mo, args.warmup + i, nv)
         times.append(time.perf_counter() - t0)
         work += w
     T = sum(times)
     value = work / T
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = f"per step: forward + back projection of the first <= {nv} views of one subset of {cfg.name} (fp64)"
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": workload_name(cfg) + " [reference step: one subset fwd+back]"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                            "sample": f"one whole subset of {cfg.name} per step (forward + back projection, fp64)"},
+           "config": {"workload": workload_name(cfg) + f" [reference step: {nv} views of one subset, fwd+back]",
+                      "config_id": cfg.name},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     return 0
 
 
+def spawn_ranks(n):
+    """--gpus N without a torchrun environment: re-launch this command under
+    torch.distributed.run with one rank per GPU (rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=20, help="timed OS-LALM outer iterations")
+    ap.add_argument("--warmup", type=int, default=3, help="untimed iterations before the timed ones")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--iters", type=int, default=None, help="override n_iter (default: the config's)")
     ap.add_argument("--inner", default="sqs", choices=("sqs", "fista"), help="inner solver (NEXT-1: fista)")
     ap.add_argument("--n-inner", type=int, default=1, help="inner FISTA iterations (with --inner fista)")
     ap.add_argument("--bb", action="store_true", help="Barzilai-Borwein scaling of the SQS Hessian (NEXT-2)")
     ap.add_argument("--zslab", action="store_true",
                     help="cone beam: z-slab decomposition over the ranks, partial sinograms summed (NEXT-3)")
     ap.add_argument("--init", default="zero", choices=("zero", "fbp"),
-                    help="initial image: zero on S (G10) or the FBP/FDK image (NEXT-4, P:586; inside the timed step)")
+                    help="initial image: zero on S (G10) or the FBP/FDK image (NEXT-4, P:586)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
 
     ws, rank, local = dist_setup()
     torch.cuda.set_device(local)
@@ -245,16 +267,15 @@ def main():
         barrier(ws)
     ctlib.load()
     cfg = I.config(args.config)
-    n_iter = args.iters or cfg.n_iter
     g = cfg.geom
     dev = torch.device("cuda", local)
+    st = torch.cuda.current_stream()
 
     # ---- inputs (synthetic, seeded), resident in HBM
     data = I.synthesize(cfg, device=dev, views_per_chunk=8 if not cfg.is2d else 128)
     y, w = data["y"].contiguous(), data["w"].contiguous()
     del data
     m0 = I.support_mask(cfg, device=dev)
-    g_full = g
     if args.zslab:   # NEXT-3: this rank's z-slab of the volume (its own geometry)
         from paper_1402_4381_b200.host import rank_zslab
         z0, z1 = rank_zslab(g["nz"], rank, ws)
@@ -274,89 +295,92 @@ def main():
     sol = ctlib.OSLALM(geo, cfg.M, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr, inner=args.inner,
                        n_inner=args.n_inner, bb=args.bb)
     sol.set_data(y, w, dl, mask)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    fbp_scratch = (torch.empty(ctlib.ct_fbp_scratch_bytes(geo.h), dtype=torch.uint8, device=dev)
-                   if args.init == "fbp" else None)
+    N = int(np.prod(geo.img_shape))
+    ws_bytes = (y.numel() + w.numel() + 6 * N) * 4        # y, W and the image-sized state
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if ws_bytes < 4 * l2_bytes else None
 
-    def step(ev=None):
+    # ---- setup (reported separately): D_L = A'WA1 and the support (S8), the initial image
+    def setup():
         mask.copy_(m0)
         ctlib.ct_sqs_denom(geo.h, w, mask, dl, scratch)
-        if ev is not None:
-            ev.record()
         sol.reset()
         if args.init == "fbp":
-            ctlib.ct_fbp(geo.h, y, x, fbp_scratch)
+            fs = torch.empty(ctlib.ct_fbp_scratch_bytes(geo.h), dtype=torch.uint8, device=dev)
+            ctlib.ct_fbp(geo.h, y, x, fs)
         else:
             x.zero_()
-        for _ in range(n_iter):
-            sol.iterate(x)
 
-    # ---- work counts (fp64 geometry on the device; once, outside any timed region)
-    step()
-    torch.cuda.synchronize()
-    U0, nnz0, C0 = geo.counts(m0)
+    setup()                                      # untimed first call (lazy module / smem setup)
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    setup()
+    e1.record(st)
+    barrier(ws)
+    setup_ms = allreduce_max(e0.elapsed_time(e1), ws)
+
+    # ---- work counts (fp64 geometry on the device; outside any timed region)
     U, nnz, C = geo.counts(mask)
-    from paper_1402_4381_b200.host import subset_views
-    # the first subset of the bit-reversal order is subset 0 (initial G, reading G10)
-    Ui = geo.counts(mask, subset_views(g["na"], cfg.M, 0))[0]
-    work = 2 * U0 + 2 * Ui + n_iter * 2 * U
-    local_counts = (nnz, U, C)          # this rank's kernels' work (a slab's voxels with --zslab)
-    if args.zslab and ws > 1:           # the slabs partition the voxels: the job's work is their sum
+    work_step = 2 * U                            # one forward + one back-projection of every view
+    local_counts = (nnz, U, C)                   # this rank's geometry (a slab's voxels with --zslab)
+    if args.zslab and ws > 1:                    # the slabs partition the voxels: the job's work is their sum
         import torch.distributed as dist
-        t = torch.tensor([work, U, nnz], dtype=torch.float64, device=dev)
+        t = torch.tensor([work_step, U, nnz], dtype=torch.float64, device=dev)
         dist.all_reduce(t)
-        work, U, nnz = (int(v) for v in t.tolist())
+        work_step, U, nnz = (int(v) for v in t.tolist())
 
-    # ---- warm-up (also captures the CUDA graph); the clock sampler starts here so that it is
-    # sampling (nvidia-smi needs ~0.3 s to start) when the timed region begins
+    # ---- warm-up iterations (the first computes the initial subset gradient and captures the
+    # CUDA graph); the clock sampler starts here so that it samples the timed region
     clk = ClockSampler(local).__enter__()
-    for _ in range(args.warmup):
-        step()
+    for _ in range(max(args.warmup, 1)):
+        sol.iterate(x)
     barrier(ws)
 
-    # ---- timed region: K steps, L2 flushed between steps (not timed)
-    st = torch.cuda.current_stream()
+    # ---- timed region: K outer iterations (iterations W+1 .. W+K of one reconstruction)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     l0 = ctlib.ct_kernel_launches()
     try:
-        # samples cover the warm-up steps and the timed region (same load)
         barrier(ws)
         for i in range(args.steps):
-            flush.zero_()
+            if flush is not None:
+                flush.zero_()
             starts[i].record(st)
-            step(mids[i])
+            sol.iterate(x)
             ends[i].record(st)
         barrier(ws)
     finally:
         clk.__exit__(None, None, None)
     launches = ctlib.ct_kernel_launches() - l0
     T = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / 1e3
-    Ti = sum(m.elapsed_time(e) for m, e in zip(mids, ends)) / 1e3
     T = allreduce_max(T, ws)
-    Ti = allreduce_max(Ti, ws)
-    value = work * args.steps / T
-    iters_per_s = n_iter * args.steps / Ti
+    value = work_step * args.steps / T
 
-    # ---- per-kernel timing pass (CUDA events around every kernel, same stream)
+    # forward-projection trimming skips voxel columns whose x is zero along a whole image line
+    # end: the S voxels in all-zero columns bound the work counted but not executed
+    colzero = (x == 0).all(dim=2) & (mask != 0).any(dim=2)
+    skipped_frac = float((mask.sum(dim=2) * colzero).sum().item()) / max(1.0, float(mask.sum().item()))
+
+    # ---- per-kernel timing pass: one more iteration with CUDA events around every kernel on
+    # the launching stream (eager launches, no graph)
     sol.set_timing(True)
-    flush.zero_()
-    step()
+    if flush is not None:
+        flush.zero_()
+    sol.iterate(x)
     torch.cuda.synchronize()
     kt = sol.timing()
     sol.set_timing(False)
-    sol.reset()
     pk = peaks()
     M = cfg.M
     # algorithmic FLOPs per projection launch: 2 nnz + 15 U + 150 C, per subset = full / M
     lnnz, lU, lC = local_counts
-    flop_launch = (2 * lnnz + 15 * lU + 150 * lC) / M / (1 if args.zslab else ws)
+    share = 1 if args.zslab else ws
+    flop_launch = (2 * lnnz + 15 * lU + 150 * lC) / M / share
     dom = max(("fwd_resid", "back_gupd"), key=lambda k: kt[k][0])
     ms_launch = kt[dom][0] / max(kt[dom][1], 1)
     achieved = flop_launch / (ms_launch / 1e3) / 1e12
     total_kt = sum(v[0] for v in kt.values())
-    N = int(np.prod(geo.img_shape))
     upd_ms = kt["sqs_update"][0] / max(kt["sqs_update"][1], 1)
     # x, G, g, D_L read (16 B) + mask (1 B) + x' write (4 B) per updated voxel (row-slab ranks update N/P)
     upd_bytes = 21 * N / (ws if (ws > 1 and not args.zslab and args.inner == "sqs") else 1)
@@ -367,6 +391,10 @@ def main():
                 "peak_src": f"derived: {N_SM} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
                 "flop_per_launch": flop_launch, "ms_per_launch": ms_launch,
                 "share_of_step": kt[dom][0] / total_kt}
+    # the projector's compulsory DRAM bytes per launch: the image once + the subset sinogram
+    # (y, W read, residual written and read back by the back-projector)
+    cells_sub = (g["na"] // M) * g["ns"] * (1 if cfg.is2d else g["nt"])
+    roofline["algorithmic_dram_bytes"] = 4 * N + 16 * cells_sub
     streaming = {"bound": "hbm", "kernel": "sqs_update", "achieved": upd_bytes / (upd_ms / 1e3) / 1e9,
                  "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": upd_bytes / (upd_ms / 1e3) / 1e9 / pk["hbm_gbs"],
                  "traffic": traffic.get("sqs_update", {}).get("bytes_per_launch"), "bytes_per_launch": upd_bytes,
@@ -376,35 +404,43 @@ def main():
     # through L2 once, T = max(T_HBM, 4 B nnz / BW_L2), BW_L2 = L2-resident read bandwidth
     # measured here (no vendor number available)
     l2 = ctlib.ct_peak_l2_read(local)
-    gather_bytes = 4.0 * lnnz / M / (1 if args.zslab else ws)
-    roofline_gather = {"bound": "l2-gather", "kernel": dom, "achieved": gather_bytes / (ms_launch / 1e3) / 1e9,
-                       "peak": l2, "unit": "GB/s", "frac": gather_bytes / (ms_launch / 1e3) / 1e9 / l2,
-                       "bytes_per_launch": gather_bytes, "peak_src": "measured in this run: ct_peak_l2_read (48 MiB buffer streamed 200x, float4 loads)"}
+    gather_bytes = 4.0 * lnnz / M / share
+    rg = {}
+    for k in ("fwd_resid", "back_gupd"):
+        ms_k = kt[k][0] / max(kt[k][1], 1)
+        rg[k] = {"achieved": gather_bytes / (ms_k / 1e3) / 1e9, "frac": gather_bytes / (ms_k / 1e3) / 1e9 / l2,
+                 "ms_per_launch": ms_k}
+    roofline_gather = {"bound": "l2-gather", "kernel": dom, "achieved": rg[dom]["achieved"],
+                       "peak": l2, "unit": "GB/s", "frac": rg[dom]["frac"], "per_kernel": rg,
+                       "bytes_per_launch": gather_bytes,
+                       "peak_src": "measured in this run: ct_peak_l2_read (48 MiB buffer streamed 200x, float4 loads)"}
 
-    # ---- end to end: host (pinned) inputs in, image out, inside the timed region
+    # ---- end to end through the C ABI: every step copies that step's inputs (y, W) from pinned
+    # host memory to the device and reads the iterate back, inside the timed region
     e2e = None
     if not args.no_e2e:
         y_h = y.cpu().pin_memory(); w_h = w.cpu().pin_memory()
         x_h = torch.empty(x.shape, dtype=torch.float32).pin_memory()
         y2, w2 = torch.empty_like(y), torch.empty_like(w)
-        sol.set_data(y2, w2, dl, mask)
-        es = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
         y2.copy_(y_h); w2.copy_(w_h)
-        step()                                   # capture the graph for the new buffers
+        sol.set_data(y2, w2, dl, mask)
+        sol.iterate(x)                           # capture the graph for the new buffers (untimed)
         x_h.copy_(x)
+        es = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
         barrier(ws)
         for i in range(args.steps):
-            flush.zero_()
+            if flush is not None:
+                flush.zero_()
             es[2 * i].record(st)
             y2.copy_(y_h, non_blocking=True)
             w2.copy_(w_h, non_blocking=True)
-            step()
+            sol.iterate(x)
             x_h.copy_(x, non_blocking=True)
             es[2 * i + 1].record(st)
         barrier(ws)
         Te = sum(es[2 * i].elapsed_time(es[2 * i + 1]) for i in range(args.steps)) / 1e3
         Te = allreduce_max(Te, ws)
-        e2e = {"value": work * args.steps / Te, "unit": UNIT,
+        e2e = {"value": work_step * args.steps / Te, "unit": UNIT,
                "h2d_bytes_per_step": int(y.numel() * 4 + w.numel() * 4), "d2h_bytes_per_step": int(x.numel() * 4),
                "ms_per_step": 1e3 * Te / args.steps}
 
@@ -417,15 +453,19 @@ def main():
 
     if rank == 0:
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "iters_per_s": iters_per_s, "setup_ms_per_step": 1e3 * (T - Ti) / args.steps,
-            "config": {"workload": workload_name(cfg), "config_id": cfg.name, "M": cfg.M, "n_iter": n_iter,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "iters_per_s": args.steps / T, "setup_ms": setup_ms,
+            "config": {"workload": workload_name(cfg), "config_id": cfg.name, "M": cfg.M, "n_iter": cfg.n_iter,
+                       "step": "one OS-LALM outer iteration", "timed_iterations": f"{args.warmup + 1}..{args.warmup + args.steps}",
                        "inner": f"{args.inner} x{args.n_inner}" + (" + BB" if args.bb else ""), "init": args.init,
                        "views_per_subset": (g["na"] + cfg.M - 1) // cfg.M, "U_full_scan": U,
-                       "nnz_full_scan": nnz, "work_per_step": work,
-                       "l2": "flushed between steps (512 MiB write, untimed)",
+                       "nnz_full_scan": nnz, "work_per_step": work_step,
+                       "work_skipped_frac_bound": skipped_frac,
+                       "setup": "D_L = A'WA1 + support + initial image, timed separately (setup_ms)",
+                       "l2": ("flushed between steps (512 MiB write, untimed)" if flush is not None else
+                              f"inputs larger than L2 ({ws_bytes / 1e9:.2f} GB vs {l2_bytes / 1e6:.0f} MB); no flush"),
                        "parallelism": (f"z-slabs over {ws} GPU(s): partial sinograms all-reduced, slab "
                                        "back-projection and update, 1-slice halos" if args.zslab else
                                        f"views of each subset split over {ws} GPU(s); NCCL reduce-scatter of G+ "
@@ -434,6 +474,7 @@ def main():
             "roofline_gather": roofline_gather,
             "kernel_ms": kernel_ms, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
             "peaks": {"fp32_tflops": pk["fp32_tflops"], "hbm_gbs": pk["hbm_gbs"], "src": pk["src"]},
+            "build": ctlib.ct_build_info(),
         }
         print(json.dumps(out))
     if ws > 1:

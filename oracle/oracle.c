@@ -179,6 +179,32 @@ static void chan_range(const or_geom* g, const or_trans* tr, int* c0, int* c1) {
 static int nzv(const or_geom* g) { return g->kind == OR_FAN2D ? 1 : g->nz; }
 static int ntv(const or_geom* g) { return g->kind == OR_FAN2D ? 1 : g->nt; }
 
+/* Loop bounds only (no arithmetic): the detector rows [r0, r1] whose bins can intersect
+ * the axial rect [tm, tp], widened by one row on each side; every row outside has
+ * Ft = 0 exactly, and the loops still test Ft != 0, so the sums are term-for-term (and
+ * bit-for-bit) those of a loop over all rows. */
+static void row_range(const or_geom* g, double tm, double tp, int* r0, int* r1) {
+    double base = -(g->nt - 1) / 2.0 - g->offt;
+    int a = (int)floor(tm / g->dt - base - 0.5) - 1;
+    int b = (int)floor(tp / g->dt - base + 0.5) + 1;
+    *r0 = a < 0 ? 0 : a;
+    *r1 = b > g->nt - 1 ? g->nt - 1 : b;
+}
+
+/* Loop bounds only: the slices whose axial rect (at the column's magnification) can meet
+ * the detector rows, widened by one slice on each side; for every slice outside, all Ft
+ * are 0 (same remark as row_range). */
+static void slice_range(const or_geom* g, const or_trans* tr, double zs, int* z0, int* z1) {
+    if (g->kind == OR_FAN2D) { *z0 = 0; *z1 = 0; return; }
+    double mag = g->dsd / tr->rho_h;
+    double t_lo = row_t(g, 0) - g->dt / 2, t_hi = row_t(g, g->nt - 1) + g->dt / 2;
+    double za = zs + t_lo / mag - g->dz / 2, zb = zs + t_hi / mag + g->dz / 2;
+    double ia = (za - g->offz) / g->dz + (g->nz - 1) / 2.0, ib = (zb - g->offz) / g->dz + (g->nz - 1) / 2.0;
+    int a = (int)floor(ia) - 1, b = (int)ceil(ib) + 1;
+    *z0 = a < 0 ? 0 : a;
+    *z1 = b > g->nz - 1 ? g->nz - 1 : b;
+}
+
 /* Forward projection  p[k][r][c] = sum_j a_{(v_k,r,c), j} x_j  over views
  * v_k = first + k*stride, k < count.  x may be masked by mask (NULL = all). */
 void or_fwd(const or_geom* g, int first, int stride, int count, const double* x, double* p) {
@@ -196,10 +222,12 @@ void or_fwd(const or_geom* g, int first, int stride, int count, const double* x,
                 transaxial(g, beta, vox_x(g, ix), vox_y(g, iy), &tr);
                 int c0, c1;
                 chan_range(g, &tr, &c0, &c1);
+                int z0, z1;
+                slice_range(g, &tr, zs, &z0, &z1);
                 for (int c = c0; c <= c1; c++) {
                     double fs = Fs(g, &tr, c);
                     if (fs == 0.0) continue;
-                    for (int iz = 0; iz < NZ; iz++) {
+                    for (int iz = z0; iz <= z1; iz++) {
                         double xv = x[((size_t)iz * g->ny + iy) * g->nx + ix];
                         if (xv == 0.0) continue;
                         if (g->kind == OR_FAN2D) {
@@ -207,8 +235,10 @@ void or_fwd(const or_geom* g, int first, int stride, int count, const double* x,
                             continue;
                         }
                         double tm, tp, lth;
+                        int r0, r1;
                         axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
-                        for (int r = 0; r < NT; r++) {
+                        row_range(g, tm, tp, &r0, &r1);
+                        for (int r = r0; r <= r1; r++) {
                             double ft = Ft(g, tm, tp, r);
                             if (ft != 0.0) pv[(size_t)r * g->ns + c] += tr.lphi * lth * fs * ft * xv;
                         }
@@ -234,17 +264,21 @@ void or_back(const or_geom* g, int first, int stride, int count, const double* p
                 transaxial(g, beta, vox_x(g, ix), vox_y(g, iy), &tr);
                 int c0, c1;
                 chan_range(g, &tr, &c0, &c1);
+                int z0, z1;
+                slice_range(g, &tr, zs, &z0, &z1);
                 for (int c = c0; c <= c1; c++) {
                     double fs = Fs(g, &tr, c);
                     if (fs == 0.0) continue;
-                    for (int iz = 0; iz < NZ; iz++) {
+                    for (int iz = z0; iz <= z1; iz++) {
                         double acc = 0.0;
                         if (g->kind == OR_FAN2D) {
                             acc = tr.lphi * fs * pv[c];
                         } else {
                             double tm, tp, lth;
+                            int r0, r1;
                             axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
-                            for (int r = 0; r < NT; r++) {
+                            row_range(g, tm, tp, &r0, &r1);
+                            for (int r = r0; r <= r1; r++) {
                                 double ft = Ft(g, tm, tp, r);
                                 if (ft != 0.0) acc += tr.lphi * lth * fs * ft * pv[(size_t)r * g->ns + c];
                             }
