@@ -148,7 +148,7 @@ def workload_name(cfg, n_iter=None):
 
 
 # views per reference-arm step: a bounded block of one subset (whole subsets for the small configs)
-REF_VIEWS = {"c1": 30, "c2": 41, "c3": 41, "c4": 64, "c5": 48}
+REF_VIEWS = {"c1": 30, "c2": 41, "c3": 16, "c4": 24, "c5": 16}
 
 
 def oracle_chunk(cfg, x, mo, i, nv):

@@ -287,12 +287,18 @@ int ct_oslalm_run(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_da
                   float* x, int n_iter, ct_oslalm_log* log, void* stream);
 
 /*
- * Multi-GPU: attach an NCCL communicator to the geometry.
- * `nccl_uid` points to the 128-byte ncclUniqueId created by rank 0 and broadcast
- * by the caller (torch.distributed).  Afterwards ct_oslalm_iter/run on this
- * geometry process only this rank's contiguous block of each subset's views and
- * sum the partial back-projections with ncclAllReduce (fp32) before the g-update.
- * NCCL is loaded at run time (libnccl.so.2); CT_ENCCL if unavailable.
+ * Multi-GPU (BASELINE.json north_star "each subset's views are
+ * sharded over GPUs ... the partial back-projections are combined"): attach an NCCL
+ * communicator to the geometry.  `nccl_uid` points to the 128-byte ncclUniqueId created by
+ * rank 0 (ct_comm_get_unique_id) and broadcast by the caller (torch.distributed).
+ * Afterwards ct_oslalm_iter/run on this geometry process only this rank's contiguous block
+ * of each subset's views; with the SQS inner step the ranks own padded row slabs of the
+ * image: the partial back-projections are combined by ncclReduceScatter (fp32) into the row
+ * slabs, the g-update, xi partial and K3 update run on the rank's slab, xi is all-reduced
+ * (fp64, 8 bytes) and the updated slabs are all-gathered (ncclAllGather) for the next forward
+ * projection.  The FISTA inner solver all-reduces full images instead.  D_L sums the ranks'
+ * partial back-projections with ncclAllReduce.  NCCL is loaded at run time (libnccl.so.2);
+ * CT_ENCCL if unavailable.  Call before creating OS-LALM states (CT_ESTATE otherwise).
  */
 int ct_comm_init(ct_geom* g, int rank, int nranks, const void* nccl_uid);
 /*
@@ -309,6 +315,21 @@ int ct_comm_init(ct_geom* g, int rank, int nranks, const void* nccl_uid);
  */
 int ct_comm_init_zslab(ct_geom* g, int rank, int nranks, const void* nccl_uid128);
 int ct_comm_get_unique_id(void* nccl_uid_out128);
+
+/*
+ * Virtual ranks (validation of the multi-rank path on ONE device):
+ * attach `nranks` distinct geometry handles gs[0..nranks-1] of one device to one group of
+ * virtual ranks (rank r = gs[r]; zslab != 0: gs[r] is rank r's z-slab geometry, as for
+ * ct_comm_init_zslab).  Every exchange step of the multi-rank path then runs as a
+ * rendezvous of the ranks' host threads: each rank must be driven by its own thread on its
+ * own stream (ct_oslalm_iter / ct_sqs_denom of all ranks concurrently, in the same order);
+ * the collective's copies and fixed-order (rank 0..P-1) sum kernels run on a group stream
+ * ordered by CUDA events after every rank's stream, and every rank's stream waits for them.
+ * No kernel waits on another kernel.  Replaces any communicator attached before.
+ * Errors: CT_EINVAL (null / duplicate handles, different devices), CT_EUNSUPPORTED (zslab on
+ * a fan geometry), CT_ECUDA.  A failed exchange returns CT_ENCCL on every rank.
+ */
+int ct_comm_init_virtual(ct_geom** gs, int nranks, int zslab);
 
 /* Library identification string (kernel names, target). */
 const char* ct_build_info(void);

@@ -205,6 +205,25 @@ static void slice_range(const or_geom* g, const or_trans* tr, double zs, int* z0
     *z1 = b > g->nz - 1 ? g->nz - 1 : b;
 }
 
+/* Loop bound only: 0 if no voxel of the volume can meet the detector rows from a source at
+ * height zs (helical scans; every a_ij of the view is then exactly 0 and the view's terms
+ * are skipped), 1 otherwise.  Any voxel's magnification lies in [dsd/(dso + rmax),
+ * dsd/(dso - rmax)] (rmax >= in-plane distance of any voxel centre from the axis), so its
+ * axial rect can only meet [t_lo, t_hi] if its z-extent meets zs + [t_lo, t_hi] / mag; the
+ * test is widened by one slice on each side. */
+static int view_sees_volume(const or_geom* g, double zs) {
+    if (g->kind != OR_CONE_HELICAL) return 1;
+    double hx = 0.5 * (g->nx - 1) * g->dx + fabs(g->offx) + g->dx;
+    double hy = 0.5 * (g->ny - 1) * g->dy + fabs(g->offy) + g->dy;
+    double rmax = sqrt(hx * hx + hy * hy);
+    if (rmax >= g->dso) return 1;
+    double mlo = g->dsd / (g->dso + rmax), mhi = g->dsd / (g->dso - rmax);
+    double t_lo = row_t(g, 0) - g->dt / 2, t_hi = row_t(g, g->nt - 1) + g->dt / 2;
+    double a = fmin(t_lo / mlo, t_lo / mhi), b = fmax(t_hi / mlo, t_hi / mhi);
+    double zlo = vox_z(g, 0) - g->dz / 2, zhi = vox_z(g, g->nz - 1) + g->dz / 2;
+    return (zlo - g->dz < zs + b) && (zhi + g->dz > zs + a);
+}
+
 /* Forward projection  p[k][r][c] = sum_j a_{(v_k,r,c), j} x_j  over views
  * v_k = first + k*stride, k < count.  x may be masked by mask (NULL = all). */
 void or_fwd(const or_geom* g, int first, int stride, int count, const double* x, double* p) {
@@ -216,6 +235,7 @@ void or_fwd(const or_geom* g, int first, int stride, int count, const double* x,
         double* pv = p + (size_t)k * cells;
         memset(pv, 0, cells * sizeof(double));
         double beta = or_view_angle(g, v), zs = or_source_z(g, v);
+        if (!view_sees_volume(g, zs)) continue;
         for (int iy = 0; iy < g->ny; iy++)
             for (int ix = 0; ix < g->nx; ix++) {
                 or_trans tr;
@@ -224,20 +244,30 @@ void or_fwd(const or_geom* g, int first, int stride, int count, const double* x,
                 chan_range(g, &tr, &c0, &c1);
                 int z0, z1;
                 slice_range(g, &tr, zs, &z0, &z1);
-                for (int c = c0; c <= c1; c++) {
-                    double fs = Fs(g, &tr, c);
-                    if (fs == 0.0) continue;
-                    for (int iz = z0; iz <= z1; iz++) {
-                        double xv = x[((size_t)iz * g->ny + iy) * g->nx + ix];
-                        if (xv == 0.0) continue;
-                        if (g->kind == OR_FAN2D) {
+                if (c1 < c0) continue;
+                /* F_s of the column's channels; slices outer, channels inner: every cell
+                 * (r, c) still receives its terms in increasing iz (column by column), the
+                 * same order as with channels outer, so the sums are bit-identical */
+                double fsv[c1 - c0 + 1];
+                for (int c = c0; c <= c1; c++) fsv[c - c0] = Fs(g, &tr, c);
+                for (int iz = z0; iz <= z1; iz++) {
+                    double xv = x[((size_t)iz * g->ny + iy) * g->nx + ix];
+                    if (xv == 0.0) continue;
+                    if (g->kind == OR_FAN2D) {
+                        for (int c = c0; c <= c1; c++) {
+                            double fs = fsv[c - c0];
+                            if (fs == 0.0) continue;
                             pv[c] += tr.lphi * fs * xv;
-                            continue;
                         }
-                        double tm, tp, lth;
-                        int r0, r1;
-                        axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
-                        row_range(g, tm, tp, &r0, &r1);
+                        continue;
+                    }
+                    double tm, tp, lth;
+                    int r0, r1;
+                    axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
+                    row_range(g, tm, tp, &r0, &r1);
+                    for (int c = c0; c <= c1; c++) {
+                        double fs = fsv[c - c0];
+                        if (fs == 0.0) continue;
                         for (int r = r0; r <= r1; r++) {
                             double ft = Ft(g, tm, tp, r);
                             if (ft != 0.0) pv[(size_t)r * g->ns + c] += tr.lphi * lth * fs * ft * xv;
@@ -260,24 +290,32 @@ void or_back(const or_geom* g, int first, int stride, int count, const double* p
                 int v = first + k * stride;
                 const double* pv = p + (size_t)k * cells;
                 double beta = or_view_angle(g, v), zs = or_source_z(g, v);
+                if (!view_sees_volume(g, zs)) continue;
                 or_trans tr;
                 transaxial(g, beta, vox_x(g, ix), vox_y(g, iy), &tr);
                 int c0, c1;
                 chan_range(g, &tr, &c0, &c1);
                 int z0, z1;
                 slice_range(g, &tr, zs, &z0, &z1);
-                for (int c = c0; c <= c1; c++) {
-                    double fs = Fs(g, &tr, c);
-                    if (fs == 0.0) continue;
-                    for (int iz = z0; iz <= z1; iz++) {
+                if (c1 < c0) continue;
+                /* slices outer, channels inner: every x[iz] still receives its terms in
+                 * increasing c (view by view), as with channels outer: bit-identical sums */
+                double fsv[c1 - c0 + 1];
+                for (int c = c0; c <= c1; c++) fsv[c - c0] = Fs(g, &tr, c);
+                for (int iz = z0; iz <= z1; iz++) {
+                    double tm = 0.0, tp = 0.0, lth = 1.0;
+                    int r0 = 0, r1 = -1;
+                    if (g->kind != OR_FAN2D) {
+                        axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
+                        row_range(g, tm, tp, &r0, &r1);
+                    }
+                    for (int c = c0; c <= c1; c++) {
+                        double fs = fsv[c - c0];
+                        if (fs == 0.0) continue;
                         double acc = 0.0;
                         if (g->kind == OR_FAN2D) {
                             acc = tr.lphi * fs * pv[c];
                         } else {
-                            double tm, tp, lth;
-                            int r0, r1;
-                            axial_rect(g, &tr, vox_z(g, iz), zs, &tm, &tp, &lth);
-                            row_range(g, tm, tp, &r0, &r1);
                             for (int r = r0; r <= r1; r++) {
                                 double ft = Ft(g, tm, tp, r);
                                 if (ft != 0.0) acc += tr.lphi * lth * fs * ft * pv[(size_t)r * g->ns + c];

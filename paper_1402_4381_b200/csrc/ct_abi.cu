@@ -19,6 +19,7 @@
 #include "ct_kernels.cuh"
 #include "ct_fan2d.cuh"
 #include "ct_fbp.cuh"
+#include "ct_comm.cuh"
 
 using namespace ct;
 
@@ -142,6 +143,46 @@ static bool load_nccl() {
 
 static const char* nccl_err(ncclResult_t r) { return g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error"; }
 
+// One process per GPU: the exchange steps as NCCL calls on the caller's stream.
+struct NcclComm : Comm {
+    ncclComm_t comm = nullptr;
+    char err[256] = "";
+    const char* kind() const override { return "nccl"; }
+    const char* last_err() const override { return err; }
+    ~NcclComm() override {
+        if (comm && g_nccl.ok) g_nccl.CommDestroy(comm);
+    }
+    int rc(ncclResult_t r, const char* what) {
+        if (r == ncclSuccess) return 0;
+        snprintf(err, sizeof(err), "%s: %s", what, nccl_err(r));
+        return -1;
+    }
+    static ncclDataType_t nt(int dt) { return dt == COMM_F64 ? ncclFloat64 : dt == COMM_F32 ? ncclFloat32 : ncclUint8; }
+    int allreduce_sum(const void* send, void* recv, size_t n, int dt, cudaStream_t st) override {
+        return rc(g_nccl.AllReduce(send, recv, n, nt(dt), ncclSum, comm, st), "ncclAllReduce");
+    }
+    int reduce_scatter_sum(const float* send, float* recv, size_t n, cudaStream_t st) override {
+        return rc(g_nccl.ReduceScatter(send, recv, n, ncclFloat32, ncclSum, comm, st), "ncclReduceScatter");
+    }
+    int all_gather(const float* send, float* recv, size_t n, cudaStream_t st) override {
+        return rc(g_nccl.AllGather(send, recv, n, ncclFloat32, comm, st), "ncclAllGather");
+    }
+    int halo(const void* send_lo, const void* send_hi, void* recv_lo, void* recv_hi, size_t n, int dt,
+             cudaStream_t st) override {
+        ncclResult_t r = g_nccl.GroupStart();
+        if (rank > 0) {
+            if (r == ncclSuccess) r = g_nccl.Send(send_lo, n, nt(dt), rank - 1, comm, st);
+            if (r == ncclSuccess) r = g_nccl.Recv(recv_lo, n, nt(dt), rank - 1, comm, st);
+        }
+        if (rank < nranks - 1) {
+            if (r == ncclSuccess) r = g_nccl.Send(send_hi, n, nt(dt), rank + 1, comm, st);
+            if (r == ncclSuccess) r = g_nccl.Recv(recv_hi, n, nt(dt), rank + 1, comm, st);
+        }
+        ncclResult_t r2 = g_nccl.GroupEnd();
+        return rc(r != ncclSuccess ? r : r2, "z-slab halo exchange");
+    }
+};
+
 
 // ---------------------------------------------------------------------------
 // geometry
@@ -155,15 +196,16 @@ struct ct_geom {
     unsigned long long* acc2d = nullptr;   // fan 2D forward: [na][ns] 64-bit fixed-point sums (kept zero)
     int2* ext3d = nullptr;                 // cone forward: nonzero column range per image row / column
     int rank = 0, nranks = 1;
-    ncclComm_t comm = nullptr;
+    Comm* comm = nullptr;    // exchange backend (NcclComm / VirtualComm); owned
     int zslab = 0;   // NEXT-3: this geometry is rank `rank`'s z-slab of the volume (sinogram-domain sums)
 };
 
+static int comm_rc(const ct_geom* g, int rc) {
+    return rc ? fail(CT_ENCCL, "%s exchange: %s", g->comm->kind(), g->comm->last_err()) : CT_OK;
+}
+
 static int allreduce(const ct_geom* g, float* buf, size_t n, cudaStream_t st) {
-    ncclResult_t r = g_nccl.AllReduce(buf, buf, n, ncclFloat32, ncclSum, g->comm, st);
-    if (r != ncclSuccess)
-        return fail(CT_ENCCL, "ncclAllReduce: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error");
-    return CT_OK;
+    return comm_rc(g, g->comm->allreduce_sum(buf, buf, n, COMM_F32, st));
 }
 
 static inline int nz_of(const ct_geom* g) { return g->d.kind == CT_FAN2D ? 1 : g->d.nz; }
@@ -319,7 +361,7 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
 extern "C" void ct_geom_destroy(ct_geom* g) {
     if (!g) return;
     DeviceGuard guard(g->d.device);
-    if (g->comm && g_nccl.ok) g_nccl.CommDestroy(g->comm);
+    delete g->comm;
     cudaFree(g->d_views);
     cudaFree(g->d_vz);
     cudaFree(g->acc2d);
@@ -991,22 +1033,11 @@ static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* 
 template <class T>
 static int zslab_halo(const ct_geom* g, const T* x, T* send_lo, T* send_hi, T* recv_lo, T* recv_hi, cudaStream_t st) {
     const int ncols = g->d.nx * g->d.ny, nz = g->d.nz;
-    const ncclDataType_t dt = sizeof(T) == 1 ? ncclUint8 : ncclFloat32;
     zslice_pack_kernel<T><<<(ncols + 255) / 256, 256, 0, st>>>(x, nz, 0, send_lo, ncols);
     zslice_pack_kernel<T><<<(ncols + 255) / 256, 256, 0, st>>>(x, nz, nz - 1, send_hi, ncols);
     CT_LAUNCHED(2);
-    ncclResult_t r = g_nccl.GroupStart();
-    if (g->rank > 0) {
-        if (r == ncclSuccess) r = g_nccl.Send(send_lo, ncols, dt, g->rank - 1, g->comm, st);
-        if (r == ncclSuccess) r = g_nccl.Recv(recv_lo, ncols, dt, g->rank - 1, g->comm, st);
-    }
-    if (g->rank < g->nranks - 1) {
-        if (r == ncclSuccess) r = g_nccl.Send(send_hi, ncols, dt, g->rank + 1, g->comm, st);
-        if (r == ncclSuccess) r = g_nccl.Recv(recv_hi, ncols, dt, g->rank + 1, g->comm, st);
-    }
-    ncclResult_t r2 = g_nccl.GroupEnd();
-    if (r != ncclSuccess || r2 != ncclSuccess) return fail(CT_ENCCL, "z-slab halo exchange: %s", nccl_err(r != ncclSuccess ? r : r2));
-    return CT_OK;
+    return comm_rc(g, g->comm->halo(send_lo, send_hi, recv_lo, recv_hi, (size_t)ncols,
+                                    sizeof(T) == 1 ? COMM_U8 : COMM_F32, st));
 }
 
 
@@ -1054,8 +1085,7 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
         if (int e = launch_back<EPI_GUPD>(g, vw, rsino, nullptr, ga, st)) return e;
         tmark_end(s, st, 2, t1);
         int t2 = tmark(s, st);
-        ncclResult_t r = g_nccl.AllReduce(s->xi_ex, s->xi_ex + 1, 1, ncclFloat64, ncclSum, g->comm, st);
-        if (r != ncclSuccess) return fail(CT_ENCCL, "ncclAllReduce(xi): %s", nccl_err(r));
+        if (int e = comm_rc(g, g->comm->allreduce_sum(s->xi_ex, s->xi_ex + 1, 1, COMM_F64, st))) return e;
         ga.xi_out = nullptr;
         xi_rule_kernel<<<1, 256, 0, st>>>(ga, s->xi_ex + 1);
         CT_LAUNCHED(1);
@@ -1083,8 +1113,7 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
         if (int e = launch_back<EPI_STORE>(g, v, s->sino, s->Gtmp, ga, st)) return e;
         tmark_end(s, st, 2, t1);
         int t2 = tmark(s, st);
-        ncclResult_t r = g_nccl.ReduceScatter(s->Gtmp, Gnew + s->off0, s->S, ncclFloat32, ncclSum, g->comm, st);
-        if (r != ncclSuccess) return fail(CT_ENCCL, "ncclReduceScatter: %s", nccl_err(r));
+        if (int e = comm_rc(g, g->comm->reduce_scatter_sum(s->Gtmp, Gnew + s->off0, s->S, st))) return e;
         const size_t j0 = s->off0, j1 = std::min(s->N, s->off0 + s->S);
         if (epi == EPI_INIT) {
             if (j1 > j0) CT_CUDA(cudaMemcpyAsync(s->gs + j0, Gnew + j0, (j1 - j0) * 4, cudaMemcpyDeviceToDevice, st));
@@ -1095,8 +1124,7 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
         ga.G_new = Gnew;
         gupd_slab_kernel<<<nblk(std::max(j1, j0 + 1) - j0), 256, 0, st>>>(ga, j0, j1, s->xi_ex);
         CT_LAUNCHED(1);
-        r = g_nccl.AllReduce(s->xi_ex, s->xi_ex + 1, 1, ncclFloat64, ncclSum, g->comm, st);
-        if (r != ncclSuccess) return fail(CT_ENCCL, "ncclAllReduce(xi): %s", nccl_err(r));
+        if (int e = comm_rc(g, g->comm->allreduce_sum(s->xi_ex, s->xi_ex + 1, 1, COMM_F64, st))) return e;
         xi_rule_kernel<<<1, 256, 0, st>>>(ga, s->xi_ex + 1);
         CT_LAUNCHED(1);
         tmark_end(s, st, 4, t2);
@@ -1164,8 +1192,7 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
                 CT_LAUNCHED(1);
             }
             if (s->slab) {   // every rank needs the full x+ for its next forward projection
-                ncclResult_t r = g_nccl.AllGather(xb + s->off0, xb, s->S, ncclFloat32, g->comm, st);
-                if (r != ncclSuccess) return fail(CT_ENCCL, "ncclAllGather: %s", nccl_err(r));
+                if (int e = comm_rc(g, g->comm->all_gather(xb + s->off0, xb, s->S, st))) return e;
             }
         } else {
             // n warm-started FISTA iterations: v_0 = x_0 = x_k (= xa), result in xb
@@ -1215,8 +1242,7 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
         bb_alpha_kernel<<<nblk(std::max(bj1, bj0 + 1) - bj0), 256, 0, st>>>(bbA, bj0, bj1);
         kernels += 1;
         if (g->comm) {
-            ncclResult_t r = g_nccl.AllReduce(s->xi_ex + 2, s->xi_ex + 2, 2, ncclFloat64, ncclSum, g->comm, st);
-            if (r != ncclSuccess) return fail(CT_ENCCL, "ncclAllReduce(BB): %s", nccl_err(r));
+            if (int e = comm_rc(g, g->comm->allreduce_sum(s->xi_ex + 2, s->xi_ex + 2, 2, COMM_F64, st))) return e;
             bb_rule_kernel<<<1, 1, 0, st>>>(s->sc, s->xi_ex + 2, c.alpha_min);
             kernels += 1;
         }
@@ -1371,23 +1397,52 @@ extern "C" int ct_comm_init(ct_geom* g, int rank, int nranks, const void* uid) {
     if (!g || !uid) return fail(CT_EINVAL, "ct_comm_init: null argument");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CT_EINVAL, "bad rank %d of %d", rank, nranks);
     // nranks == 1 still creates a (trivial) communicator: the exchange path (partial
-    // back-projection, all-reduce, unfused g-update) then runs on one GPU, which is
-    // how the multi-GPU code path is exercised when only one GPU is available.
+    // back-projection, reduce-scatter, slab g-update, all-gather) then runs on one GPU.
     if (!load_nccl()) return fail(CT_ENCCL, "libnccl.so.2 not loadable");
-    if (g->comm) {
-        g_nccl.CommDestroy(g->comm);
-        g->comm = nullptr;
-    }
+    delete g->comm;
+    g->comm = nullptr;
     DeviceGuard guard(g->d.device);
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));
-    ncclComm_t comm;
-    ncclResult_t r = g_nccl.CommInitRank(&comm, nranks, id, rank);
-    if (r != ncclSuccess) return fail(CT_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error");
-    g->comm = comm;
+    NcclComm* c = new NcclComm();
+    ncclResult_t r = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        c->comm = nullptr;
+        delete c;
+        return fail(CT_ENCCL, "ncclCommInitRank: %s", nccl_err(r));
+    }
+    c->rank = rank;
+    c->nranks = nranks;
+    g->comm = c;
     g->rank = rank;
     g->nranks = nranks;
     g->zslab = 0;
+    return CT_OK;
+}
+
+extern "C" int ct_comm_init_virtual(ct_geom** gs, int nranks, int zslab) {
+    if (!gs || nranks < 1) return fail(CT_EINVAL, "ct_comm_init_virtual: bad arguments");
+    for (int r = 0; r < nranks; r++) {
+        if (!gs[r]) return fail(CT_EINVAL, "ct_comm_init_virtual: null geometry %d", r);
+        if (gs[r]->d.device != gs[0]->d.device) return fail(CT_EINVAL, "virtual ranks must share one device");
+        if (zslab && gs[r]->d.kind == CT_FAN2D) return fail(CT_EUNSUPPORTED, "z-slab decomposition needs a cone-beam geometry");
+        for (int q = 0; q < r; q++)
+            if (gs[q] == gs[r]) return fail(CT_EINVAL, "virtual ranks need distinct geometry handles");
+    }
+    DeviceGuard guard(gs[0]->d.device);
+    auto grp = std::make_shared<VirtualGroup>();
+    if (grp->init(nranks, gs[0]->d.device)) return fail(CT_ECUDA, "virtual ranks: stream / event creation failed");
+    for (int r = 0; r < nranks; r++) {
+        delete gs[r]->comm;
+        VirtualComm* c = new VirtualComm();
+        c->grp = grp;
+        c->rank = r;
+        c->nranks = nranks;
+        gs[r]->comm = c;
+        gs[r]->rank = r;
+        gs[r]->nranks = nranks;
+        gs[r]->zslab = zslab ? 1 : 0;
+    }
     return CT_OK;
 }
 

@@ -309,10 +309,18 @@ constexpr size_t fwd3d_smem() {
 // Table fields (footprint phase): w[j] = lphi F_s(cA + j) / kz (F_t = overlap / kz folded
 // in); ax.qf = lower edge of row 0 relative to qi; ax.inv_kz holds tzc, the l_theta
 // offset tz(slice qi + m) = m dz_rho + tzc; rows = 32-bit index of (column, slice qi).
+#ifndef CT_FWD3D2_KS
+#define CT_FWD3D2_KS 1     // per-column slice-window specialisation (3 / 4 / 5 slices per row pair)
+#endif
 #ifndef CT_FWD3D2_MINB
 #define CT_FWD3D2_MINB 5   // 5 CTAs of 4 warps per SM (A/B: c3 2.32 -> 2.12, c5 15.2 -> 13.3 ms vs 4)
 #endif
 
+// KS = slices a lane's row pair can meet: rows 2l, 2l + 1 cover [lo, lo + 2 kz] with
+// lo in [z0, z0 + 1), i.e. slices z0 .. z0 + KS - 1 when 1 + 2 kz <= KS (KS = 3: kz <= 1,
+// KS = 4: kz <= 1.5, KS = 5: kz < 2); chosen per column (warp-uniform), so near-source
+// columns (small kz) do not pay for the far side's longer windows.
+template <int KS>
 __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __restrict__ x, int l, int nz) {
     const float kz = f.ax.kz;
     const float lo = fmaf((float)(2 * l), kz, f.ax.qf);
@@ -322,9 +330,9 @@ __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __r
     const float tz0 = fmaf(z0, f.ax.dz_rho, f.ax.inv_kz);
     const int iz0 = i0 + f.ax.qi;
     const float* xp = x + (f.rows + i0);
-    float xl[5];   // x l_theta of slices z0 .. z0 + 4 (0 outside the volume)
+    float xl[KS];   // x l_theta of slices z0 .. z0 + KS - 1 (0 outside the volume)
 #pragma unroll
-    for (int m = 0; m < 5; m++) {
+    for (int m = 0; m < KS; m++) {
         const float tz = fmaf((float)m, f.ax.dz_rho, tz0);
         const bool in = (unsigned)(iz0 + m) < (unsigned)nz && (m < 2 || z0 + (float)m < hi);
         const float v = in ? __ldg(xp + m) : 0.0f;
@@ -338,8 +346,8 @@ __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __r
     // row 2l + 1: [mid, hi], clamped slice boundaries b(m) = clamp(z0 + m, mid, hi)
     float B = 0.0f, pb = mid;
 #pragma unroll
-    for (int m = 0; m < 5; m++) {
-        const float nb = m < 4 ? fminf(fmaxf(z0 + (float)(m + 1), mid), hi) : hi;
+    for (int m = 0; m < KS; m++) {
+        const float nb = m < KS - 1 ? fminf(fmaxf(z0 + (float)(m + 1), mid), hi) : hi;
         B = fmaf(xl[m], nb - pb, B);
         pb = nb;
     }
@@ -359,11 +367,16 @@ __device__ __forceinline__ float fwd_axial_row(const Foot& f, const float* __res
 }
 
 // Accumulator updates of the pair-row forward: p points at the first channel's row pair.
+#ifndef CT_FWD3D2_ACC4
+#define CT_FWD3D2_ACC4 1   // the first 4 channels unconditionally (their weights past n are exactly 0)
+#endif
 template <int LW>
 __device__ __forceinline__ void acc_one(float2* p, const Foot& f, float2 A) {
 #pragma unroll
     for (int jj = 0; jj < kMaxFoot; jj++) {
-        if (jj >= f.n) break;
+        // w[jj] = 0 for jj >= n (column_footprint), and the accumulator has kMaxFoot slots past
+        // any first channel, so the first CT_FWD3D2_ACC4 * 4 updates need no count test
+        if (!(CT_FWD3D2_ACC4 && jj < 4) && jj >= f.n) break;
         float2 t = p[jj * LW];
         t.x = fmaf(f.w[jj], A.x, t.x);
         t.y = fmaf(f.w[jj], A.y, t.y);
@@ -450,9 +463,16 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
                 if (j + 1 < nq) load_foot(&tab[j + 1], f1); else f1.n = 0;
                 if (f0.n <= 0 && f1.n <= 0) continue;
                 float2 A0 = make_float2(0.0f, 0.0f), A1 = A0;
-                if (f0.ax.kz < 2.0f && f1.ax.kz < 2.0f) {
-                    if (f0.n > 0) A0 = fwd_axial_pair(f0, x, ll, nz);
-                    if (f1.n > 0) A1 = fwd_axial_pair(f1, x, ll, nz);
+                const float kzm = fmaxf(f0.n > 0 ? f0.ax.kz : 0.0f, f1.n > 0 ? f1.ax.kz : 0.0f);
+                if (CT_FWD3D2_KS && kzm <= 0.999f) {
+                    if (f0.n > 0) A0 = fwd_axial_pair<3>(f0, x, ll, nz);
+                    if (f1.n > 0) A1 = fwd_axial_pair<3>(f1, x, ll, nz);
+                } else if (CT_FWD3D2_KS && kzm <= 1.499f) {
+                    if (f0.n > 0) A0 = fwd_axial_pair<4>(f0, x, ll, nz);
+                    if (f1.n > 0) A1 = fwd_axial_pair<4>(f1, x, ll, nz);
+                } else if (kzm < 2.0f) {
+                    if (f0.n > 0) A0 = fwd_axial_pair<5>(f0, x, ll, nz);
+                    if (f1.n > 0) A1 = fwd_axial_pair<5>(f1, x, ll, nz);
                 } else {
                     if (f0.n > 0) {
                         const float l0 = fmaf((float)(2 * ll), f0.ax.kz, f0.ax.qf);

@@ -29,7 +29,7 @@ EXPORTS = ("ct_geom_create", "ct_geom_destroy", "ct_last_error", "ct_fwd_proj", 
            "ct_sqs_denom_scratch_bytes", "ct_sqs_denom", "ct_reg_grad", "ct_count_vv", "ct_oslalm_state_bytes",
            "ct_oslalm_state_create", "ct_fbp", "ct_fbp_scratch_bytes", "ct_peak_l2_read", "ct_oslalm_state_destroy", "ct_oslalm_state_get", "ct_oslalm_state_reset",
            "ct_oslalm_set_timing", "ct_oslalm_get_timing", "ct_oslalm_iter",
-           "ct_oslalm_run", "ct_comm_init", "ct_comm_init_zslab", "ct_comm_get_unique_id", "ct_build_info", "ct_kernel_launches")
+           "ct_oslalm_run", "ct_comm_init", "ct_comm_init_zslab", "ct_comm_init_virtual", "ct_comm_get_unique_id", "ct_build_info", "ct_kernel_launches")
 
 
 class CTError(RuntimeError):
@@ -112,6 +112,7 @@ def load():
     L.ct_oslalm_run.argtypes = [vp, P(ct_oslalm_cfg), P(ct_oslalm_data), vp, vp, i, P(ct_oslalm_log), vp]
     L.ct_comm_init.argtypes = [vp, i, i, vp]
     L.ct_comm_init_zslab.argtypes = [vp, i, i, vp]
+    L.ct_comm_init_virtual.argtypes = [P(vp), i, i]
     L.ct_comm_get_unique_id.argtypes = [vp]
     _lib = L
     return L
@@ -263,6 +264,13 @@ def ct_comm_init(h, rank, nranks, uid: bytes, zslab=False):
     _check(f(h, int(rank), int(nranks), buf))
 
 
+def ct_comm_init_virtual(handles, zslab=False):
+    """Attach len(handles) geometry handles of one device as virtual ranks 0..P-1 (validation
+    of the multi-rank path on one GPU; each rank must then be driven by its own thread)."""
+    arr = (ctypes.c_void_p * len(handles))(*[h.value for h in handles])
+    _check(load().ct_comm_init_virtual(arr, len(handles), 1 if zslab else 0))
+
+
 # ---------------------------------------------------------------------------
 # Convenience wrappers
 # ---------------------------------------------------------------------------
@@ -342,6 +350,13 @@ class Geometry:
         """(U, nnz, C) of the view list."""
         scratch = torch.zeros(32, dtype=torch.uint8, device=self.device)
         return ct_count_vv(self.h, views or self.views(), mask, scratch)
+
+    @staticmethod
+    def comm_init_virtual(geos, zslab=False):
+        """geos[r] becomes virtual rank r of len(geos) (one device, one host thread per rank)."""
+        ct_comm_init_virtual([g.h for g in geos], zslab)
+        for r, g in enumerate(geos):
+            g.rank, g.nranks = r, len(geos)
 
     def comm_init(self, rank, nranks, uid, zslab=False):
         """Attach an NCCL communicator.  zslab=True: this geometry is rank `rank`'s z-slab of the
