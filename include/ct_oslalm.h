@@ -90,10 +90,12 @@ typedef struct {
 } ct_views;
 
 /* Validate the description and build per-view tables on the device.
- * The geometry tables are immutable afterwards.  Fan-beam (2D) forward projections
- * accumulate into a geometry-owned 64-bit fixed-point buffer (kept zero between
- * calls), so 2D projections with one geometry must be ordered on one stream (or by
- * events); cone-beam geometries may be used from several streams at once.
+ * The geometry tables are immutable afterwards, and every call that needs scratch takes
+ * it from a caller-owned buffer (ct_sqs_denom's scratch, the OS-LALM state's workspace),
+ * so cone-beam geometries may be used from several streams at once.  The one exception:
+ * ct_fwd_proj on a FAN2D geometry accumulates into a geometry-owned 64-bit fixed-point
+ * buffer (kept zero between calls), so standalone fan-beam ct_fwd_proj calls with one
+ * geometry must be ordered on one stream (or by events).
  * Returns CT_EINVAL for inconsistent sizes, CT_EUNSUPPORTED if some voxel's
  * transaxial footprint could span more than 7 channels (kernel window limit), or,
  * for fan beams, if consecutive pixels can be less than 1/8 channel apart on the
@@ -109,11 +111,20 @@ const char* ct_last_error(void);
  * O2 / G1):  a_ij = l_phi * l_theta * F_s(c) * F_t(r).
  * x: [ny][nx][nz]; y: [count][ns][nt], overwritten.  Deterministic: no floating-point
  * atomics (the 2D tile sums meet in exact 64-bit integer adds, order-independent).
+ * Fan beam (FAN2D): the 32x32-pixel tile partial sums are added in 64-bit fixed point
+ * with unit 2^-40 (absolute quantum 9.1e-13 per tile partial); valid while every tile
+ * partial and every |y| stays below 2^23 = 8.4e6 (with attenuation-scale images, ~0.02
+ * mm^-1 and line integrals <= ~20, x may be scaled from ~1e-7 to ~1e5 and keep 1e-6
+ * relative accuracy).  Outside that range the result is undefined (the fixed-point sum
+ * overflows); nothing checks it.  Cone beam: plain fp32 sums in a fixed order, no range
+ * limit.  Cone-beam ct_fwd_proj does not trim all-zero image columns (the OS-LALM path
+ * and ct_sqs_denom do, with per-call scratch).
  */
 int ct_fwd_proj(const ct_geom* g, ct_views v, const float* x, float* y, void* stream);
 
 /*
- * Back projection x (+)= A_v' y, the exact adjoint of ct_fwd_proj (same a_ij).
+ * Back projection x (+)= A_v' y, the exact adjoint of ct_fwd_proj (same a_ij; "one
+ * multiplication by A'"; the gradient M A_m'(W(A_m x - y)) of P:380-397).
  * y: [count][ns][nt]; x: [ny][nx][nz]; accumulate != 0 adds to x, else overwrites.
  */
 int ct_back_proj(const ct_geom* g, ct_views v, const float* y, float* x, int accumulate, void* stream);

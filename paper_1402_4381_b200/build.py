@@ -19,11 +19,24 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
 
+def source_hash(extra=()) -> str:
+    """sha256 (16 hex digits) of every source the library is built from and the nvcc flags;
+    compiled into ct_build_info() as "src=<hash>" and checked by ctlib.load()."""
+    import hashlib
+    h = hashlib.sha256()
+    for s in SOURCES:
+        h.update(os.path.basename(s).encode())
+        with open(s, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(FLAGS + list(extra)).encode())
+    return h.hexdigest()[:16]
+
+
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".srchash"):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(s) > t for s in SOURCES)
+    with open(LIB + ".srchash") as f:
+        return f.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, extra=()) -> str:
@@ -32,7 +45,8 @@ def build(force: bool = False, verbose: bool = False, out: str = None, extra=())
     if out is None and not force and not needs_build():
         return LIB
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *extra, "-o", tmp, os.path.join(HERE, "csrc", "ct_abi.cu"), "-ldl"]
+    sh = source_hash(extra)
+    cmd = [NVCC, *FLAGS, *extra, f"-DCT_SRC_HASH=\"{sh}\"", "-o", tmp, os.path.join(HERE, "csrc", "ct_abi.cu"), "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -43,6 +57,9 @@ def build(force: bool = False, verbose: bool = False, out: str = None, extra=())
     if verbose:
         sys.stderr.write(r.stderr)
     os.replace(tmp, lib)
+    if out is None:
+        with open(LIB + ".srchash", "w") as f:
+            f.write(sh)
     return lib
 
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (ranges visible to ncu --nvtx / nsys)
 
 #include <atomic>
 #include <cmath>
@@ -91,10 +92,20 @@ static int fail(int code, const char* fmt, ...) {
         g_launches += (nk);                                                                    \
     } while (0)
 
+// NVTX range over one ABI call (host side; a CUDA-graph replay shows as one range)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 extern "C" const char* ct_last_error(void) { return g_err; }
 extern "C" unsigned long long ct_kernel_launches(void) { return g_launches.load(); }
+#ifndef CT_SRC_HASH
+#define CT_SRC_HASH "unknown"
+#endif
 extern "C" const char* ct_build_info(void) {
-    return "ct_oslalm sm_100a: fwd2d fwd3d back2d back3d (fused g-update + xi/rho finalize) sqs_update reg_grad gupd count_vv";
+    return "ct_oslalm sm_100a: fwd2d fwd3d back2d back3d (fused g-update + xi/rho finalize) sqs_update reg_grad gupd "
+           "count_vv; src=" CT_SRC_HASH;
 }
 
 // ---------------------------------------------------------------------------
@@ -193,8 +204,7 @@ struct ct_geom {
     DevGeomD dgd;
     float4* d_views = nullptr;
     double2* d_vz = nullptr;
-    unsigned long long* acc2d = nullptr;   // fan 2D forward: [na][ns] 64-bit fixed-point sums (kept zero)
-    int2* ext3d = nullptr;                 // cone forward: nonzero column range per image row / column
+    unsigned long long* acc2d = nullptr;   // fan 2D ct_fwd_proj: [na][ns] 64-bit fixed-point sums (kept zero)
     int rank = 0, nranks = 1;
     Comm* comm = nullptr;    // exchange backend (NcclComm / VirtualComm); owned
     int zslab = 0;   // NEXT-3: this geometry is rank `rank`'s z-slab of the volume (sinogram-domain sums)
@@ -340,12 +350,10 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     if (e == cudaSuccess) e = cudaMemcpy(g->d_vz, hvz.data(), sizeof(double2) * d->na, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && is2d) e = cudaMalloc(&g->acc2d, sizeof(unsigned long long) * d->na * d->ns);
     if (e == cudaSuccess && is2d) e = cudaMemset(g->acc2d, 0, sizeof(unsigned long long) * d->na * d->ns);
-    if (e == cudaSuccess && !is2d) e = cudaMalloc(&g->ext3d, sizeof(int2) * (d->nx + d->ny));
     if (e != cudaSuccess) {
         cudaFree(g->d_views);
         cudaFree(g->d_vz);
         cudaFree(g->acc2d);
-        cudaFree(g->ext3d);
         delete g;
         return fail(e == cudaErrorMemoryAllocation ? CT_ENOMEM : CT_ECUDA, "geometry tables: %s", cudaGetErrorString(e));
     }
@@ -365,7 +373,6 @@ extern "C" void ct_geom_destroy(ct_geom* g) {
     cudaFree(g->d_views);
     cudaFree(g->d_vz);
     cudaFree(g->acc2d);
-    cudaFree(g->ext3d);
     delete g;
 }
 
@@ -418,9 +425,18 @@ static cudaError_t launch_fwd3d2(const DevGeom& dg, ct_views v, const float* x, 
     return cudaSuccess;
 }
 
+// Per-call forward-projection scratch (owned by the caller of launch_fwd, so concurrent
+// projections through one geometry on different streams never share it):
+//   acc2d  fan beam: [count][ns] 64-bit fixed-point sums, zero on entry and on exit
+//   ext    cone beam: per image line the range of columns with a nonzero voxel (nullptr: no trimming)
+struct FwdScratch {
+    unsigned long long* acc2d;
+    int2* ext;
+};
+
 template <bool RESID>
 static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, const float* yobs, const float* w,
-                      float scale, cudaStream_t st) {
+                      float scale, cudaStream_t st, FwdScratch fs) {
     if (v.count == 0) return CT_OK;
     const DevGeom& dg = g->dg;
     if (dg.kind == CT_FAN2D) {
@@ -432,36 +448,42 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
                                : dg.fpar == 1 && CT_FWD2D_PT ? fwd2d_tile_kernel<false, 1> : fwd2d_tile_kernel<false, 0>);
         CT_CUDA(ensure_dyn_smem((const void*)kern, smem));
         dim3 grid((dg.nx + kF2T - 1) / kF2T, (dg.ny + kF2T - 1) / kF2T, (v.count + kF2VC - 1) / kF2VC);
-        CT_CUDA(launch_pdl(kern, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, g->acc2d));
+        CT_CUDA(launch_pdl(kern, grid, dim3(256), smem, st, dg, v.first, v.stride, v.count, x, fs.acc2d));
         const int cells = v.count * dg.ns;
-        CT_CUDA(launch_pdl(fwd2d_finalize_kernel<RESID>, dim3((cells + 255) / 256), dim3(256), 0, st, dg, v.first,
-                           v.stride, v.count, g->acc2d, out, yobs, w, scale));
+        cudaError_t fe = launch_pdl(fwd2d_finalize_kernel<RESID>, dim3((cells + 255) / 256), dim3(256), 0, st, dg,
+                                    v.first, v.stride, v.count, fs.acc2d, out, yobs, w, scale);
+        if (fe != cudaSuccess) {   // the finalize re-zeroes the accumulator: do it here instead
+            cudaMemsetAsync(fs.acc2d, 0, sizeof(unsigned long long) * (size_t)cells, st);
+            return fail(CT_ECUDA, "fwd2d_finalize launch: %s", cudaGetErrorString(fe));
+        }
         CT_LAUNCHED(1);
     } else {
         // per line, the columns holding a nonzero voxel of x (trims the wedge walk)
         const int next = dg.nx + dg.ny;
-        fwd3d_extent_init<<<(next + 255) / 256, 256, 0, st>>>(g->ext3d, next);
-        fwd3d_extent_kernel<<<(dg.nx * dg.ny + 7) / 8, 256, 0, st>>>(dg, x, g->ext3d);
+        if (fs.ext) {
+            fwd3d_extent_init<<<(next + 255) / 256, 256, 0, st>>>(fs.ext, next);
+            fwd3d_extent_kernel<<<(dg.nx * dg.ny + 7) / 8, 256, 0, st>>>(dg, x, fs.ext);
+            CT_LAUNCHED(2);
+        }
         constexpr int TC = CT_FWD3D_TC;
         if (v.count > 65535) {   // gridDim.y limit: launch the view list in chunks
             for (int c0 = 0; c0 < v.count; c0 += 65535) {
                 const ct_views vc{v.first + c0 * v.stride, v.stride, std::min(65535, v.count - c0)};
-                if (int e = launch_fwd<RESID>(g, vc, x, out + (size_t)c0 * dg.ns * dg.nt, yobs, w, scale, st)) return e;
+                if (int e = launch_fwd<RESID>(g, vc, x, out + (size_t)c0 * dg.ns * dg.nt, yobs, w, scale, st, fs)) return e;
             }
             return CT_OK;
         }
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32 && CT_FWD3D_PAIR)
-            CT_CUDA((launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 2, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st)));
+            CT_CUDA((launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 2, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st)));
         else if (dg.nt <= 32)
-            CT_CUDA((launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st)));
+            CT_CUDA((launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, fs.ext, st)));
         else if (dg.nt <= 64 && CT_FWD3D_PAIR)
-            CT_CUDA((launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 1, RESID>(dg, v, x, out, yobs, w, scale, g->ext3d, st)));
+            CT_CUDA((launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 1, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st)));
         else if (dg.nt <= 64)
-            CT_CUDA((launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st)));
+            CT_CUDA((launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, fs.ext, st)));
         else
-            CT_CUDA((launch_fwd3d<TC, 128, RESID>(dg, grid, v, x, out, yobs, w, scale, g->ext3d, st)));
-        CT_LAUNCHED(2);
+            CT_CUDA((launch_fwd3d<TC, 128, RESID>(dg, grid, v, x, out, yobs, w, scale, fs.ext, st)));
     }
     CT_LAUNCHED(1);
     return CT_OK;
@@ -517,13 +539,17 @@ static inline unsigned nblk(size_t n) { return (unsigned)((n + 255) / 256); }
 // projections, D_L, regulariser, U
 // ---------------------------------------------------------------------------
 extern "C" int ct_fwd_proj(const ct_geom* g, ct_views v, const float* x, float* y, void* stream) {
+    NvtxRange nvtx_("ct_fwd_proj");
     if (!g || !x || !y) return fail(CT_EINVAL, "ct_fwd_proj: null argument");
     if (int e = check_views(g, v)) return e;
     DeviceGuard guard(g->d.device);
-    return launch_fwd<false>(g, v, x, y, nullptr, nullptr, 1.0f, (cudaStream_t)stream);
+    // cone beam: no column trimming (it needs per-call scratch); fan beam: the geometry's
+    // accumulator (FAN2D handles: one stream at a time for ct_fwd_proj, include/ct_oslalm.h)
+    return launch_fwd<false>(g, v, x, y, nullptr, nullptr, 1.0f, (cudaStream_t)stream, FwdScratch{g->acc2d, nullptr});
 }
 
 extern "C" int ct_back_proj(const ct_geom* g, ct_views v, const float* y, float* x, int accumulate, void* stream) {
+    NvtxRange nvtx_("ct_back_proj");
     if (!g || !x || (!y && v.count > 0)) return fail(CT_EINVAL, "ct_back_proj: null argument");
     if (int e = check_views(g, v)) return e;
     DeviceGuard guard(g->d.device);
@@ -596,6 +622,7 @@ extern "C" int ct_fbp_scratch_bytes(const ct_geom* g, size_t* out) {
 }
 
 extern "C" int ct_fbp(const ct_geom* g, const float* y, float* x, void* scratch, void* stream) {
+    NvtxRange nvtx_("ct_fbp");
     if (!g || !y || !x || !scratch) return fail(CT_EINVAL, "ct_fbp: null argument");
     if (int e = check_fbp(g)) return e;
     DeviceGuard guard(g->d.device);
@@ -610,23 +637,50 @@ extern "C" int ct_fbp(const ct_geom* g, const float* y, float* x, void* scratch,
     return CT_OK;
 }
 
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// Forward-projection scratch for `count` views: fan accumulator [count][ns] (8 B) or cone
+// column extents [nx + ny] (8 B).
+static size_t fwd_scratch_bytes(const ct_geom* g, int count) {
+    return g->d.kind == CT_FAN2D ? align256((size_t)count * g->d.ns * 8) : align256((size_t)(g->d.nx + g->d.ny) * 8);
+}
+
+static FwdScratch fwd_scratch_at(const ct_geom* g, void* p) {
+    return g->d.kind == CT_FAN2D ? FwdScratch{(unsigned long long*)p, nullptr} : FwdScratch{nullptr, (int2*)p};
+}
+
+// ct_sqs_denom scratch: 1_S image | all-view sinogram | forward scratch (all views)
+static void sqs_scratch_layout(const ct_geom* g, size_t off[3], size_t* total) {
+    off[0] = 0;
+    off[1] = align256(n_vox(g) * sizeof(float));
+    off[2] = off[1] + align256((size_t)g->d.na * n_cells_view(g) * sizeof(float));
+    *total = off[2] + fwd_scratch_bytes(g, g->d.na) + 256;   // + 256: the caller's pointer may be unaligned
+}
+
 extern "C" int ct_sqs_denom_scratch_bytes(const ct_geom* g, size_t* out) {
     if (!g || !out) return fail(CT_EINVAL, "ct_sqs_denom_scratch_bytes: null argument");
-    *out = n_vox(g) * sizeof(float) + (size_t)g->d.na * n_cells_view(g) * sizeof(float) + 256;
+    size_t off[3];
+    sqs_scratch_layout(g, off, out);
     return CT_OK;
 }
 
 static void zslab_window(const ct_geom* g, ct_views v, int* k0, int* k1);
 static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* out, const float* y, const float* w,
-                           float scale, cudaStream_t st);
+                           float scale, cudaStream_t st, FwdScratch fs);
 
 extern "C" int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask, float* dl, void* scratch, void* stream) {
+    NvtxRange nvtx_("ct_sqs_denom");
     if (!g || !w || !mask || !dl || !scratch) return fail(CT_EINVAL, "ct_sqs_denom: null argument");
     DeviceGuard guard(g->d.device);
     cudaStream_t st = (cudaStream_t)stream;
     size_t N = n_vox(g);
-    float* one = (float*)scratch;
-    float* sino = (float*)(((uintptr_t)(one + N) + 255) & ~(uintptr_t)255);
+    size_t soff[3], stotal;
+    sqs_scratch_layout(g, soff, &stotal);
+    char* sbase = (char*)(((uintptr_t)scratch + 255) & ~(uintptr_t)255);
+    float* one = (float*)(sbase + soff[0]);
+    float* sino = (float*)(sbase + soff[1]);
+    const FwdScratch fs = fwd_scratch_at(g, sbase + soff[2]);
+    if (fs.acc2d) CT_CUDA(cudaMemsetAsync(fs.acc2d, 0, (size_t)g->d.na * g->d.ns * 8, st));
     // multi-rank: this rank's contiguous block of all views, partial D_L summed with NCCL
     int base = g->d.na / g->nranks, extra = g->d.na % g->nranks;
     ct_views all{g->rank * base + std::min(g->rank, extra), 1, base + (g->rank < extra ? 1 : 0)};
@@ -637,13 +691,13 @@ extern "C" int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask, flo
     if (g->zslab) {
         // z-slab ranks: A 1_S summed over the slabs (every ray), weighted, back onto the slab
         const ct_views va{0, 1, g->d.na};
-        if (int e = zslab_fwd_resid(g, va, one, sino, nullptr, w, 1.0f, st)) return e;
+        if (int e = zslab_fwd_resid(g, va, one, sino, nullptr, w, 1.0f, st, fs)) return e;
         int k0, k1;
         zslab_window(g, va, &k0, &k1);
         if (int e = launch_back<EPI_STORE>(g, ct_views{k0, 1, k1 - k0}, sino + (size_t)k0 * n_cells_view(g), dl, ga, st))
             return e;
     } else {
-        if (int e = launch_fwd<true>(g, all, one, sino, nullptr, w, 1.0f, st)) return e;
+        if (int e = launch_fwd<true>(g, all, one, sino, nullptr, w, 1.0f, st, fs)) return e;
         if (int e = launch_back<EPI_STORE>(g, all, sino, dl, ga, st)) return e;
         if (g->comm)
             if (int e = allreduce(g, dl, N, st)) return e;
@@ -675,6 +729,7 @@ static int check_reg(const ct_geom* g, const ct_reg* r) {
 
 extern "C" int ct_reg_grad(const ct_geom* g, const ct_reg* r, const uint8_t* mask, const float* x, float* grad,
                            float* curv, void* stream) {
+    NvtxRange nvtx_("ct_reg_grad");
     if (!g || !mask || !x || !grad) return fail(CT_EINVAL, "ct_reg_grad: null argument");
     if (int e = check_reg(g, r)) return e;
     DeviceGuard guard(g->d.device);
@@ -738,6 +793,7 @@ struct ct_oslalm_state {
     uint8_t* zmask[2] = {nullptr, nullptr};
     int zmask_ready = 0;
     double* xi_part;
+    FwdScratch fs{nullptr, nullptr};     // this state's forward-projection scratch (own, per state)
     Scalars* sc;
     double* dlog;        // M x 3 doubles (per iteration)
     int curG = 0;
@@ -787,8 +843,6 @@ static int tcollect(ct_oslalm_state* s) {
     s->evmarks.clear();
     return CT_OK;
 }
-
-static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 static void bit_reversal(int M, std::vector<int>& order) {
     int bits = 0;
@@ -861,6 +915,9 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16
     off[12] = o; o += c->bb ? 4 * align256(N * 4) + align256(2 * 8 * nblk(N)) : 0;   // BB: xbar_prev, gbar, gbar_prev, xbar, partials
     const size_t ncols = (size_t)g->d.nx * g->d.ny;
     off[13] = o; o += g->zslab ? 4 * align256(ncols * 4) + 2 * align256(ncols) : 0;   // z-slab halos
+    // forward-projection scratch (fan accumulator for one subset's views; z-slab ranks project
+    // whole subsets too; cone column extents)
+    off[14] = o; o += fwd_scratch_bytes(g, maxcount);
     *total = o;
 }
 
@@ -913,6 +970,7 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
         s->xp[1] = (float*)(b + off[10] + align256(s->Npad * 4));
     }
     s->xi_ex = (double*)(b + off[11]);
+    s->fs = fwd_scratch_at(g, b + off[14]);
     if (g->zslab) {
         const size_t ncols = (size_t)g->d.nx * g->d.ny, fb = align256(ncols * 4);
         s->zsend[0] = (float*)(b + off[13]);
@@ -1012,7 +1070,7 @@ static void zslab_window(const ct_geom* g, ct_views v, int* k0, int* k1) {
 // views k < v.count (only the rank's view window is projected; other views contribute 0),
 // then s <- scale W (s - y) on every ray (y nullable).
 static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* out, const float* y, const float* w,
-                           float scale, cudaStream_t st) {
+                           float scale, cudaStream_t st, FwdScratch fs) {
     const size_t cells = n_cells_view(g);
     int k0, k1;
     zslab_window(g, v, &k0, &k1);
@@ -1020,7 +1078,7 @@ static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* 
     if (k1 < v.count) CT_CUDA(cudaMemsetAsync(out + (size_t)k1 * cells, 0, (size_t)(v.count - k1) * cells * 4, st));
     if (k1 > k0)
         if (int e = launch_fwd<false>(g, ct_views{v.first + k0 * v.stride, v.stride, k1 - k0}, x, out + (size_t)k0 * cells,
-                                      nullptr, nullptr, 1.0f, st))
+                                      nullptr, nullptr, 1.0f, st, fs))
             return e;
     if (int e = allreduce(g, out, (size_t)v.count * cells, st)) return e;
     const size_t n = (size_t)v.count * cells;
@@ -1049,9 +1107,9 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
     ct_views v = rank_views(g, M, m);
     int t0 = tmark(s, st);
     if (g->zslab) {
-        if (int e = zslab_fwd_resid(g, v, x, s->sino, d->y, d->w, (float)M, st)) return e;
+        if (int e = zslab_fwd_resid(g, v, x, s->sino, d->y, d->w, (float)M, st, s->fs)) return e;
     } else {
-        if (int e = launch_fwd<true>(g, v, x, s->sino, d->y, d->w, (float)M, st)) return e;
+        if (int e = launch_fwd<true>(g, v, x, s->sino, d->y, d->w, (float)M, st, s->fs)) return e;
     }
     tmark_end(s, st, 1, t0);
     GupdArgs ga{};
@@ -1260,6 +1318,10 @@ static int ensure_initialised(ct_oslalm_state* s, const ct_oslalm_data* d, float
     const ct_oslalm_cfg& c = s->cfg;
     init_scalars_kernel<<<1, 1, 0, st>>>(s->sc, c.mode == CT_RHO_FIXED ? c.rho_fixed : 1.0);
     CT_LAUNCHED(1);
+    if (s->fs.acc2d) {   // the fan accumulator is kept zero by the projections from here on
+        const int maxcount = (s->g->d.na + c.M - 1) / c.M;
+        CT_CUDA(cudaMemsetAsync(s->fs.acc2d, 0, (size_t)maxcount * s->g->d.ns * 8, st));
+    }
     zero_offmask_kernel<<<nblk(s->N), 256, 0, st>>>(x, d->mask, s->N);
     CT_LAUNCHED(1);
     if (c.bb) CT_CUDA(cudaMemsetAsync(s->gbar, 0, s->Npad * 4, st));
@@ -1287,6 +1349,7 @@ static bool cfg_equal(const ct_oslalm_cfg& a, const ct_oslalm_cfg& b) {
 
 extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_data* d, ct_oslalm_state* s,
                               float* x, void* stream) {
+    NvtxRange nvtx_("ct_oslalm_iter");
     if (!g || !s) return fail(CT_EINVAL, "ct_oslalm_iter: null argument");
     if (s->g != g) return fail(CT_ESTATE, "state was created for another geometry");
     if (cfg && !cfg_equal(*cfg, s->cfg)) {
@@ -1356,6 +1419,7 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
 
 extern "C" int ct_oslalm_run(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_data* d, ct_oslalm_state* s,
                              float* x, int n_iter, ct_oslalm_log* log, void* stream) {
+    NvtxRange nvtx_("ct_oslalm_run");
     if (n_iter < 0) return fail(CT_EINVAL, "n_iter < 0");
     if (log) log->count = 0;
     DeviceGuard guard(g ? g->d.device : 0);

@@ -41,6 +41,8 @@ __device__ __forceinline__ float vertex_ch(const DevGeom& g, float sb, float cb,
 // reference atan per (block, view).  Forward and back use the same owner block for every
 // vertex, so both see identical vertex values.
 constexpr int kVB = 8;   // reference block edge (vertices)
+constexpr int kVBShift = 3;
+static_assert((1 << kVBShift) == kVB, "kVB must be 1 << kVBShift (vertex_tab's block index)");
 
 struct VRef {
     float G;                  // reference arc position (centred channel units)
@@ -71,7 +73,7 @@ __device__ __forceinline__ float vertex_rel(const DevGeom& g, const VRef& R, flo
 // block is (bx0, by0); RT[(by - by0) * NBX + (bx - bx0)].
 template <int NBX>
 __device__ __forceinline__ float vertex_tab(const DevGeom& g, const VRef* RT, int bx0, int by0, int vx, int vy) {
-    const VRef& R = RT[((vy >> 3) - by0) * NBX + ((vx >> 3) - bx0)];
+    const VRef& R = RT[((vy >> kVBShift) - by0) * NBX + ((vx >> kVBShift) - bx0)];
     return vertex_rel(g, R, (float)((vx & (kVB - 1)) - kVB / 2), (float)((vy & (kVB - 1)) - kVB / 2));
 }
 
@@ -179,7 +181,7 @@ __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, cons
 //      (consecutive pixels advance >= 1/P channel, validated at create), so every add in
 //      one instruction goes to a distinct address: no atomics, fixed order;
 //  (c) the 8 x P buffers are summed in fixed order over the tile's channel span and
-//      added to the 64-bit fixed-point accumulator acc[k][c] (2^-32 units) with integer
+//      added to the 64-bit fixed-point accumulator acc[k][c] (2^-40 units) with integer
 //      atomics, which are exact and order-independent: the result is bit-reproducible.
 //      fwd2d_finalize converts, applies the residual epilogue r = scale W (Ax - y) and
 //      re-zeroes acc.
@@ -191,7 +193,11 @@ __device__ __forceinline__ float foot_dot(const DevGeom& g, const Foot2& f, cons
 #endif
 constexpr int kF2T = 32;      // tile edge (pixels)
 constexpr int kF2VC = 8;      // views per CTA
-constexpr float kFix = 4294967296.0f;   // 2^32
+// Fixed-point unit 2^-40: absolute quantum 9.1e-13 per tile partial, range |partial|,
+// |A x| < 2^23 = 8.4e6 per detector cell (include/ct_oslalm.h, ct_fwd_proj), i.e. x from
+// ~1e-7 to ~1e5 times attenuation scale (0.02 mm^-1) keeps 1e-6 relative accuracy.
+constexpr float kFix = 1099511627776.0f;   // 2^40
+constexpr double kFixInv = 1.0 / 1099511627776.0;
 
 // NR rounds of the forward tile (NR = warp max of the lanes' bin counts n): round j adds
 // lane's bin cA + j.  Bins j >= n add exactly 0 (Fn = Fp = mass); the last round needs no CDF
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
     }
 }
 
-// out[k][c] = acc * 2^-32 (RESID: scale W (Ax - y)); acc is re-zeroed for the next launch.
+// out[k][c] = acc * 2^-40 (RESID: scale W (Ax - y)); acc is re-zeroed for the next launch.
 template <bool RESID>
 __global__ void __launch_bounds__(256) fwd2d_finalize_kernel(DevGeom g, int first, int stride, int count,
                                                             unsigned long long* __restrict__ acc, float* __restrict__ out,
@@ -361,7 +367,7 @@ __global__ void __launch_bounds__(256) fwd2d_finalize_kernel(DevGeom g, int firs
     if (i >= count * g.ns) return;
     const long long q = (long long)acc[i];
     acc[i] = 0ull;
-    const float s = (float)((double)q * (1.0 / 4294967296.0));
+    const float s = (float)((double)q * kFixInv);
     if (RESID) {
         const int k = i / g.ns, c = i - k * g.ns;
         const size_t gi = (size_t)(first + k * stride) * g.ns + c;

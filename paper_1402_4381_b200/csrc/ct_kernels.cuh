@@ -106,10 +106,18 @@ __device__ __forceinline__ void load_foot(const Foot* src, Foot& d) {
     d.ax.kz = e.x; d.ax.inv_kz = e.y; d.ax.dz_rho = e.z; d.rows = __float_as_int(e.w);
 }
 
-__device__ __forceinline__ void column_footprint(const DevGeom& g, float4 vw, float xc, float yc, Foot& f) {
+// [clo, chi): channel window the footprint is clipped to (the forward projector's tile;
+// the back-projector passes the whole detector).
+__device__ __forceinline__ void column_footprint(const DevGeom& g, float4 vw, float xc, float yc, Foot& f,
+                                                 int clo = 0, int chi = 0x7fffffff) {
     Trans tr;
     transaxial(g, vw.x, vw.y, xc, yc, tr);
     foot_range(g, tr, f.cA, f.n);
+    {
+        const int a = max(f.cA, clo), b = min(f.cA + f.n, chi);
+        f.cA = a;
+        f.n = b - a;
+    }
     TrapCdf F(tr);
     float e = (float)f.cA - 0.5f - tr.cc;
     float Fp = F(e);
@@ -176,6 +184,15 @@ __device__ __forceinline__ float fwd_axial_any(const Foot& f, const float* __res
 // kMaxFoot - 1 channels left of it and spans at most kMaxFoot channels.
 template <int TC>
 __host__ __device__ constexpr int fwd3d_tcp() { return TC + 2 * kMaxFoot - 2; }
+
+// Pair-row forward: footprints are clipped to the tile, so the accumulator holds the tile's
+// channels plus the 3 slots the unconditional first-4-channel updates (acc_one) may touch.
+#ifndef CT_FWD3D2_CLIP
+#define CT_FWD3D2_CLIP 1
+#endif
+template <int TC>
+__host__ __device__ constexpr int fwd3d2_tcp() { return CT_FWD3D2_CLIP ? TC + 3 : fwd3d_tcp<TC>(); }
+__host__ __device__ constexpr int fwd3d2_base() { return CT_FWD3D2_CLIP ? 0 : kMaxFoot - 1; }
 
 #ifndef CT_FWD3D_MINB
 #define CT_FWD3D_MINB 4   // min resident CTAs per SM for the register budget (A/B: 4 beats 1 by 1.3-1.5x)
@@ -411,7 +428,7 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
                                                                      const float* __restrict__ yobs,
                                                                      const float* __restrict__ wts, float scale,
                                                                      const int2* __restrict__ ext) {
-    constexpr int TCP = fwd3d_tcp<TC>();
+    constexpr int TCP = fwd3d2_tcp<TC>(), CB = fwd3d2_base();
     constexpr int LW = 32 / H;   // lanes per column (row pairs)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* Pacc = reinterpret_cast<float2*>(smem_raw);                                   // [NW][H][TCP][LW]
@@ -444,8 +461,12 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
                 const int u = lo + q;
                 const int ix = w.rows ? u : L, iy = w.rows ? L : u;
                 Foot f;
-                column_footprint(g, vw, g.x0 + ix * g.dx, g.y0 + iy * g.dy, f);
-                if (!(f.n > 0 && f.cA + f.n > c0 && f.cA < c0 + TC)) f.n = 0;   // misses the tile
+                if (CT_FWD3D2_CLIP) {
+                    column_footprint(g, vw, g.x0 + ix * g.dx, g.y0 + iy * g.dy, f, c0, c0 + TC);   // n <= 0: misses the tile
+                } else {
+                    column_footprint(g, vw, g.x0 + ix * g.dx, g.y0 + iy * g.dy, f);
+                    if (!(f.n > 0 && f.cA + f.n > c0 && f.cA < c0 + TC)) f.n = 0;   // misses the tile
+                }
 #pragma unroll
                 for (int j = 0; j < kMaxFoot; j++) f.w[j] *= f.ax.inv_kz;
                 const float qf = f.ax.qf;
@@ -491,7 +512,7 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
                     // the union (f0's term first, then f1's, as in the separate loops).  A/B: c4
                     // (half-warp streams) 4.09 -> 3.82 ms; c3 / c5 (H = 1) 1-2 % slower, not used
 
-                    float2* p = Pg + (min(f0.cA, f1.cA) - c0 + kMaxFoot - 1) * LW;
+                    float2* p = Pg + (min(f0.cA, f1.cA) - c0 + CB) * LW;
                     switch (dd) {
                         case -3: acc_pair<3, 0, LW>(p, f0, A0, f1, A1); break;
                         case -2: acc_pair<2, 0, LW>(p, f0, A0, f1, A1); break;
@@ -502,8 +523,8 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
                         default: acc_pair<0, 3, LW>(p, f0, A0, f1, A1); break;
                     }
                 } else {
-                    if (f0.n > 0) acc_one<LW>(Pg + (f0.cA - c0 + kMaxFoot - 1) * LW, f0, A0);
-                    if (f1.n > 0) acc_one<LW>(Pg + (f1.cA - c0 + kMaxFoot - 1) * LW, f1, A1);
+                    if (f0.n > 0) acc_one<LW>(Pg + (f0.cA - c0 + CB) * LW, f0, A0);
+                    if (f1.n > 0) acc_one<LW>(Pg + (f1.cA - c0 + CB) * LW, f1, A1);
                 }
             }
             __syncwarp();
@@ -518,7 +539,7 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
         if (rr >= g.nt || c0 + c >= g.ns) continue;
         float s = 0.0f;
 #pragma unroll
-        for (int q = 0; q < NW * H; q++) s += Pf[(q * TCP + c + kMaxFoot - 1) * RW + rr];
+        for (int q = 0; q < NW * H; q++) s += Pf[(q * TCP + c + CB) * RW + rr];
         const size_t oi = ((size_t)k * g.ns + c0 + c) * g.nt + rr;
         if (RESID) {
             const size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
@@ -532,7 +553,7 @@ __global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom
 
 template <int TC, int NW>
 constexpr size_t fwd3d2_smem() {
-    return sizeof(float2) * NW * fwd3d_tcp<TC>() * 32 + sizeof(Foot) * NW * 32;
+    return sizeof(float2) * NW * fwd3d2_tcp<TC>() * 32 + sizeof(Foot) * NW * 32;
 }
 
 // Per image line, the range of columns holding a nonzero voxel (forward-projection

@@ -114,8 +114,23 @@ def load():
     L.ct_comm_init_zslab.argtypes = [vp, i, i, vp]
     L.ct_comm_init_virtual.argtypes = [P(vp), i, i]
     L.ct_comm_get_unique_id.argtypes = [vp]
+    _check_provenance(L)
     _lib = L
     return L
+
+
+def _check_provenance(L):
+    """The library must have been built from the sources next to it (source hash compiled
+    into ct_build_info), so a GPU run provably uses the HEAD build.  Tuning variants loaded
+    through CT_OSLALM_LIB are exempt."""
+    if "CT_OSLALM_LIB" in os.environ:
+        return
+    from . import build as _b
+    info = L.ct_build_info().decode()
+    want = _b.source_hash()
+    if f"src={want}" not in info:
+        raise CTError(f"{LIB_PATH} is stale ({info.split('src=')[-1]} != sources {want}): "
+                      f"rebuild with `python -m paper_1402_4381_b200.build`")
 
 
 def _check(rc):

@@ -1,0 +1,166 @@
+"""Full-size OS-LALM parity on the BASELINE configs, running the production kernel instances
+(the bench's launch configuration) against the fp64 oracle (north_star: "within 0.5 HU image
+RMS after 20 iterations ... on all five configs"; PAPER.md P:380-398 is the loop, P:516 the
+restart rule).  Costs are bounded by the oracle (~50-200 ns per voxel-view per core):
+
+* c2  (configs[1], 512^2 fan, M = 24): the full 20 iterations;
+* c3  (configs[2], 512^2 x 64 axial cone, M = 24): 2 iterations at full size;
+* c4 / c5 (configs[3] / configs[4], helical, M = 24): full transaxial size and the full view
+  set on a z-cropped volume (64 / 32 slices around the centre; `inputs.slab_geom`), 1
+  iteration -- this runs fwd3d2<22,4,2|1,RESID>, back3d<EPI_INIT|EPI_GUPD, 32|64> and the
+  26-neighbour K3 on 512^2 planes inside an OS-LALM iteration;
+* whole-subset projector parity for c4 (123 views) and c5 (287 views);
+* an M = 24 run in which restarts (xi > 0) actually fire.
+
+Bar: RMS over S <= 0.5 HU (1 HU = 2e-5 mm^-1), identical restart decisions and rho
+trajectory, support bit-exact; projections <= 1e-4 relative L2 per view.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1402_4381_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+MARGINS = []
+
+
+@pytest.fixture(scope="module")
+def ct():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1402_4381_b200 import build, ctlib
+    build.build()
+    ctlib.load()
+    return ctlib
+
+
+@pytest.fixture(scope="module")
+def O():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _write_margins():
+    yield
+    import json
+    import os
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if MARGINS and os.path.isdir(out):
+        with open(os.path.join(out, "parity_margins_fullsize.json"), "w") as f:
+            json.dump(MARGINS, f, indent=1)
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def run_pair(ct, O, cfg, n_iter, tag, data=None):
+    """GPU (C ABI, graph replay) and oracle reconstructions of cfg from x = 0."""
+    g = cfg.geom
+    d = data or I.synthesize(cfg, device="cuda", views_per_chunk=8 if not cfg.is2d else 128)
+    y, w = d["y"].cuda(), d["w"].cuda()
+    m0 = I.support_mask(cfg, device="cuda")
+    geo = ct.Geometry(g)
+    dl, S = geo.sqs_denom(w, m0)
+    sol = ct.OSLALM(geo, cfg.M, beta=cfg.beta, delta=cfg.delta, nbr=cfg.nbr)
+    sol.set_data(y, w, dl, S)
+    x = torch.zeros(geo.img_shape, device="cuda")
+    log = np.array(sol.run(x, n_iter, log=True))
+    xg = I.to_oracle_image(x.cpu().numpy())
+    Sg = I.to_oracle_image(S.cpu().numpy()).astype(np.uint8)
+    yo, wo = I.to_oracle_sino(y.cpu()), I.to_oracle_sino(w.cpu())
+    del x, dl, sol, geo, y, w
+    torch.cuda.empty_cache()
+    dlo, So = O.sqs_denom(g, wo, I.to_oracle_image(m0.cpu()).astype(np.uint8))
+    assert np.array_equal(Sg, So), f"{tag}: support differs"
+    xo, logo, _, _ = O.oslalm_run(g, yo, wo, dlo, So, np.zeros(O.img_shape(g)), M=cfg.M, beta=cfg.beta,
+                                  delta=cfg.delta, nbr=cfg.nbr, n_iter=n_iter)
+    rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
+    MARGINS.append({"case": tag, "iters": n_iter, "rms_HU": rms, "max_abs_HU": float(np.abs(xg - xo)[So > 0].max() / I.HU),
+                    "restarts_gpu": int(log[:, 2].sum()), "restarts_oracle": int(logo[:, 2].sum()),
+                    "image_rms_HU": math.sqrt((xo[So > 0] ** 2).mean()) / I.HU})
+    return xg, xo, log, logo, rms
+
+
+def check(xg, xo, log, logo, rms, tag):
+    assert rms <= 0.5, (tag, rms)
+    assert np.array_equal(log[:, 2], logo[:, 2]), tag        # identical restart decisions
+    assert np.allclose(log[:, 0], logo[:, 0], rtol=1e-12), tag  # identical rho trajectory
+    assert np.abs(xo).max() > 0.01, tag                     # a non-trivial reconstruction
+
+
+def test_oslalm_c2_20_iterations(ct, O):
+    """configs[1] at full size for the north_star's 20 iterations (M = 24)."""
+    cfg = I.config("c2")
+    r = run_pair(ct, O, cfg, 20, "c2 full size, 20 iterations")
+    check(*r, "c2")
+
+
+def test_oslalm_c3_full_size(ct, O):
+    """configs[2] (512^2 x 64, 888 x 64 detector, 984 views, M = 24) at full size, 2 iterations."""
+    cfg = I.config("c3")
+    r = run_pair(ct, O, cfg, 2, "c3 full size, 2 iterations")
+    check(*r, "c3")
+
+
+def zcrop(cfg, nz_keep):
+    """cfg with its volume cropped to the central nz_keep slices (same scan, same views)."""
+    g = cfg.geom
+    z0 = (g["nz"] - nz_keep) // 2
+    gc = I.slab_geom(g, z0, z0 + nz_keep)
+    return I.ScanConfig(cfg.name, gc, cfg.M, cfg.n_iter, cfg.beta, cfg.delta, cfg.nbr, cfg.I0, cfg.sigma,
+                        cfg.recipe, cfg.body_z, dict(cfg.extra))
+
+
+@pytest.mark.parametrize("cname,nz_keep", [("c4", 64), ("c5", 32)])
+def test_oslalm_helical_zcrop(ct, O, cname, nz_keep):
+    """configs[3] / configs[4]: full 512^2 planes, full detector and view set, the central
+    nz_keep slices (the phantom's body continues beyond them: the data are those of the full
+    object, a long-object scan), M = 24, 1 iteration."""
+    cfg = zcrop(I.config(cname), nz_keep)
+    r = run_pair(ct, O, cfg, 1, f"{cname} z-cropped to {nz_keep} slices, 1 iteration")
+    check(*r, cname)
+
+
+@pytest.mark.parametrize("cname,sub", [("c4", 7), ("c5", 13)])
+def test_projector_whole_subset_helical(ct, O, cname, sub):
+    """A whole subset of the helical configs (c4: 123 views, c5: 287 views) at full size, on a
+    random non-negative image on S and a random residual sinogram."""
+    cfg = I.config(cname)
+    g = cfg.geom
+    geo = ct.Geometry(g)
+    views = (sub, cfg.M, (g["na"] - sub + cfg.M - 1) // cfg.M)
+    rng = np.random.default_rng(11)
+    x = (rng.random(geo.img_shape).astype(np.float32) * 0.02) * I.support_mask(cfg).numpy()
+    yg = geo.fwd(torch.from_numpy(x).cuda(), views).cpu().numpy()
+    yo = O.fwd(g, I.to_oracle_image(x), *views)
+    ygo = I.to_oracle_sino(yg)
+    e = rel_l2(ygo, yo)
+    per_view = max(rel_l2(ygo[k], yo[k]) for k in range(views[2]) if np.abs(yo[k]).max() > 0)
+    MARGINS.append({"case": f"fwd whole subset {cname} {views}", "rel_l2": e, "max_per_view": per_view})
+    assert e <= 1e-4 and per_view <= 1e-4
+    p = rng.random(yg.shape).astype(np.float32)
+    bg = geo.back(torch.from_numpy(p).cuda(), views).cpu().numpy()
+    bo = O.back(g, I.to_oracle_sino(p), *views)
+    e = rel_l2(I.to_oracle_image(bg), bo)
+    MARGINS.append({"case": f"back whole subset {cname} {views}", "rel_l2": e})
+    assert e <= 1e-4
+
+
+def test_oslalm_M24_restarts_fire(ct, O):
+    """M = 24 with 100 views per subset (c1 geometry, 32^2 image, 2400 views): the restart rule
+    (xi > 0 => l = 0) fires inside the first iteration; the GPU takes the same decisions
+    (|xi| is ~1e16 at the restarts, far from the fp32 / fp64 rounding level) and the same image."""
+    cfg = I.scaled(I.config("c1"), "c1r24", na=2400, nx=32, ny=32)
+    cfg.M = 24
+    r = run_pair(ct, O, cfg, 6, "c1 geometry, 2400 views, M = 24, 6 iterations (restarts fire)")
+    xg, xo, log, logo, rms = r
+    assert logo[:, 2].sum() >= 1
+    check(*r, "M24 restarts")

@@ -162,6 +162,47 @@ def test_projector_full_size(ct, O, cname, views):
     assert rel_l2(I.to_oracle_image(bg), bo, f"back full-size {cname} {views}") <= 1e-4
 
 
+@pytest.mark.parametrize("scale", [1e-6, 1e4])
+def test_fan_forward_input_scale(ct, O, scale):
+    """The 2D forward's 64-bit fixed-point tile sums (unit 2^-40, include/ct_oslalm.h) keep the
+    1e-4 parity bound for images scaled 1e-6 and 1e4 times attenuation scale (c2 subset)."""
+    cfg = I.config("c2")
+    g = cfg.geom
+    geo = ct.Geometry(g)
+    views = (5, 24, 41)
+    rng = np.random.default_rng(14)
+    x = (rng.random(geo.img_shape) * 0.02 * scale * I.support_mask(cfg).numpy()).astype(np.float32)
+    yg = I.to_oracle_sino(geo.fwd(torch.from_numpy(x).cuda(), views).cpu().numpy())
+    yo = O.fwd(g, I.to_oracle_image(x), *views)
+    e = rel_l2(yg, yo, f"fwd c2 subset, x scaled {scale:g}")
+    assert e <= 1e-4, e
+    for k in range(views[2]):
+        assert rel_l2(yg[k], yo[k]) <= 1e-4
+
+
+def test_cone_forward_two_streams(ct):
+    """Cone-beam projections through ONE geometry on two streams at once (different images):
+    each equals its single-stream result (per-call scratch)."""
+    g = I.config("c3").geom
+    geo = ct.Geometry(g)
+    views = (3, 24, 41)
+    x1 = torch.rand(geo.img_shape, device="cuda")
+    x2 = torch.zeros(geo.img_shape, device="cuda")
+    x2[200:300, 100:400, :] = torch.rand(100, 300, g["nz"], device="cuda")   # different zero columns
+    r1, r2 = geo.fwd(x1, views), geo.fwd(x2, views)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(3):
+        a = torch.empty_like(r1); b = torch.empty_like(r2)
+        ct.ct_fwd_proj(geo.h, views, x1, a, stream=s1)
+        ct.ct_fwd_proj(geo.h, views, x2, b, stream=s2)
+        outs.append((a, b))
+    torch.cuda.synchronize()
+    for a, b in outs:
+        assert torch.equal(a, r1) and torch.equal(b, r2)
+
+
 @pytest.mark.parametrize("name", ["fan_c1", "axial_c3", "helical_c4", "fan_offsets"])
 def test_count_vv_exact(ct, O, name):
     g = geoms_small()[name]
@@ -211,8 +252,13 @@ def test_reg_grad(ct, O, name, nbr):
     gr, cu = geo.reg_grad(torch.from_numpy(x).cuda(), torch.from_numpy(m).cuda(), beta, delta, nbr)
     gro, cuo = O.reg_grad(g, beta, delta, nbr, I.to_oracle_image(m).astype(np.uint8), I.to_oracle_image(x))
     gr = I.to_oracle_image(gr.cpu().numpy()); cu = I.to_oracle_image(cu.cpu().numpy())
-    assert np.all(np.abs(gr - gro) <= 1e-5 * np.abs(gro).max() + 1e-4 * np.abs(gro))
-    assert np.all(np.abs(cu - cuo) <= 1e-5 * np.abs(cuo).max() + 1e-5 * np.abs(cuo))
+    # 1e-5 relative elementwise; the absolute floor (1e-6 of the max) covers the
+    # gradients that cancel to ~0 (26 terms of both signs, MUFU reciprocal ~1 ulp per term)
+    MARGINS.append({"case": f"reg_grad {name} nbr={nbr}", "grad_rel_max": float((np.abs(gr - gro) / np.maximum(np.abs(gro), 1e-30))[np.abs(gro) > 1e-3 * np.abs(gro).max()].max()),
+                    "grad_err_over_max": float(np.abs(gr - gro).max() / np.abs(gro).max()),
+                    "curv_rel_max": float((np.abs(cu - cuo) / np.maximum(np.abs(cuo), 1e-30))[cuo > 0].max())})
+    assert np.all(np.abs(gr - gro) <= 1e-6 * np.abs(gro).max() + 1e-5 * np.abs(gro))
+    assert np.all(np.abs(cu - cuo) <= 1e-6 * np.abs(cuo).max() + 1e-5 * np.abs(cuo))
 
 
 # --------------------------------------------------------------------------- OS-LALM
@@ -294,14 +340,6 @@ def test_oslalm_3d_small(ct, O, name):
                                   np.zeros(O.img_shape(g)), M=4, beta=cfg.beta, delta=cfg.delta, nbr=26, n_iter=8)
     xg = I.to_oracle_image(x.cpu().numpy())
     rms = math.sqrt(((xg - xo)[So > 0] ** 2).mean()) / I.HU
-    assert rms <= 0.5, rms
-    assert np.array_equal(log[:, 2], logo[:, 2])
-
-
-def test_oslalm_c2_full_size(ct, O):
-    """c2 (BASELINE configs[1]) at full size for 2 iterations (oracle cost bound): <= 0.5 HU."""
-    cfg = I.config("c2")
-    xg, xo, log, logo, rms = _run_pair(ct, O, cfg, 2)
     assert rms <= 0.5, rms
     assert np.array_equal(log[:, 2], logo[:, 2])
 
