@@ -56,7 +56,16 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 #define CT_FWD3D_PAIR 1   // nt <= 64: pair-row forward kernel (fwd3d2_kernel); 0: fwd3d_kernel
 #endif
 #ifndef CT_FWD3D2_TC
-#define CT_FWD3D2_TC 22   // A/B (c3, c5): 22 beats 16, 18, 20, 24 by 2-10 %
+#define CT_FWD3D2_TC 22   // axial scans; A/B (c3): 22 beats 16, 18, 20, 24, 26, 32 by 2-10 %
+#endif
+#ifndef CT_FWD3D2_MINB
+#define CT_FWD3D2_MINB 5
+#endif
+#ifndef CT_FWD3D2_TC_HEL
+#define CT_FWD3D2_TC_HEL 26   // helical scans; A/B (c4, c5): 26 (6 CTAs/SM) beats 22, 32, 40, 48
+#endif
+#ifndef CT_FWD3D2_MINB_HEL
+#define CT_FWD3D2_MINB_HEL 6
 #endif
 #ifndef CT_FWD3D2_NW
 #define CT_FWD3D2_NW 4    // warps (row groups) per CTA (8: c3 -1 %, c5 +12 %)
@@ -414,15 +423,25 @@ static cudaError_t launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const 
     return cudaSuccess;
 }
 
-template <int TC, int NW, int H, bool RESID>
+template <int TC, int NW, int H, bool RESID, int MINB>
 static cudaError_t launch_fwd3d2(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
                                  const float* w, float scale, const int2* ext, cudaStream_t st) {
     constexpr size_t smem = fwd3d2_smem<TC, NW>();
-    cudaError_t e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, RESID>, smem);
+    cudaError_t e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, RESID, MINB>, smem);
     if (e != cudaSuccess) return e;
     dim3 grid((dg.ns + TC - 1) / TC, v.count);
-    fwd3d2_kernel<TC, NW, H, RESID><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
+    fwd3d2_kernel<TC, NW, H, RESID, MINB><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
     return cudaSuccess;
+}
+
+// Pair-row forward (nt <= 64): tile width and resident CTAs per SM by scan kind (A/B, c3-c5)
+template <int H, bool RESID>
+static cudaError_t launch_fwd3d2_sel(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
+                                     const float* w, float scale, const int2* ext, cudaStream_t st) {
+    if (dg.kind == CT_CONE_HELICAL)
+        return launch_fwd3d2<CT_FWD3D2_TC_HEL, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB_HEL>(dg, v, x, out, yobs, w, scale,
+                                                                                        ext, st);
+    return launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB>(dg, v, x, out, yobs, w, scale, ext, st);
 }
 
 // Per-call forward-projection scratch (owned by the caller of launch_fwd, so concurrent
@@ -475,11 +494,11 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         }
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32 && CT_FWD3D_PAIR)
-            CT_CUDA((launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 2, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st)));
+            CT_CUDA((launch_fwd3d2_sel<2, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st)));
         else if (dg.nt <= 32)
             CT_CUDA((launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, fs.ext, st)));
         else if (dg.nt <= 64 && CT_FWD3D_PAIR)
-            CT_CUDA((launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, 1, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st)));
+            CT_CUDA((launch_fwd3d2_sel<1, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st)));
         else if (dg.nt <= 64)
             CT_CUDA((launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, fs.ext, st)));
         else

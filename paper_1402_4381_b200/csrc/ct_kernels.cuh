@@ -197,9 +197,7 @@ __host__ __device__ constexpr int fwd3d2_base() { return CT_FWD3D2_CLIP ? 0 : kM
 #ifndef CT_FWD3D_MINB
 #define CT_FWD3D_MINB 4   // min resident CTAs per SM for the register budget (A/B: 4 beats 1 by 1.3-1.5x)
 #endif
-#ifndef CT_BACK3D_MINB
-#define CT_BACK3D_MINB 5   // A/B (c3, c5): 5 beats 4 by 2-3% despite a few spilled bytes; 3 is 12% slower
-#endif
+
 
 template <int TC, int NTP, int NTHR, bool RESID>
 __global__ void __launch_bounds__(NTHR, CT_FWD3D_MINB) fwd3d_kernel(DevGeom g, int first, int stride, const float* __restrict__ x,
@@ -329,9 +327,9 @@ constexpr size_t fwd3d_smem() {
 #ifndef CT_FWD3D2_KS
 #define CT_FWD3D2_KS 1     // per-column slice-window specialisation (3 / 4 / 5 slices per row pair)
 #endif
-#ifndef CT_FWD3D2_MINB
-#define CT_FWD3D2_MINB 5   // 5 CTAs of 4 warps per SM (A/B: c3 2.32 -> 2.12, c5 15.2 -> 13.3 ms vs 4)
-#endif
+// Resident CTAs per SM (register budget) is a template parameter: 5 CTAs of 4 warps for
+// axial scans (A/B: c3 2.32 -> 2.12 ms vs 4), 6 for helical ones (with 26-channel tiles:
+// c5 12.01 -> 11.41, c4 3.72 -> 3.31 ms vs 22 channels / 5 CTAs; c3 prefers the latter).
 
 // KS = slices a lane's row pair can meet: rows 2l, 2l + 1 cover [lo, lo + 2 kz] with
 // lo in [z0, z0 + 1), i.e. slices z0 .. z0 + KS - 1 when 1 + 2 kz <= KS (KS = 3: kz <= 1,
@@ -422,8 +420,8 @@ __device__ __forceinline__ void acc_pair(float2* p, const Foot& f0, float2 A0, c
     }
 }
 
-template <int TC, int NW, int H, bool RESID>
-__global__ void __launch_bounds__(NW * 32, CT_FWD3D2_MINB) fwd3d2_kernel(DevGeom g, int first, int stride,
+template <int TC, int NW, int H, bool RESID, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int first, int stride,
                                                                      const float* __restrict__ x, float* __restrict__ out,
                                                                      const float* __restrict__ yobs,
                                                                      const float* __restrict__ wts, float scale,
@@ -742,11 +740,20 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 //      PF(u(iz + 1)) - PF(u(iz)) with PF the piecewise-linear cumulative sum.
 // Work per (column, view) is proportional to the slices the cone actually meets,
 // which matters for helical scans (a view sees ~20-30 % of a long volume).
+#ifndef CT_BACK3D_PAIR
+#define CT_BACK3D_PAIR 0   // 1: two views per slice walk (one accumulator update per slice for both); A/B: slower (64 registers, 4 CTAs/SM: c5 11.25 -> 12.38 ms)
+#endif
+#ifndef CT_BACK3D_MINB
+// one view per walk: 5 CTAs/SM (A/B c3, c5: beats 4 by 2-3 %; 3 is 12 % slower); two views per
+// walk need 64 registers (48 spill ~200 bytes)
+#define CT_BACK3D_MINB (CT_BACK3D_PAIR ? 4 : 5)
+#endif
+
 constexpr int kBackRows = 128;   // >= nt (validated)
 constexpr int kBackPad = 32;     // per-warp accumulator padding past nz (slice-loop tail lanes add 0 there)
 
 __host__ __device__ constexpr size_t back3d_smem_fixed() {
-    return sizeof(Foot) * 8 * 32 + sizeof(float2) * 8 * (kBackRows + 4);
+    return sizeof(Foot) * 8 * 32 + sizeof(float2) * 8 * (CT_BACK3D_PAIR ? 2 : 1) * (kBackRows + 4);
 }
 
 // Two filtered detector rows (float2) of one view: q = sum_{c < n} w[c] y[c][r..r+1].
@@ -772,15 +779,136 @@ __device__ __forceinline__ void filt_rows1(const float* __restrict__ yr, int pit
     for (int c = 0; c < NC; c++) q0 = fmaf(f.w[c], vv[c], q0);
 }
 
+// Filtered detector rows of one (column, view) and their prefix sums into QP (step (1) below).
+// QP[k] = (PF[k], Q(r_lo + k)) for k < nr, QP[nr] = (total, 0); returns r_lo, nr.
+template <int NTM>
+__device__ __forceinline__ void back3d_rows(const DevGeom& g, const Foot& f, const float* __restrict__ yv0, int lane,
+                                            float2* QP, int& r_lo, int& nr) {
+    const int nt = NTM ? NTM : g.nt;
+    r_lo = 0;
+    nr = nt;
+    if (NTM == 64) {
+        // the common 64-row detector: one pass over every row, two rows per lane
+        // (the rows the active slices miss are cheap to include)
+        const float2* yr = reinterpret_cast<const float2*>(yv0) + lane;
+        float q0 = 0.0f, q1 = 0.0f;
+        if (f.n <= 3) filt_rows2<3>(yr, 32, true, f, q0, q1);
+        else if (f.n <= 4) filt_rows2<4>(yr, 32, true, f, q0, q1);
+        else filt_rows2<kMaxFoot>(yr, 32, true, f, q0, q1);
+        const float s2 = q0 + q1;
+        float inc = s2;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const float ex = inc - s2;
+        reinterpret_cast<float4*>(QP)[lane] = make_float4(ex, q0, ex + q0, q1);
+        if (lane == 31) QP[64] = make_float2(inc, 0.0f);
+    } else if (NTM == 32) {
+        // 32-row detector: one pass over every row, one row per lane
+        const float* yr = yv0 + lane;
+        float q0 = 0.0f;
+        if (f.n <= 3) filt_rows1<3>(yr, 32, true, f, q0);
+        else if (f.n <= 4) filt_rows1<4>(yr, 32, true, f, q0);
+        else filt_rows1<kMaxFoot>(yr, 32, true, f, q0);
+        float inc = q0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        QP[lane] = make_float2(inc - q0, q0);
+        if (lane == 31) QP[32] = make_float2(inc, 0.0f);
+    } else {
+        // rows met by the active slices, from an even row (float2 loads)
+        const int za = f.rows & 0xffff, nzs = f.rows >> 16;
+        const float ub = g.rbase + 0.5f;
+        const float zq = (float)(za - f.ax.qi) - f.ax.qf;
+        // two rows per lane (float2) for tall detectors; float2 rows need an even row pitch
+        const bool even = (nt & 1) == 0 && nt > 32;
+        r_lo = min(max(__float2int_rd(fmaf(zq, f.ax.inv_kz, ub)), 0), nt - 1) & (even ? ~1 : ~0);
+        const int r_hi = min(max(__float2int_rd(fmaf(zq + (float)nzs, f.ax.inv_kz, ub)), 0), nt - 1);
+        nr = r_hi - r_lo + 1;
+        const float* yv = yv0 + r_lo;   // < 2^31 (validated at create)
+        float carry = 0.0f;
+        const int RPL = even ? 2 : 1;
+        for (int p0 = 0; p0 < nr; p0 += 32 * RPL) {
+            const int p = p0 + RPL * lane;
+            const bool inr = p < nr;
+            float q0 = 0.0f, q1 = 0.0f;
+            if (even) {
+                const float2* yr = reinterpret_cast<const float2*>(yv + (inr ? p : 0));
+                // warp-uniform channel count: issue all loads, then the FMAs
+                if (f.n <= 3) filt_rows2<3>(yr, nt >> 1, inr, f, q0, q1);
+                else if (f.n <= 4) filt_rows2<4>(yr, nt >> 1, inr, f, q0, q1);
+                else filt_rows2<kMaxFoot>(yr, nt >> 1, inr, f, q0, q1);
+                if (p + 1 >= nr) q1 = 0.0f;   // row past r_hi (odd count)
+            } else {
+                const float* yr = yv + (inr ? p : 0);
+                if (f.n <= 3) filt_rows1<3>(yr, nt, inr, f, q0);
+                else if (f.n <= 4) filt_rows1<4>(yr, nt, inr, f, q0);
+                else filt_rows1<kMaxFoot>(yr, nt, inr, f, q0);
+            }
+            const float s2 = q0 + q1;
+            float inc = s2;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            const float ex = carry + inc - s2;
+            if (inr) {
+                QP[p] = make_float2(ex, q0);
+                if (even) QP[p + 1] = make_float2(ex + q0, q1);
+                if (p + RPL >= nr) QP[p + RPL] = make_float2(ex + s2, 0.0f);   // upper edge of the last row
+            }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+}
+
+// Per-view constants of the slice walk (step (2)): the slice edge zi (voxel units relative to
+// the view's qi, minus qf) maps to the detector-row coordinate u = zi inv_kz + ubl in [0, nr].
+struct SliceWalk {
+    float zl;        // this lane's edge in pass 0 of a walk starting at slice z0
+    float inv_kz, ubl, fnr, dz_rho, hdz;
+    const float2* QP;
+    __device__ __forceinline__ void init(const Foot& f, const DevGeom& g, int z0, int lane, int r_lo, int nr,
+                                         const float2* qp) {
+        zl = (float)(z0 + lane - f.ax.qi) - f.ax.qf;
+        inv_kz = f.ax.inv_kz;
+        ubl = g.rbase + 0.5f - (float)r_lo;
+        fnr = (float)nr;
+        dz_rho = f.ax.dz_rho;
+        hdz = 0.5f * f.ax.dz_rho;
+        QP = qp;
+    }
+    // l_theta-weighted integral of the row-wise constant Q over this lane's slice in the pass at
+    // offset sf: PF(u(zi + 1)) - PF(u(zi)), the upper edge taken from the next lane.  Edges
+    // outside the view's rows clamp to 0 / nr, so slices outside its window contribute 0.
+    __device__ __forceinline__ float contrib(float sf) const {
+        const float zi = zl + sf;
+        const float u = fminf(fmaxf(fmaf(zi, inv_kz, ubl), 0.0f), fnr);
+        const int k = __float2int_rd(u);
+        const float2 qp = QP[k];
+        const float pf = fmaf(u - (float)k, qp.y, qp.x);
+        const float up = __shfl_down_sync(0xffffffffu, pf, 1);
+        const float tz = fmaf(zi, dz_rho, hdz);
+        return sqrt_approx(fmaf(tz, tz, 1.0f)) * (up - pf);
+    }
+};
+
 // NTM: detector-row specialisation, 64 or 32 (every row in one pass, nt a compile-time
 // constant) or 0 (general nt: the rows the active slices meet).
 template <int EPI, int NTM>
 __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, int first, int stride, int count,
                                                     const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
+    constexpr int NQ = CT_BACK3D_PAIR ? 2 : 1;
     Foot* table = reinterpret_cast<Foot*>(sm_raw);
     float2* QPs = reinterpret_cast<float2*>(sm_raw + sizeof(Foot) * 8 * 32);
-    float* ACC = reinterpret_cast<float*>(QPs + 8 * (kBackRows + 4));
+    float* ACC = reinterpret_cast<float*>(QPs + 8 * NQ * (kBackRows + 4));
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ix = blockIdx.x * 4 + (wid & 3);
     const int iy = blockIdx.y * 2 + (wid >> 2);
@@ -789,8 +917,10 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
     const int col = ((colok ? iy : 0) * g.nx + (colok ? ix : 0)) * nz;
     Foot* tab = table + wid * 32;
     // QP[k] = (PF[k], Q(r_lo + k)): prefix sum of the filtered rows below row r_lo + k and the
-    // row itself (one 8-byte load per slice edge); QP[nr] = (total, 0)
-    float2* QP = QPs + wid * (kBackRows + 4);
+    // row itself (one 8-byte load per slice edge); QP[nr] = (total, 0).  Two tables with
+    // CT_BACK3D_PAIR (the two views of a slice walk).
+    float2* QPA = QPs + wid * NQ * (kBackRows + 4);
+    float2* QPB = QPA + (NQ - 1) * (kBackRows + 4);
     float* acc = ACC + wid * (nz + kBackPad);   // + kBackPad: the slice loop's unpredicated tail
     bool any = false;
     for (int iz = lane; iz < nz; iz += 32) {
@@ -801,7 +931,6 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
     any = __any_sync(0xffffffffu, any);
     if (any) {
         const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
-        const float ub = g.rbase + 0.5f;   // row-edge coordinate: detector row r covers u in [r, r + 1)
         for (int vb = 0; vb < count; vb += 32) {
             const int kk = vb + lane;
             if (kk < count) {
@@ -818,116 +947,44 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
             }
             __syncwarp();
             const int nb = min(32, count - vb);
-            for (int j = 0; j < nb; j++) {
-                Foot f;
-                load_foot(&tab[j], f);
-                if (f.n <= 0) continue;
-                const int za = f.rows & 0xffff, nzs = f.rows >> 16;
-                int r_lo = 0, nr = nt;
-                if (NTM == 64) {
-                    // the common 64-row detector: one pass over every row, two rows per lane
-                    // (the rows the active slices miss are cheap to include)
-                    const float2* yr = reinterpret_cast<const float2*>(y + ((vb + j) * ns + f.cA) * 64) + lane;
-                    float q0 = 0.0f, q1 = 0.0f;
-                    if (f.n <= 3) filt_rows2<3>(yr, 32, true, f, q0, q1);
-                    else if (f.n <= 4) filt_rows2<4>(yr, 32, true, f, q0, q1);
-                    else filt_rows2<kMaxFoot>(yr, 32, true, f, q0, q1);
-                    const float s2 = q0 + q1;
-                    float inc = s2;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const float t = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (lane >= o) inc += t;
-                    }
-                    const float ex = inc - s2;
-                    reinterpret_cast<float4*>(QP)[lane] = make_float4(ex, q0, ex + q0, q1);
-                    if (lane == 31) QP[64] = make_float2(inc, 0.0f);
-                } else if (NTM == 32) {
-                    // 32-row detector: one pass over every row, one row per lane
-                    const float* yr = y + ((vb + j) * ns + f.cA) * 32 + lane;
-                    float q0 = 0.0f;
-                    if (f.n <= 3) filt_rows1<3>(yr, 32, true, f, q0);
-                    else if (f.n <= 4) filt_rows1<4>(yr, 32, true, f, q0);
-                    else filt_rows1<kMaxFoot>(yr, 32, true, f, q0);
-                    float inc = q0;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const float t = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (lane >= o) inc += t;
-                    }
-                    QP[lane] = make_float2(inc - q0, q0);
-                    if (lane == 31) QP[32] = make_float2(inc, 0.0f);
-                } else {
-                    // rows met by the active slices, from an even row (float2 loads)
-                    const float zq = (float)(za - f.ax.qi) - f.ax.qf;
-                    // two rows per lane (float2) for tall detectors; float2 rows need an even row pitch
-                    const bool even = (nt & 1) == 0 && nt > 32;
-                    r_lo = min(max(__float2int_rd(fmaf(zq, f.ax.inv_kz, ub)), 0), nt - 1) & (even ? ~1 : ~0);
-                    const int r_hi = min(max(__float2int_rd(fmaf(zq + (float)nzs, f.ax.inv_kz, ub)), 0), nt - 1);
-                    nr = r_hi - r_lo + 1;
-                    const float* yv = y + (((vb + j) * ns + f.cA) * nt + r_lo);   // < 2^31 (validated at create)
-                    // (1) filtered rows Q(r) = sum_c lphi F_s(c) y[c][r] and prefix sums
-                    //     PF[k] = sum_{r < r_lo + k} Q(r): lane = two rows (float2), pair sum + warp scan
-                    float carry = 0.0f;
-                    const int RPL = even ? 2 : 1;
-                    for (int p0 = 0; p0 < nr; p0 += 32 * RPL) {
-                        const int p = p0 + RPL * lane;
-                        const bool inr = p < nr;
-                        float q0 = 0.0f, q1 = 0.0f;
-                        if (even) {
-                            const float2* yr = reinterpret_cast<const float2*>(yv + (inr ? p : 0));
-                            // warp-uniform channel count: issue all loads, then the FMAs
-                            if (f.n <= 3) filt_rows2<3>(yr, nt >> 1, inr, f, q0, q1);
-                            else if (f.n <= 4) filt_rows2<4>(yr, nt >> 1, inr, f, q0, q1);
-                            else filt_rows2<kMaxFoot>(yr, nt >> 1, inr, f, q0, q1);
-                            if (p + 1 >= nr) q1 = 0.0f;   // row past r_hi (odd count)
-                        } else {
-                            const float* yr = yv + (inr ? p : 0);
-                            if (f.n <= 3) filt_rows1<3>(yr, nt, inr, f, q0);
-                            else if (f.n <= 4) filt_rows1<4>(yr, nt, inr, f, q0);
-                            else filt_rows1<kMaxFoot>(yr, nt, inr, f, q0);
-                        }
-                        const float s2 = q0 + q1;
-                        float inc = s2;
-    #pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const float t = __shfl_up_sync(0xffffffffu, inc, o);
-                            if (lane >= o) inc += t;
-                        }
-                        const float ex = carry + inc - s2;
-                        if (inr) {
-                            QP[p] = make_float2(ex, q0);
-                            if (even) QP[p + 1] = make_float2(ex + q0, q1);
-                            if (p + RPL >= nr) QP[p + RPL] = make_float2(ex + s2, 0.0f);   // upper edge of the last row
-                        }
-                        carry += __shfl_sync(0xffffffffu, inc, 31);
-                    }
-
-                }
+            for (int j = 0; j < nb; j += NQ) {
+                Foot fa, fb;
+                load_foot(&tab[j], fa);
+                if (NQ == 2 && j + 1 < nb) load_foot(&tab[j + 1], fb); else fb.n = 0;
+                const bool va = fa.n > 0, vbv = NQ == 2 && fb.n > 0;
+                if (!va && !vbv) continue;
+                // (1) filtered rows Q(r) = sum_c lphi F_s(c) y[k][c][r] and their prefix sums
+                int rla = 0, nra = 0, rlb = 0, nrb = 0;
+                if (va) back3d_rows<NTM>(g, fa, y + ((size_t)(vb + j) * ns + fa.cA) * nt, lane, QPA, rla, nra);
+                if (vbv) back3d_rows<NTM>(g, fb, y + ((size_t)(vb + j + 1) * ns + fb.cA) * nt, lane, QPB, rlb, nrb);
                 __syncwarp();
-                // (2) active slices (lanes = slices): integral of the row-wise constant Q over
-                //     the slice's extent on the detector, PF(u(iz + 1)) - PF(u(iz))
-                //     Lanes evaluate PF at consecutive slice edges; slice iz takes its upper edge
-                //     from the next lane, so a pass of 32 edges completes 31 slices.
-                //     (u = nr, the top edge, reads QP[nr] = (total, 0); l_theta of slice iz from
-                //     its lower edge's zi: tz = (zi + 1/2) dz / rho)
-                const float fnr = (float)nr, ubl = ub - (float)r_lo, hdz = 0.5f * f.ax.dz_rho;
-                const float zl = (float)(za + lane - f.ax.qi) - f.ax.qf;   // this lane's edge in pass 0
-                float* accl = acc + za + lane;
+                // (2) the union of the views' active slices (lanes = slices): per view the integral
+                //     of the row-wise constant Q over the slice's extent on the detector,
+                //     PF(u(iz + 1)) - PF(u(iz)); lanes evaluate PF at consecutive slice edges and
+                //     slice iz takes its upper edge from the next lane, so a pass of 32 edges
+                //     completes 31 slices (u = nr, the top edge, reads QP[nr] = (total, 0);
+                //     l_theta of slice iz from its lower edge's zi: tz = (zi + 1/2) dz / rho)
+                const int zaA = fa.rows & 0xffff, zeA = zaA + (fa.rows >> 16);
+                const int zaB = fb.rows & 0xffff, zeB = zaB + (fb.rows >> 16);
+                const int z0 = va ? (vbv ? min(zaA, zaB) : zaA) : zaB;
+                const int nzs = (va ? (vbv ? max(zeA, zeB) : zeA) : zeB) - z0;
+                SliceWalk wa, wb;
+                if (va) wa.init(fa, g, z0, lane, rla, nra, QPA);
+                if (vbv) wb.init(fb, g, z0, lane, rlb, nrb, QPB);
+                float* accl = acc + z0 + lane;
                 float sf = 0.0f;   // (float)s0
+                if (va && vbv) {
+#pragma unroll 1
+                    for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) {
+                        // no predicate: lanes past the union window (and lane 31, whose up = pf) add
+                        // exactly 0 (both edges clamp to the same u), into slots < nz + kBackPad
+                        const float c = wa.contrib(sf) + wb.contrib(sf);
+                        accl[s0] += c;
+                    }
+                } else {
+                    const SliceWalk& w1 = va ? wa : wb;
 #pragma unroll 1   // (A/B: the compiler's unrolled version needs more registers, -5 %)
-                for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) {
-                    // lower edge of slice za + s0 + lane (lane 31: upper edge of the pass's last slice)
-                    const float zi = zl + sf;
-                    const float u = fminf(fmaxf(fmaf(zi, f.ax.inv_kz, ubl), 0.0f), fnr);
-                    const int k = __float2int_rd(u);
-                    const float2 qp = QP[k];
-                    const float pf = fmaf(u - (float)k, qp.y, qp.x);
-                    const float up = __shfl_down_sync(0xffffffffu, pf, 1);
-                    const float tz = fmaf(zi, f.ax.dz_rho, hdz);
-                    // no predicate: lanes past the active window (and lane 31, whose up = pf) add
-                    // exactly 0 (both edges clamp to the same u), into slots < nz + kBackPad
-                    accl[s0] = fmaf(sqrt_approx(fmaf(tz, tz, 1.0f)), up - pf, accl[s0]);
+                    for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) accl[s0] += w1.contrib(sf);
                 }
                 __syncwarp();
             }
