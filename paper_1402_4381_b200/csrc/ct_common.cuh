@@ -17,6 +17,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Debug build (-DCT_DEBUG_CHECKS=1, tools/debug_checks.sh): device asserts on the invariants the
+// kernels rely on without checking them (shared-memory indices in range, the forward tile's
+// one-writer-per-address rounds, zero contributions of the back-projector's unpredicated tail
+// lanes).  compute-sanitizer is not available on the GPU pool; this is its stand-in.
+#ifndef CT_DEBUG_CHECKS
+#define CT_DEBUG_CHECKS 0
+#endif
+#if CT_DEBUG_CHECKS
+#undef NDEBUG
+#include <cassert>
+#define CT_DCHECK(c) assert(c)
+#else
+#define CT_DCHECK(c) ((void)0)
+#endif
+
 namespace ct {
 
 constexpr int kMaxFoot = 8;   // channel window of a voxel footprint (validated at create)

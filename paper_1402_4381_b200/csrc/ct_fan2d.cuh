@@ -204,7 +204,8 @@ constexpr double kFixInv = 1.0 / 1099511627776.0;
 // (every lane is at or past its right edge).  The CDF is evaluated on every lane and
 // selected, so the rounds are branch-free.
 template <int NR>
-__device__ __forceinline__ void fwd_rounds(float* bp, const Trap2& T, float koff, int n, bool act, float lx) {
+__device__ __forceinline__ void fwd_rounds(float* bp, const Trap2& T, float koff, int n, bool act, float lx,
+                                           const float* wb_lo = nullptr, const float* wb_hi = nullptr) {
     float Fp = 0.0f;   // unclipped: F = 0 at the left edge of bin cA
 #pragma unroll
     for (int j = 0; j < NR; j++) {
@@ -213,6 +214,14 @@ __device__ __forceinline__ void fwd_rounds(float* bp, const Trap2& T, float koff
             const float Fv = T.F(__fadd_rn(T.u0, koff + (float)(j + 1)));
             Fn = (j + 1 < n) ? Fv : T.mass;
         }
+#if CT_DEBUG_CHECKS
+        {   // the round's read-modify-writes must hit distinct addresses (no lost update) in range
+            const int lane = threadIdx.x & 31;
+            const unsigned long long a = act ? (unsigned long long)(bp + j) : ~(unsigned long long)lane;
+            CT_DCHECK(__match_any_sync(0xffffffffu, a) == (1u << lane));
+            CT_DCHECK(!act || (bp + j >= wb_lo && bp + j < wb_hi));
+        }
+#endif
         if (act) bp[j] += lx * __fsub_rn(Fn, Fp);
         Fp = Fn;
         __syncwarp();   // round j's stores are visible to round j + 1's loads
@@ -324,14 +333,14 @@ __global__ void __launch_bounds__(256, CT_FWD2D_MINB) fwd2d_tile_kernel(DevGeom 
                 const float koff = (float)(f.cA - T.c0);
                 // warp-uniform round count: straight-line rounds, no per-round branches
                 switch (nmax) {
-                    case 1: fwd_rounds<1>(bp, T, koff, n, act, lx); break;
-                    case 2: fwd_rounds<2>(bp, T, koff, n, act, lx); break;
-                    case 3: fwd_rounds<3>(bp, T, koff, n, act, lx); break;
-                    case 4: fwd_rounds<4>(bp, T, koff, n, act, lx); break;
-                    case 5: fwd_rounds<5>(bp, T, koff, n, act, lx); break;
-                    case 6: fwd_rounds<6>(bp, T, koff, n, act, lx); break;
-                    case 7: fwd_rounds<7>(bp, T, koff, n, act, lx); break;
-                    default: fwd_rounds<kMaxFoot>(bp, T, koff, n, act, lx); break;
+                    case 1: fwd_rounds<1>(bp, T, koff, n, act, lx, wb, wb + 8 * P * SPAN); break;
+                    case 2: fwd_rounds<2>(bp, T, koff, n, act, lx, wb, wb + 8 * P * SPAN); break;
+                    case 3: fwd_rounds<3>(bp, T, koff, n, act, lx, wb, wb + 8 * P * SPAN); break;
+                    case 4: fwd_rounds<4>(bp, T, koff, n, act, lx, wb, wb + 8 * P * SPAN); break;
+                    case 5: fwd_rounds<5>(bp, T, koff, n, act, lx, wb, wb + 8 * P * SPAN); break;
+                    case 6: fwd_rounds<6>(bp, T, koff, n, act, lx, wb, wb + 8 * P * SPAN); break;
+                    case 7: fwd_rounds<7>(bp, T, koff, n, act, lx, wb, wb + 8 * P * SPAN); break;
+                    default: fwd_rounds<kMaxFoot>(bp, T, koff, n, act, lx, wb, wb + 8 * P * SPAN); break;
                 }
             }
         }

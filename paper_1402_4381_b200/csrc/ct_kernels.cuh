@@ -324,6 +324,9 @@ constexpr size_t fwd3d_smem() {
 // Table fields (footprint phase): w[j] = lphi F_s(cA + j) / kz (F_t = overlap / kz folded
 // in); ax.qf = lower edge of row 0 relative to qi; ax.inv_kz holds tzc, the l_theta
 // offset tz(slice qi + m) = m dz_rho + tzc; rows = 32-bit index of (column, slice qi).
+#ifndef CT_FWD3D2_UNPRED
+#define CT_FWD3D2_UNPRED 0
+#endif
 #ifndef CT_FWD3D2_KS
 #define CT_FWD3D2_KS 1     // per-column slice-window specialisation (3 / 4 / 5 slices per row pair)
 #endif
@@ -349,7 +352,8 @@ __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __r
 #pragma unroll
     for (int m = 0; m < KS; m++) {
         const float tz = fmaf((float)m, f.ax.dz_rho, tz0);
-        const bool in = (unsigned)(iz0 + m) < (unsigned)nz && (m < 2 || z0 + (float)m < hi);
+        // slices past hi get weight 0 below; skipping their loads saves L1 traffic (CT_FWD3D2_UNPRED = 1: load them)
+        const bool in = (unsigned)(iz0 + m) < (unsigned)nz && (CT_FWD3D2_UNPRED || m < 2 || z0 + (float)m < hi);
         const float v = in ? __ldg(xp + m) : 0.0f;
         xl[m] = v * sqrt_approx(fmaf(tz, tz, 1.0f));
     }
@@ -386,9 +390,11 @@ __device__ __forceinline__ float fwd_axial_row(const Foot& f, const float* __res
 #define CT_FWD3D2_ACC4 1   // the first 4 channels unconditionally (their weights past n are exactly 0)
 #endif
 template <int LW>
-__device__ __forceinline__ void acc_one(float2* p, const Foot& f, float2 A) {
+__device__ __forceinline__ void acc_one(float2* p, const Foot& f, float2 A, const float2* lo = nullptr,
+                                        const float2* hi = nullptr) {
 #pragma unroll
     for (int jj = 0; jj < kMaxFoot; jj++) {
+        CT_DCHECK(lo == nullptr || (p + jj * LW >= lo && p + jj * LW < hi) || (jj >= f.n && !(CT_FWD3D2_ACC4 && jj < 4)));
         // w[jj] = 0 for jj >= n (column_footprint), and the accumulator has kMaxFoot slots past
         // any first channel, so the first CT_FWD3D2_ACC4 * 4 updates need no count test
         if (!(CT_FWD3D2_ACC4 && jj < 4) && jj >= f.n) break;
@@ -401,12 +407,14 @@ __device__ __forceinline__ void acc_one(float2* p, const Foot& f, float2 A) {
 
 // Two columns whose first channels are D0 / D1 channels past p's (one of D0, D1 is 0).
 template <int D0, int D1, int LW>
-__device__ __forceinline__ void acc_pair(float2* p, const Foot& f0, float2 A0, const Foot& f1, float2 A1) {
+__device__ __forceinline__ void acc_pair(float2* p, const Foot& f0, float2 A0, const Foot& f1, float2 A1,
+                                         const float2* lo = nullptr, const float2* hi = nullptr) {
     constexpr int DM = D0 > D1 ? D0 : D1;
     const int nu = max(D0 + f0.n, D1 + f1.n);
 #pragma unroll
     for (int jj = 0; jj < kMaxFoot + DM; jj++) {
         if (jj >= nu) break;
+        CT_DCHECK(lo == nullptr || (p + jj * LW >= lo && p + jj * LW < hi));
         float2 t = p[jj * LW];
         if (jj >= D0 && jj - D0 < kMaxFoot && jj - D0 < f0.n) {
             t.x = fmaf(f0.w[jj - D0], A0.x, t.x);
@@ -439,6 +447,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
     const int hf = lane / LW, ll = lane % LW;   // half (column stream) and row pair
     Foot* tab = table + gi * 32;
     float2* Pg = Pacc + (gi * H + hf) * TCP * LW + ll;   // rows 2 ll, 2 ll + 1 of stream hf
+    const float2* PgLo = CT_DEBUG_CHECKS ? Pacc + (gi * H + hf) * TCP * LW : nullptr;   // this stream's accumulator
+    const float2* PgHi = PgLo + TCP * LW;
 #pragma unroll
     for (int c = 0; c < TCP; c++) Pg[c * LW] = make_float2(0.0f, 0.0f);
     const Wedge w = make_wedge(g, vw.x, vw.y, c0, TC);
@@ -512,17 +522,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
 
                     float2* p = Pg + (min(f0.cA, f1.cA) - c0 + CB) * LW;
                     switch (dd) {
-                        case -3: acc_pair<3, 0, LW>(p, f0, A0, f1, A1); break;
-                        case -2: acc_pair<2, 0, LW>(p, f0, A0, f1, A1); break;
-                        case -1: acc_pair<1, 0, LW>(p, f0, A0, f1, A1); break;
-                        case 0: acc_pair<0, 0, LW>(p, f0, A0, f1, A1); break;
-                        case 1: acc_pair<0, 1, LW>(p, f0, A0, f1, A1); break;
-                        case 2: acc_pair<0, 2, LW>(p, f0, A0, f1, A1); break;
-                        default: acc_pair<0, 3, LW>(p, f0, A0, f1, A1); break;
+                        case -3: acc_pair<3, 0, LW>(p, f0, A0, f1, A1, PgLo, PgHi); break;
+                        case -2: acc_pair<2, 0, LW>(p, f0, A0, f1, A1, PgLo, PgHi); break;
+                        case -1: acc_pair<1, 0, LW>(p, f0, A0, f1, A1, PgLo, PgHi); break;
+                        case 0: acc_pair<0, 0, LW>(p, f0, A0, f1, A1, PgLo, PgHi); break;
+                        case 1: acc_pair<0, 1, LW>(p, f0, A0, f1, A1, PgLo, PgHi); break;
+                        case 2: acc_pair<0, 2, LW>(p, f0, A0, f1, A1, PgLo, PgHi); break;
+                        default: acc_pair<0, 3, LW>(p, f0, A0, f1, A1, PgLo, PgHi); break;
                     }
                 } else {
-                    if (f0.n > 0) acc_one<LW>(Pg + (f0.cA - c0 + CB) * LW, f0, A0);
-                    if (f1.n > 0) acc_one<LW>(Pg + (f1.cA - c0 + CB) * LW, f1, A1);
+                    if (f0.n > 0) acc_one<LW>(Pg + (f0.cA - c0 + CB) * LW, f0, A0, PgLo, PgHi);
+                    if (f1.n > 0) acc_one<LW>(Pg + (f1.cA - c0 + CB) * LW, f1, A1, PgLo, PgHi);
                 }
             }
             __syncwarp();
@@ -973,11 +983,21 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 if (vbv) wb.init(fb, g, z0, lane, rlb, nrb, QPB);
                 float* accl = acc + z0 + lane;
                 float sf = 0.0f;   // (float)s0
+#if CT_DEBUG_CHECKS
+                for (int s0 = 0; s0 < nzs; s0 += 31) {
+                    const float c = (va ? wa.contrib((float)s0) : 0.0f) + (vbv ? wb.contrib((float)s0) : 0.0f);
+                    CT_DCHECK(z0 + s0 + lane < nz + kBackPad);
+                    // tail lanes add exactly 0, except past the volume's last slice (window clamped
+                    // to nz - 1), where they land in the discarded padding slots
+                    CT_DCHECK((s0 + lane < nzs && lane < 31) || c == 0.0f || z0 + s0 + lane >= nz);
+                }
+#endif
                 if (va && vbv) {
 #pragma unroll 1
                     for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) {
                         // no predicate: lanes past the union window (and lane 31, whose up = pf) add
-                        // exactly 0 (both edges clamp to the same u), into slots < nz + kBackPad
+                        // exactly 0 (both edges clamp to the same u), or, past a window clamped to the
+                        // volume's last slice, land in the padding slots [nz, nz + kBackPad)
                         const float c = wa.contrib(sf) + wb.contrib(sf);
                         accl[s0] += c;
                     }
