@@ -328,6 +328,27 @@ int ct_comm_init_zslab(ct_geom* g, int rank, int nranks, const void* nccl_uid128
 int ct_comm_get_unique_id(void* nccl_uid_out128);
 
 /*
+ * Exchange of the row-slab multi-rank path (SURVEY §8(e) "Helical (c4, c5):
+ * band-limited exchange"):
+ *   CT_EXCHANGE_FULL  reduce-scatter of the full partial image into row slabs, all-gather of x+;
+ *   CT_EXCHANGE_BAND  a rank's partial back-projection of a subset is non-zero only in the
+ *                     z-band of slices its contiguous view block can see (source heights of the
+ *                     block +- the cone's z reach), and its next forward projection reads x only
+ *                     there: only those z-band blocks are exchanged (grouped send / receive, a
+ *                     fixed rank-order sum), plus one boundary row each way for the stencil and
+ *                     one full all-gather per outer iteration;
+ *   CT_EXCHANGE_AUTO  BAND for helical scans with 2..16 ranks each owning >= 1 image row, else FULL
+ *                     (the default).
+ * Call before creating OS-LALM states.  CT_EINVAL for an unknown mode, CT_EUNSUPPORTED for BAND
+ * on a fan-beam geometry (an axial scan's bands cover the whole volume: it runs, exchanging
+ * the same bytes as FULL).
+ */
+#define CT_EXCHANGE_AUTO 0
+#define CT_EXCHANGE_FULL 1
+#define CT_EXCHANGE_BAND 2
+int ct_comm_set_exchange(ct_geom* g, int mode);
+
+/*
  * Virtual ranks (validation of the multi-rank path on ONE device):
  * attach `nranks` distinct geometry handles gs[0..nranks-1] of one device to one group of
  * virtual ranks (rank r = gs[r]; zslab != 0: gs[r] is rank r's z-slab geometry, as for

@@ -201,6 +201,26 @@ struct NcclComm : Comm {
         ncclResult_t r2 = g_nccl.GroupEnd();
         return rc(r != ncclSuccess ? r : r2, "z-slab halo exchange");
     }
+    int alltoallv(const float* const* send, const size_t* scount, float* const* recv, const size_t* rcount,
+                  cudaStream_t st) override {
+        if (scount[rank] != rcount[rank]) {
+            snprintf(err, sizeof(err), "alltoallv: self block %zu != %zu", scount[rank], rcount[rank]);
+            return -1;
+        }
+        if (scount[rank] && cudaMemcpyAsync(recv[rank], send[rank], scount[rank] * 4, cudaMemcpyDeviceToDevice, st) !=
+                                cudaSuccess) {
+            snprintf(err, sizeof(err), "alltoallv: self copy failed");
+            return -1;
+        }
+        ncclResult_t r = g_nccl.GroupStart();
+        for (int q = 0; q < nranks && r == ncclSuccess; q++) {
+            if (q == rank) continue;
+            if (scount[q]) r = g_nccl.Send(send[q], scount[q], ncclFloat32, q, comm, st);
+            if (r == ncclSuccess && rcount[q]) r = g_nccl.Recv(recv[q], rcount[q], ncclFloat32, q, comm, st);
+        }
+        ncclResult_t r2 = g_nccl.GroupEnd();
+        return rc(r != ncclSuccess ? r : r2, "band exchange (grouped send/recv)");
+    }
 };
 
 
@@ -217,6 +237,7 @@ struct ct_geom {
     int rank = 0, nranks = 1;
     Comm* comm = nullptr;    // exchange backend (NcclComm / VirtualComm); owned
     int zslab = 0;   // NEXT-3: this geometry is rank `rank`'s z-slab of the volume (sinogram-domain sums)
+    int exchange = CT_EXCHANGE_AUTO;   // row-slab path: full reduce-scatter / all-gather or z-band blocks
 };
 
 static int comm_rc(const ct_geom* g, int rc) {
@@ -800,6 +821,8 @@ struct ct_oslalm_state {
     bool has_comm = false;
     size_t S = 0, off0 = 0, Npad = 0;
     float* xp[2] = {nullptr, nullptr};   // full images (all-gathered), ping-pong
+    int band = 0;                        // band-limited exchange (helical row slabs)
+    float* bbuf[4] = {nullptr, nullptr, nullptr, nullptr};   // reduce send / recv, gather send / recv
     double* xi_ex = nullptr;             // [0] this rank's xi, [1] all-reduced xi, [2..3] BB sums
     float* xprev = nullptr;              // BB: xbar of the previous outer iteration
     float* xbar = nullptr;               // BB: mean of the current iteration's inner iterates
@@ -908,6 +931,19 @@ static bool use_slabs(const ct_geom* g, const ct_oslalm_cfg* c) {
     return g->comm != nullptr && !g->zslab && c->inner == CT_INNER_SQS;
 }
 
+// Band-limited exchange for the row-slab path: helical scans, 2..16 ranks,
+// every rank owning at least one image row, unless ct_comm_set_exchange chose FULL.
+static bool use_band(const ct_geom* g, const ct_oslalm_cfg* c) {
+    if (!use_slabs(g, c) || g->nranks < 2 || g->nranks > kMaxBandRanks) return false;
+    if (g->exchange == CT_EXCHANGE_FULL) return false;
+    if (g->exchange == CT_EXCHANGE_AUTO && g->d.kind != CT_CONE_HELICAL) return false;
+    if (g->d.kind == CT_FAN2D) return false;
+    int iy0, iy1;
+    size_t S;
+    slab_geometry(g, g->nranks, g->nranks - 1, &iy0, &iy1, &S);
+    return iy1 > iy0;
+}
+
 static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16], size_t* total) {
     int iy0, iy1;
     size_t S;
@@ -937,6 +973,7 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16
     // forward-projection scratch (fan accumulator for one subset's views; z-slab ranks project
     // whole subsets too; cone column extents)
     off[14] = o; o += fwd_scratch_bytes(g, maxcount);
+    off[15] = o; o += use_band(g, c) ? 4 * align256(N * 4) : 0;   // band exchange buffers
     *total = o;
 }
 
@@ -990,6 +1027,9 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
     }
     s->xi_ex = (double*)(b + off[11]);
     s->fs = fwd_scratch_at(g, b + off[14]);
+    s->band = use_band(g, c) ? 1 : 0;
+    if (s->band)
+        for (int i = 0; i < 4; i++) s->bbuf[i] = (float*)(b + off[15] + i * align256(s->Npad * 4));
     if (g->zslab) {
         const size_t ncols = (size_t)g->d.nx * g->d.ny, fb = align256(ncols * 4);
         s->zsend[0] = (float*)(b + off[13]);
@@ -1118,6 +1158,124 @@ static int zslab_halo(const ct_geom* g, const T* x, T* send_lo, T* send_hi, T* r
 }
 
 
+// Slices [b0, b1) in which rank q's partial back-projection of subset m can be non-zero, and
+// which its forward projection of subset m reads: the source heights of its contiguous view
+// block widened by the cone's z reach (dg.zhalf, a bound over every voxel) and one slice.
+static void rank_band(const ct_geom* g, int M, int m, int q, int* b0, int* b1) {
+    const DevGeom& dg = g->dg;
+    const int count = (g->d.na - m + M - 1) / M;
+    const int base = count / g->nranks, extra = count % g->nranks;
+    const int k0 = q * base + std::min(q, extra), n = base + (q < extra ? 1 : 0);
+    if (n <= 0) {
+        *b0 = *b1 = 0;
+        return;
+    }
+    const double za = (double)dg.zs0 + (double)(m + k0 * M) * dg.dzs, zb = (double)dg.zs0 + (double)(m + (k0 + n - 1) * M) * dg.dzs;
+    const double zh = (double)dg.zhalf + dg.dz;
+    *b0 = std::max(0, (int)floor((std::min(za, zb) - zh - dg.zb0) / dg.dz) - 1);
+    *b1 = std::min(g->d.nz, (int)ceil((std::max(za, zb) + zh - dg.zb0) / dg.dz) + 1);
+    if (*b1 < *b0) *b1 = *b0;
+}
+
+static void rank_rows(const ct_geom* g, int q, int* iy0, int* rows) {
+    int a, b;
+    size_t S;
+    slab_geometry(g, g->nranks, q, &a, &b, &S);
+    *iy0 = a;
+    *rows = b - a;
+}
+
+static unsigned band_grid(size_t n) { return (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16); }
+
+// G+ slab of this rank (rows [iy0, iy1), all slices) = sum over ranks of their partial
+// back-projections Gpart, exchanging only the z-band blocks (replaces the reduce-scatter).
+static int band_reduce(ct_oslalm_state* s, int m, const float* Gpart, float* Gnew, cudaStream_t st) {
+    const ct_geom* g = s->g;
+    const int P = s->P, p = s->prank, nx = g->d.nx, nz = g->d.nz;
+    int b0[kMaxBandRanks], b1[kMaxBandRanks], ry[kMaxBandRanks], rn[kMaxBandRanks];
+    for (int q = 0; q < P; q++) {
+        rank_band(g, s->cfg.M, m, q, &b0[q], &b1[q]);
+        rank_rows(g, q, &ry[q], &rn[q]);
+    }
+    const float* sptr[kMaxBandRanks];
+    float* rptr[kMaxBandRanks];
+    size_t sc[kMaxBandRanks], rc[kMaxBandRanks];
+    size_t so = 0, ro = 0;
+    BandSet bs{};
+    bs.P = P;
+    const int bl = b1[p] - b0[p];
+    for (int q = 0; q < P; q++) {
+        // to q: q's rows of my partial, my band
+        sc[q] = q == p ? 0 : (size_t)rn[q] * nx * bl;
+        sptr[q] = s->bbuf[0] + so;
+        if (sc[q]) {
+            band_pack_kernel<<<band_grid(sc[q]), 256, 0, st>>>(Gpart, s->bbuf[0] + so, ry[q], rn[q], nx, nz, b0[p], bl);
+            CT_LAUNCHED(1);
+        }
+        so += sc[q];
+        // from q: my rows of q's partial, q's band (my own block packed locally)
+        const size_t n = (size_t)rn[p] * nx * (b1[q] - b0[q]);
+        rc[q] = q == p ? 0 : n;
+        rptr[q] = s->bbuf[1] + ro;
+        if (q == p && n) {
+            band_pack_kernel<<<band_grid(n), 256, 0, st>>>(Gpart, s->bbuf[1] + ro, ry[p], rn[p], nx, nz, b0[p], bl);
+            CT_LAUNCHED(1);
+        }
+        bs.buf[q] = s->bbuf[1] + ro;
+        bs.b0[q] = b0[q];
+        bs.b1[q] = b1[q];
+        ro += n;
+    }
+    if (int e = comm_rc(g, g->comm->alltoallv(sptr, sc, rptr, rc, st))) return e;
+    band_sum_kernel<<<band_grid((size_t)rn[p] * nx * nz), 256, 0, st>>>(Gnew, ry[p], rn[p], nx, nz, bs);
+    CT_LAUNCHED(1);
+    return CT_OK;
+}
+
+// After the K3 update of this rank's rows of xb: the neighbours' boundary rows (every slice;
+// the next update's stencil) and every other rank's rows inside this rank's band of subset m
+// (its next forward projection) -- replaces the all-gather.
+static int band_gather(ct_oslalm_state* s, int m, float* xb, cudaStream_t st) {
+    const ct_geom* g = s->g;
+    const int P = s->P, p = s->prank, nx = g->d.nx, nz = g->d.nz;
+    const size_t row = (size_t)nx * nz;
+    int b0[kMaxBandRanks], b1[kMaxBandRanks], ry[kMaxBandRanks], rn[kMaxBandRanks];
+    for (int q = 0; q < P; q++) {
+        rank_band(g, s->cfg.M, m, q, &b0[q], &b1[q]);
+        rank_rows(g, q, &ry[q], &rn[q]);
+    }
+    const int y0 = ry[p], y1 = ry[p] + rn[p];
+    if (int e = comm_rc(g, g->comm->halo(xb + (size_t)y0 * row, xb + (size_t)(y1 - 1) * row,
+                                         y0 > 0 ? xb + (size_t)(y0 - 1) * row : nullptr,
+                                         y1 < g->d.ny ? xb + (size_t)y1 * row : nullptr, row, COMM_F32, st)))
+        return e;
+    const float* sptr[kMaxBandRanks];
+    float* rptr[kMaxBandRanks];
+    size_t sc[kMaxBandRanks], rc[kMaxBandRanks];
+    size_t so = 0, ro = 0;
+    for (int q = 0; q < P; q++) {
+        // to q: my rows, q's band
+        sc[q] = q == p ? 0 : (size_t)rn[p] * nx * (b1[q] - b0[q]);
+        sptr[q] = s->bbuf[2] + so;
+        if (sc[q]) {
+            band_pack_kernel<<<band_grid(sc[q]), 256, 0, st>>>(xb, s->bbuf[2] + so, ry[p], rn[p], nx, nz, b0[q], b1[q] - b0[q]);
+            CT_LAUNCHED(1);
+        }
+        so += sc[q];
+        // from q: q's rows, my band
+        rc[q] = q == p ? 0 : (size_t)rn[q] * nx * (b1[p] - b0[p]);
+        rptr[q] = s->bbuf[3] + ro;
+        ro += rc[q];
+    }
+    if (int e = comm_rc(g, g->comm->alltoallv(sptr, sc, rptr, rc, st))) return e;
+    for (int q = 0; q < P; q++)
+        if (rc[q]) {
+            band_unpack_kernel<<<band_grid(rc[q]), 256, 0, st>>>(xb, rptr[q], ry[q], rn[q], nx, nz, b0[p], b1[p] - b0[p]);
+            CT_LAUNCHED(1);
+        }
+    return CT_OK;
+}
+
 // G+ = M A_m'(W (A_m x - y)) for subset m with the requested epilogue.
 static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const float* x, int m, int epi, cudaStream_t st) {
     // the fused K4 logs into slot s->log_slot (set by the caller)
@@ -1190,7 +1348,11 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
         if (int e = launch_back<EPI_STORE>(g, v, s->sino, s->Gtmp, ga, st)) return e;
         tmark_end(s, st, 2, t1);
         int t2 = tmark(s, st);
-        if (int e = comm_rc(g, g->comm->reduce_scatter_sum(s->Gtmp, Gnew + s->off0, s->S, st))) return e;
+        if (s->band) {   // helical: z-band blocks instead of the full reduce-scatter
+            if (int e = band_reduce(s, m, s->Gtmp, Gnew, st)) return e;
+        } else {
+            if (int e = comm_rc(g, g->comm->reduce_scatter_sum(s->Gtmp, Gnew + s->off0, s->S, st))) return e;
+        }
         const size_t j0 = s->off0, j1 = std::min(s->N, s->off0 + s->S);
         if (epi == EPI_INIT) {
             if (j1 > j0) CT_CUDA(cudaMemcpyAsync(s->gs + j0, Gnew + j0, (j1 - j0) * 4, cudaMemcpyDeviceToDevice, st));
@@ -1268,7 +1430,9 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
                 }
                 CT_LAUNCHED(1);
             }
-            if (s->slab) {   // every rank needs the full x+ for its next forward projection
+            if (s->band) {   // x+ inside the next subset's band (+ the stencil's halo rows)
+                if (int e = band_gather(s, s->order[(j + 1) % M], xb, st)) return e;
+            } else if (s->slab) {   // every rank needs the full x+ for its next forward projection
                 if (int e = comm_rc(g, g->comm->all_gather(xb + s->off0, xb, s->S, st))) return e;
             }
         } else {
@@ -1324,6 +1488,8 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
             kernels += 1;
         }
     }
+    if (s->band)   // the iterate in full on every rank once per outer iteration
+        if (int e = comm_rc(g, g->comm->all_gather(xa + s->off0, xa, s->S, st))) return e;
     if (xa != x) {
         CT_CUDA(cudaMemcpyAsync(x, xa, s->N * 4, cudaMemcpyDeviceToDevice, st));
     }
@@ -1500,6 +1666,16 @@ extern "C" int ct_comm_init(ct_geom* g, int rank, int nranks, const void* uid) {
     g->rank = rank;
     g->nranks = nranks;
     g->zslab = 0;
+    return CT_OK;
+}
+
+extern "C" int ct_comm_set_exchange(ct_geom* g, int mode) {
+    if (!g) return fail(CT_EINVAL, "ct_comm_set_exchange: null geometry");
+    if (mode != CT_EXCHANGE_AUTO && mode != CT_EXCHANGE_FULL && mode != CT_EXCHANGE_BAND)
+        return fail(CT_EINVAL, "ct_comm_set_exchange: bad mode %d", mode);
+    if (mode == CT_EXCHANGE_BAND && g->d.kind == CT_FAN2D)
+        return fail(CT_EUNSUPPORTED, "band-limited exchange needs a cone-beam geometry");
+    g->exchange = mode;
     return CT_OK;
 }
 

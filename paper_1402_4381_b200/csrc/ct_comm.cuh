@@ -42,6 +42,11 @@ struct Comm {
     // neighbour exchange along the rank order: recv_lo <- (rank - 1).send_hi, recv_hi <- (rank + 1).send_lo
     virtual int halo(const void* send_lo, const void* send_hi, void* recv_lo, void* recv_hi, size_t n, int dt,
                      cudaStream_t st) = 0;
+    // personalised exchange (fp32): send[q] (scount[q] floats) goes to rank q, recv[q] (rcount[q]
+    // floats) comes from rank q; q = rank is a local copy; zero counts are skipped.  Every pair
+    // of ranks must agree on the counts (rank q's scount[p] = rank p's rcount[q]).
+    virtual int alltoallv(const float* const* send, const size_t* scount, float* const* recv, const size_t* rcount,
+                          cudaStream_t st) = 0;
 };
 
 template <class T>
@@ -54,7 +59,7 @@ __global__ void comm_add_kernel(T* __restrict__ dst, const T* __restrict__ src, 
 // Virtual ranks
 // ---------------------------------------------------------------------------
 struct VirtualGroup {
-    enum Op { OP_ALLREDUCE = 1, OP_REDUCE_SCATTER = 2, OP_ALL_GATHER = 3, OP_HALO = 4 };
+    enum Op { OP_ALLREDUCE = 1, OP_REDUCE_SCATTER = 2, OP_ALL_GATHER = 3, OP_HALO = 4, OP_ALLTOALLV = 5 };
     struct Slot {
         int op;
         const void* send;
@@ -64,6 +69,10 @@ struct VirtualGroup {
         size_t n;
         int dt;
         cudaStream_t st;
+        std::vector<const float*> vs;   // OP_ALLTOALLV: per-peer buffers and counts
+        std::vector<size_t> vsc;
+        std::vector<float*> vr;
+        std::vector<size_t> vrc;
     };
     int P = 0, device = 0;
     std::mutex mu;
@@ -158,6 +167,19 @@ struct VirtualGroup {
                             e = cudaMemcpyAsync(dst, slots[q].send, n * 4, cudaMemcpyDeviceToDevice, gst);
                     }
                 break;
+            case OP_ALLTOALLV:
+                for (int p = 0; p < P && e == cudaSuccess; p++)
+                    for (int q = 0; q < P && e == cudaSuccess; q++) {
+                        // rank q's block for p -> rank p's block from q
+                        const size_t c = slots[q].vsc[p];
+                        if (c != slots[p].vrc[q]) {
+                            snprintf(err, sizeof(err), "virtual ranks: alltoallv count mismatch %d->%d (%zu vs %zu)",
+                                     q, p, c, slots[p].vrc[q]);
+                            return cudaErrorInvalidValue;
+                        }
+                        if (c) e = cudaMemcpyAsync(slots[p].vr[q], slots[q].vs[p], c * 4, cudaMemcpyDeviceToDevice, gst);
+                    }
+                break;
             case OP_HALO:
                 for (int p = 0; p < P && e == cudaSuccess; p++) {
                     if (p > 0 && slots[p].recv)
@@ -235,6 +257,15 @@ struct VirtualComm : Comm {
              cudaStream_t st) override {
         return run(VirtualGroup::OP_HALO, send_lo, send_hi, rank > 0 ? recv_lo : nullptr,
                    rank < nranks - 1 ? recv_hi : nullptr, n, dt, st);
+    }
+    int alltoallv(const float* const* send, const size_t* scount, float* const* recv, const size_t* rcount,
+                  cudaStream_t st) override {
+        VirtualGroup::Slot s{VirtualGroup::OP_ALLTOALLV, nullptr, nullptr, nullptr, nullptr, 0, COMM_F32, st};
+        s.vs.assign(send, send + nranks);
+        s.vsc.assign(scount, scount + nranks);
+        s.vr.assign(recv, recv + nranks);
+        s.vrc.assign(rcount, rcount + nranks);
+        return grp->collective(rank, s, err, sizeof(err));
     }
 };
 

@@ -1357,6 +1357,53 @@ __global__ void __launch_bounds__(256) gupd_kernel(const float* __restrict__ Gp,
     xi_arrive<256>(ga, gridDim.x);
 }
 
+// ---------------------------------------------------------------------------
+// Band-limited exchange of the helical multi-rank path: a rank's partial
+// back-projection is non-zero only in the z-band of slices its contiguous view block can see,
+// and its next forward projection reads x only there.  Blocks of rows [ra, ra + rows) x
+// slices [b0, b0 + bl) of an [*][nx][nz] image travel packed as [(iy - ra) nx + ix][z - b0].
+// ---------------------------------------------------------------------------
+constexpr int kMaxBandRanks = 16;
+
+__global__ void __launch_bounds__(256) band_pack_kernel(const float* __restrict__ img, float* __restrict__ buf, int ra,
+                                                       int rows, int nx, int nz, int b0, int bl) {
+    const size_t n = (size_t)rows * nx * bl;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t c = i / bl;
+        buf[i] = img[((size_t)ra * nx + c) * nz + b0 + (int)(i - c * bl)];
+    }
+}
+
+__global__ void __launch_bounds__(256) band_unpack_kernel(float* __restrict__ img, const float* __restrict__ buf, int ra,
+                                                         int rows, int nx, int nz, int b0, int bl) {
+    const size_t n = (size_t)rows * nx * bl;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t c = i / bl;
+        img[((size_t)ra * nx + c) * nz + b0 + (int)(i - c * bl)] = buf[i];
+    }
+}
+
+struct BandSet {
+    const float* buf[kMaxBandRanks];   // rank q's block for this rank's rows, slices [b0[q], b1[q])
+    int b0[kMaxBandRanks], b1[kMaxBandRanks];
+    int P;
+};
+
+// dst rows [ra, ra + rows), every slice: the sum over ranks q = 0 .. P-1 (fixed order) of
+// rank q's block where the slice lies in its band (0 elsewhere).
+__global__ void __launch_bounds__(256) band_sum_kernel(float* __restrict__ dst, int ra, int rows, int nx, int nz,
+                                                      BandSet bs) {
+    const size_t n = (size_t)rows * nx * nz;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t c = i / nz;
+        const int z = (int)(i - c * nz);
+        float v = 0.0f;
+        for (int q = 0; q < bs.P; q++)
+            if (z >= bs.b0[q] && z < bs.b1[q]) v += bs.buf[q][c * (size_t)(bs.b1[q] - bs.b0[q]) + (z - bs.b0[q])];
+        dst[(size_t)ra * nx * nz + i] = v;
+    }
+}
+
 // Multi-rank slab path: G+ (already reduce-scattered into G_new[j0, j1)) -> g-update and
 // this rank's xi; the last block stores the rank's fixed-order xi sum in *xi_out (the
 // ranks' sums are then all-reduced and xi_rule_kernel applies K4 on every rank).

@@ -29,7 +29,7 @@ EXPORTS = ("ct_geom_create", "ct_geom_destroy", "ct_last_error", "ct_fwd_proj", 
            "ct_sqs_denom_scratch_bytes", "ct_sqs_denom", "ct_reg_grad", "ct_count_vv", "ct_oslalm_state_bytes",
            "ct_oslalm_state_create", "ct_fbp", "ct_fbp_scratch_bytes", "ct_peak_l2_read", "ct_oslalm_state_destroy", "ct_oslalm_state_get", "ct_oslalm_state_reset",
            "ct_oslalm_set_timing", "ct_oslalm_get_timing", "ct_oslalm_iter",
-           "ct_oslalm_run", "ct_comm_init", "ct_comm_init_zslab", "ct_comm_init_virtual", "ct_comm_get_unique_id", "ct_build_info", "ct_kernel_launches")
+           "ct_oslalm_run", "ct_comm_init", "ct_comm_init_zslab", "ct_comm_init_virtual", "ct_comm_set_exchange", "ct_comm_get_unique_id", "ct_build_info", "ct_kernel_launches")
 
 
 class CTError(RuntimeError):
@@ -113,6 +113,7 @@ def load():
     L.ct_comm_init.argtypes = [vp, i, i, vp]
     L.ct_comm_init_zslab.argtypes = [vp, i, i, vp]
     L.ct_comm_init_virtual.argtypes = [P(vp), i, i]
+    L.ct_comm_set_exchange.argtypes = [vp, i]
     L.ct_comm_get_unique_id.argtypes = [vp]
     _check_provenance(L)
     _lib = L
@@ -277,6 +278,15 @@ def ct_comm_init(h, rank, nranks, uid: bytes, zslab=False):
     buf = ctypes.create_string_buffer(bytes(uid), 128)
     f = load().ct_comm_init_zslab if zslab else load().ct_comm_init
     _check(f(h, int(rank), int(nranks), buf))
+
+
+EXCHANGE = {"auto": 0, "full": 1, "band": 2}
+
+
+def ct_comm_set_exchange(h, mode="auto"):
+    """Row-slab multi-rank exchange: "full" (reduce-scatter / all-gather), "band" (z-band blocks,
+    helical) or "auto" (band for helical scans)."""
+    _check(load().ct_comm_set_exchange(h, EXCHANGE[mode]))
 
 
 def ct_comm_init_virtual(handles, zslab=False):

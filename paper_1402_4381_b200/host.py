@@ -9,6 +9,8 @@
 * ``rank_slab`` — the multi-GPU partition of the image for the SQS update: rank p owns a
   contiguous block of image rows (iy); buffers are padded to P equal slabs (mirror of
   ``slab_geometry`` in ct_abi.cu).
+* ``rank_band`` — the z-band of slices a rank's view block of a subset can see (band-limited
+  exchange of helical scans; mirror of ``rank_band`` in ct_abi.cu).
 """
 from __future__ import annotations
 
@@ -48,3 +50,32 @@ def rank_zslab(nz: int, rank: int, nranks: int) -> tuple[int, int]:
     base, extra = divmod(nz, nranks)
     z0 = rank * base + min(rank, extra)
     return z0, z0 + base + (1 if rank < extra else 0)
+
+
+def helical_zhalf(g: dict) -> float:
+    """Bound on |z - z_s| of any voxel a view can see (mm): half the detector height (plus its
+    offset) at the smallest magnification, plus one slice (mirror of DevGeom.zhalf)."""
+    hx = 0.5 * (g["nx"] - 1) * g["dx"] + abs(g.get("offx", 0.0)) + g["dx"]
+    hy = 0.5 * (g["ny"] - 1) * g["dy"] + abs(g.get("offy", 0.0)) + g["dy"]
+    rmax = math.hypot(hx, hy)
+    return (0.5 * g["nt"] * g["dt"] + 0.5 * abs(g.get("offt", 0.0)) * g["dt"]) * (g["dso"] + rmax) / g["dsd"] + g["dz"]
+
+
+def rank_band(g: dict, M: int, m: int, rank: int, nranks: int) -> tuple[int, int]:
+    """Slices [b0, b1) in which `rank`'s partial back-projection of subset m can be non-zero:
+    the source heights of its contiguous view block widened by the cone's z reach and one
+    slice (helical scans)."""
+    count = (g["na"] - m + M - 1) // M
+    k0, n = rank_view_block(count, rank, nranks)
+    if n <= 0:
+        return 0, 0
+    turns = g["orbit_deg"] / 360.0
+    h = g["pitch"] * g["nt"] * g["dt"] * g["dso"] / g["dsd"]
+    dzs = h / (g["na"] / turns)
+    zs0 = -(g["na"] - 1) / 2.0 * dzs
+    za, zb = zs0 + (m + k0 * M) * dzs, zs0 + (m + (k0 + n - 1) * M) * dzs
+    zh = helical_zhalf(g) + g["dz"]
+    zb0 = -(g["nz"] - 1) / 2.0 * g["dz"] + g.get("offz", 0.0) - 0.5 * g["dz"]
+    b0 = max(0, math.floor((min(za, zb) - zh - zb0) / g["dz"]) - 1)
+    b1 = min(g["nz"], math.ceil((max(za, zb) + zh - zb0) / g["dz"]) + 1)
+    return b0, max(b0, b1)

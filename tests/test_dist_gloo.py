@@ -225,3 +225,30 @@ def test_gloo_two_rank_back_projection_sum(ws):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0] <= 1e-12 and res[1] <= 1e-12
+
+
+def test_rank_band_contains_every_seen_slice():
+    """Band-limited exchange (helical): every slice that any view of a rank's block of a subset
+    sees (a non-zero oracle projection of that slice alone) lies inside host.rank_band, and the
+    bands are much narrower than the volume on a long helix (the exchange saving)."""
+    import numpy as np
+    import oracle as O
+    from paper_1402_4381_b200 import host
+    from tests import geomutil as GU
+    g = GU.geom("cone_helical", nx=12, nz=40, dx=0.9766, dz=0.625, ns=24, ds=1.0239, nt=6, dt=1.0964, na=144,
+                turns=6.0, pitch=0.8)
+    M, P = 4, 3
+    widths = []
+    for m in range(M):
+        count = O.nviews(g, m, M)
+        for r in range(P):
+            k0, n = host.rank_view_block(count, r, P)
+            b0, b1 = host.rank_band(g, M, m, r, P)
+            widths.append(b1 - b0)
+            for z in range(g["nz"]):
+                x = np.zeros(O.img_shape(g))
+                x[z] = 1.0
+                p = O.fwd(g, x, m + k0 * M, M, n)
+                if np.abs(p).max() > 0:
+                    assert b0 <= z < b1, (m, r, z, b0, b1)
+    assert max(widths) <= 0.75 * g["nz"]
