@@ -207,12 +207,16 @@ typedef struct {
     int n_inner;      /* inner iterations: 1 for CT_INNER_SQS, 1..64 for FISTA   */
     int inner;        /* ct_inner_mode                                           */
     ct_reg reg;
-    /* Barzilai-Borwein scaling (NEXT-2, supplement P:1472-1492): with bb = 1 the
-     * SQS Hessian D_L is replaced by H_k = alpha_k D_L, alpha_k fitted to the secant
-     * equation y_k ~ H_k s_k in the D_L^{-1}-weighted least-squares sense, alpha <= 1:
-     *   alpha_k = min(1, max(alpha_min, y_k's_k / s_k'D_L s_k)),  s_k = x^k - x^{k-1},
-     * y_k = difference of the mean subset gradients of outer iterations k and k-1
-     * (reading B-BB); alpha = 1 for the first two outer iterations.          */
+    /* EXPERIMENTAL.  Barzilai-Borwein scaling (NEXT-2, supplement P:1472-1492): with
+     * bb = 1 the SQS Hessian D_L is replaced by H_k = alpha_k D_L, alpha_k fitted to the
+     * secant equation y_k ~ H_k s_k in the D_L^{-1}-weighted least-squares sense, alpha <= 1:
+     *   alpha_k = min(1, max(alpha_min, y_k's_k / s_k'D_L s_k)),
+     * s_k = xbar_k - xbar_{k-1} (xbar_k: mean of outer iteration k's inner iterates, the points
+     * its subset gradients were taken at), y_k = the difference of the mean subset gradients
+     * of outer iterations k and k-1 (reading B-BB; for M = 1, xbar_k = x^k and this
+     * is the paper's pair); alpha = 1 for the first two outer iterations.  With ordered subsets
+     * (M = 4 .. 24 from x = 0) alpha cycles and the scaled steps can collapse the image towards
+     * 0 (DESIGN.md B-BB): an option, not a default.                                        */
     int bb;           /* 0 or 1                                                  */
     double alpha_min; /* lower clip of alpha, in (0, 1] (1e-6)                   */
 } ct_oslalm_cfg;

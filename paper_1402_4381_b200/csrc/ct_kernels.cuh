@@ -1437,7 +1437,8 @@ __global__ void __launch_bounds__(256) gupd_slab_kernel(GupdArgs ga, size_t j0, 
 // ---------------------------------------------------------------------------
 // Barzilai-Borwein scale (NEXT-2, reading B-BB): at the end of outer
 // iteration k, over S and voxels [j0, j1) (this rank's rows):
-//   num = sum (gbar_k - gbar_{k-1})(x^k - x^{k-1}),  den = sum D_L (x^k - x^{k-1})^2,
+//   num = sum (gbar_k - gbar_{k-1})(xbar_k - xbar_{k-1}),  den = sum D_L (xbar_k - xbar_{k-1})^2  (xbar: the mean of
+//   the iteration's inner iterates, the points its subset gradients were taken at),
 // then x_prev <- xbar, gbar_prev <- gbar, gbar <- 0, xbar <- 0.  The last block (single rank) sets
 // alpha = clip(num / den, alpha_min, 1) once two iterations are complete; with several
 // ranks it stores (num, den) for an all-reduce and bb_rule_kernel applies the rule.

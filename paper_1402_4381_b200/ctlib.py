@@ -140,8 +140,10 @@ def _check(rc):
         raise CTError(f"{STATUS.get(rc, rc)}: {msg}")
 
 
-def _stream(stream=None):
-    s = torch.cuda.current_stream() if stream is None else stream
+def _stream(stream=None, h=None):
+    """The caller's stream (default: the current stream of the geometry's device)."""
+    s = (torch.cuda.current_stream(_dev(h)) if h is not None and _dev(h) is not None else torch.cuda.current_stream()) \
+        if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -177,6 +179,20 @@ def _na(h):
     return _SIZES[h.value][2] if h.value in _SIZES else 0
 
 
+def _dev(h):
+    return _SIZES[h.value][3] if h is not None and h.value in _SIZES else None
+
+
+def _on_dev(h, *tensors):
+    """Every tensor handed to a call on geometry h must live on h's device (the C ABI takes
+    bare pointers and launches on the geometry's device)."""
+    d = _dev(h)
+    if d is None:
+        return
+    for t in tensors:
+        if isinstance(t, torch.Tensor) and t.is_cuda and t.device.index != d:
+            raise CTError(f"tensor on cuda:{t.device.index}, geometry on cuda:{d}")
+
 # ---------------------------------------------------------------------------
 # ABI-named functions (marshalling only)
 # ---------------------------------------------------------------------------
@@ -195,7 +211,7 @@ def ct_geom_create(geom: dict, device: int = 0):
     _check(L.ct_geom_create(ctypes.byref(d), ctypes.byref(h)))
     is2d = geom["kind"] == "fan2d"
     _SIZES[h.value] = (int(geom["nx"]) * int(geom["ny"]) * (1 if is2d else int(geom["nz"])),
-                       int(geom["ns"]) * (1 if is2d else int(geom["nt"])), int(geom["na"]))
+                       int(geom["ns"]) * (1 if is2d else int(geom["nt"])), int(geom["na"]), int(device))
     return h
 
 
@@ -205,8 +221,9 @@ def ct_geom_destroy(h):
 
 
 def ct_fwd_proj(h, views, x, y, stream=None):
+    _on_dev(h, x, y)
     _check(load().ct_fwd_proj(h, ct_views(*views), _ptr(x, torch.float32, "x", _img(h)),
-                              _ptr(y, torch.float32, "y", _cells(h, views[2])), _stream(stream)))
+                              _ptr(y, torch.float32, "y", _cells(h, views[2])), _stream(stream, h)))
 
 
 def ct_peak_l2_read(device=0, mib=48, reps=200):
@@ -223,13 +240,15 @@ def ct_fbp_scratch_bytes(h):
 
 
 def ct_fbp(h, y, x, scratch, stream=None):
+    _on_dev(h, y, x, scratch)
     _check(load().ct_fbp(h, _ptr(y, torch.float32, "y", _cells(h, _na(h))), _ptr(x, torch.float32, "x", _img(h)),
-                         _ptr(scratch, torch.uint8, "scratch", ct_fbp_scratch_bytes(h)), _stream(stream)))
+                         _ptr(scratch, torch.uint8, "scratch", ct_fbp_scratch_bytes(h)), _stream(stream, h)))
 
 
 def ct_back_proj(h, views, y, x, accumulate=False, stream=None):
+    _on_dev(h, y, x)
     _check(load().ct_back_proj(h, ct_views(*views), _ptr(y, torch.float32, "y", _cells(h, views[2])),
-                               _ptr(x, torch.float32, "x", _img(h)), 1 if accumulate else 0, _stream(stream)))
+                               _ptr(x, torch.float32, "x", _img(h)), 1 if accumulate else 0, _stream(stream, h)))
 
 
 def ct_sqs_denom_scratch_bytes(h):
@@ -239,24 +258,27 @@ def ct_sqs_denom_scratch_bytes(h):
 
 
 def ct_sqs_denom(h, w, mask, dl, scratch, stream=None):
+    _on_dev(h, w, mask, dl, scratch)
     _check(load().ct_sqs_denom(h, _ptr(w, torch.float32, "w", _cells(h, _na(h))), _ptr(mask, torch.uint8, "mask", _img(h)),
                                _ptr(dl, torch.float32, "dl", _img(h)),
-                               _ptr(scratch, torch.uint8, "scratch", ct_sqs_denom_scratch_bytes(h)), _stream(stream)))
+                               _ptr(scratch, torch.uint8, "scratch", ct_sqs_denom_scratch_bytes(h)), _stream(stream, h)))
 
 
 def ct_reg_grad(h, reg, mask, x, grad, curv=None, stream=None):
+    _on_dev(h, mask, x, grad, curv)
     r = ct_reg(float(reg[0]), float(reg[1]), int(reg[2]))
     n = _img(h)
     _check(load().ct_reg_grad(h, ctypes.byref(r), _ptr(mask, torch.uint8, "mask", n), _ptr(x, torch.float32, "x", n),
                               _ptr(grad, torch.float32, "grad", n), _ptr(curv, torch.float32, "curv", n),
-                              _stream(stream)))
+                              _stream(stream, h)))
 
 
 def ct_count_vv(h, views, mask, scratch, stream=None):
+    _on_dev(h, mask, scratch)
     """Returns (U, nnz, C) of the view list (see the header)."""
     out = (ctypes.c_longlong * 3)()
     _check(load().ct_count_vv(h, ct_views(*views), _ptr(mask, torch.uint8, "mask", _img(h)),
-                              _ptr(scratch, torch.uint8, "scratch"), out, _stream(stream)))
+                              _ptr(scratch, torch.uint8, "scratch"), out, _stream(stream, h)))
     return tuple(int(v) for v in out)
 
 
@@ -358,7 +380,7 @@ class Geometry:
         scratch = torch.empty(n.value, dtype=torch.uint8, device=self.device)
         x = torch.empty(self.img_shape, dtype=torch.float32, device=self.device)
         _check(L.ct_fbp(self.h, _ptr(y, torch.float32, "y", _cells(self.h, self.na)), _ptr(x, torch.float32, "x"),
-                        ctypes.c_void_p(scratch.data_ptr()), _stream(stream)))
+                        ctypes.c_void_p(scratch.data_ptr()), _stream(stream, self.h)))
         return x
 
     def reg_grad(self, x, mask, beta, delta, nbr, want_curv=True):
@@ -418,14 +440,16 @@ class OSLALM:
             pass
 
     def set_data(self, y, w, dl, mask):
+        _on_dev(self.geo.h, y, w, dl, mask)
         self._keep = (y, w, dl, mask)
         h, na = self.geo.h, self.geo.na
         self._data = ct_oslalm_data(_ptr(y, torch.float32, "y", _cells(h, na)), _ptr(w, torch.float32, "w", _cells(h, na)),
                                     _ptr(dl, torch.float32, "dl", _img(h)), _ptr(mask, torch.uint8, "mask", _img(h)))
 
     def iterate(self, x, stream=None):
+        _on_dev(self.geo.h, x)
         _check(load().ct_oslalm_iter(self.geo.h, ctypes.byref(self.cfg), ctypes.byref(self._data), self.h,
-                                     _ptr(x, torch.float32, "x", _img(self.geo.h)), _stream(stream)))
+                                     _ptr(x, torch.float32, "x", _img(self.geo.h)), _stream(stream, self.geo.h)))
 
     def reset(self):
         _check(load().ct_oslalm_state_reset(self.h))
@@ -441,6 +465,7 @@ class OSLALM:
         return {names[i]: (ms[i], n[i]) for i in range(5)}
 
     def run(self, x, n_iter, log=False, stream=None):
+        _on_dev(self.geo.h, x)
         L = load()
         lg = None
         if log:
@@ -449,7 +474,7 @@ class OSLALM:
             lg = ct_oslalm_log(rho, xi, rs, cap, 0)
         _check(L.ct_oslalm_run(self.geo.h, ctypes.byref(self.cfg), ctypes.byref(self._data), self.h,
                                _ptr(x, torch.float32, "x", _img(self.geo.h)), int(n_iter), ctypes.byref(lg) if lg else None,
-                               _stream(stream)))
+                               _stream(stream, self.geo.h)))
         if log:
             n = lg.count
             return [(rho[i], xi[i], rs[i]) for i in range(n)]
