@@ -175,12 +175,15 @@ int ct_count_vv(const ct_geom* g, ct_views v, const uint8_t* mask, void* scratch
  * back-projection (FBP) reconstruction"; reading B-FBP): full-scan equiangular
  * fan-beam FBP (Ram-Lak taps, cos gamma pre-weight, 1/L^2 back-projection weight,
  * linear interpolation), with the FDK extension (cone weight D / sqrt(D^2 + zeta^2),
- * bilinear interpolation) for axial cone beam.
+ * bilinear interpolation) for axial cone beam.  Helical scans (the paper's helical cases
+ * start from an FBP image too; reading B-FBP-H): the same filtering and
+ * a back-projection over the views whose cone sees the voxel (projected row inside
+ * [0, nt - 1]), normalised by their number (2 pi / #seen instead of 2 pi / na).
  *   y        : [na][ns][nt] post-log sinogram (device, read-only)
  *   x        : [ny][nx][nz] output image in mm^-1 (device, overwritten)
  *   scratch  : ct_fbp_scratch_bytes() bytes of device memory (filtered sinogram)
- * Errors: CT_EINVAL (null pointers), CT_EUNSUPPORTED (helical scan, or an orbit that is
- * not one full turn).  The image is not clipped to x >= 0 (OS-LALM's first update does).
+ * Errors: CT_EINVAL (null pointers), CT_EUNSUPPORTED (a circular orbit that is not one full
+ * turn).  The image is not clipped to x >= 0 (OS-LALM's first update does).
  */
 int ct_fbp_scratch_bytes(const ct_geom* g, size_t* out);
 /* Diagnostic (no ct_geom): L2-resident read bandwidth of `device` in GB/s, measured by

@@ -248,13 +248,13 @@ def inner_fista(g, beta, delta, nbr, mask, dl, rho, xk, s, n):
 
 
 def fbp(g, p):
-    """FBP (fan) / FDK (cone, circular orbit) initial image of sinogram p (reading B-FBP);
-    raises for helical scans."""
+    """FBP (fan) / FDK (cone, circular orbit) initial image of sinogram p (reading B-FBP), or
+    the view-normalised helical FDK (reading B-FBP-H); raises for a partial circular orbit."""
     p, pp = _d(np.reshape(p, sino_shape(g, g["na"])))
     x = np.zeros(img_shape(g))
     _, xp = _d(x)
     if lib().or_fbp(geom(g), pp, xp) != 0:
-        raise ValueError("FBP needs a fan or axial cone scan over one full turn")
+        raise ValueError("FBP of a circular orbit needs one full turn")
     return x
 
 

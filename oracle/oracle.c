@@ -706,10 +706,17 @@ void or_oslalm_run(const or_geom* g, const double* y, const double* w, const dou
  * with D = dso, tau = ds/dsd the angular channel pitch, L the in-plane source-voxel
  * distance, gamma(p) / t(p) the fan angle / detector row height of the voxel centre
  * (O1), linear interpolation in gamma and t (0 outside the detector), dbeta = 2 pi / na.
- * Returns 0, or -1 for a helical scan or an orbit that is not one full turn.
+ * Helical scans (P:573, P:586 and P:1495 start the helical reconstructions from "the initial
+ * FBP image"; which FBP is not said -- reading B-FBP-H in DESIGN.md): the same row-wise
+ * filtering, and a voxel-driven back-projection over the views whose cone sees the voxel
+ * (projected row coordinate inside [0, nt-1]), normalised by their number:
+ *   f(p) = 2 pi * sum_{v seen} Q_v(gamma(p), t(p)) / L(p)^2 / #{v seen}
+ * (with every view seen this is the circular-orbit formula, dbeta = 2 pi / na).
+ * Returns 0, or -1 for a circular orbit that is not one full turn.
  */
 int or_fbp(const or_geom* g, const double* p, double* x) {
-    if (g->kind == OR_CONE_HELICAL || fabs(g->orbit_deg - 360.0) > 1e-9) return -1;
+    const int helical = g->kind == OR_CONE_HELICAL;
+    if (!helical && fabs(g->orbit_deg - 360.0) > 1e-9) return -1;
     int NT = ntv(g), NZ = nzv(g);
     double D = g->dso, tau = g->ds / g->dsd;
     int ns = g->ns;
@@ -747,12 +754,17 @@ int or_fbp(const or_geom* g, const double* p, double* x) {
         for (int iz = 0; iz < NZ; iz++)
             for (int ix = 0; ix < g->nx; ix++) {
                 double xc = vox_x(g, ix), yc = vox_y(g, iy), zc = vox_z(g, iz), acc = 0.0;
+                long long seen = 0;
                 for (int v = 0; v < g->na; v++) {
                     double b = or_view_angle(g, v), sb = sin(b), cb = cos(b);
                     double along = D + xc * sb - yc * cb, perp = xc * cb + yc * sb;
                     double L2 = along * along + perp * perp;
                     double uc = atan2(perp, along) / tau + c0;         /* channel coordinate */
                     double ur = g->kind == OR_FAN2D ? 0.0 : (zc - or_source_z(g, v)) * g->dsd / sqrt(L2) / g->dt + r0;
+                    if (helical) {
+                        if (!(ur >= 0.0 && ur <= NT - 1)) continue;   /* the view does not see the voxel */
+                        seen++;
+                    }
                     int k0 = (int)floor(uc), r0i = (int)floor(ur);
                     double fk = uc - k0, fr = ur - r0i, val = 0.0;
                     for (int a = 0; a < 2; a++)
@@ -764,7 +776,8 @@ int or_fbp(const or_geom* g, const double* p, double* x) {
                         }
                     acc += val / L2;
                 }
-                x[((size_t)iz * g->ny + iy) * g->nx + ix] = dbeta * acc;
+                x[((size_t)iz * g->ny + iy) * g->nx + ix] =
+                    helical ? (seen ? 2.0 * M_PI * acc / (double)seen : 0.0) : dbeta * acc;
             }
     free(q);
     free(gk);

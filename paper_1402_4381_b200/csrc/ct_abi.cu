@@ -649,8 +649,8 @@ extern "C" int ct_peak_l2_read(int device, size_t bytes, int reps, double* gbs) 
 
 // FBP / FDK initial image (NEXT-4; reading B-FBP)
 static int check_fbp(const ct_geom* g) {
-    if (g->d.kind == CT_CONE_HELICAL) return fail(CT_EUNSUPPORTED, "ct_fbp: helical scans are not supported");
-    if (fabs(g->d.orbit_deg - 360.0) > 1e-9) return fail(CT_EUNSUPPORTED, "ct_fbp needs one full turn (orbit 360 deg)");
+    if (g->d.kind != CT_CONE_HELICAL && fabs(g->d.orbit_deg - 360.0) > 1e-9)
+        return fail(CT_EUNSUPPORTED, "ct_fbp of a circular orbit needs one full turn (orbit 360 deg)");
     return CT_OK;
 }
 

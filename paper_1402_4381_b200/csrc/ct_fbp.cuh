@@ -2,7 +2,9 @@
 // filtered back-projection (FBP) reconstruction"; reading B-FBP in DESIGN.md).  sm_100a, fp32.
 //
 // Full-scan equiangular fan-beam FBP with the FDK extension for a cylindrical detector on a
-// circular orbit (helical scans: CT_EUNSUPPORTED):
+// circular orbit; for helical scans (reading B-FBP-H) the same filtering
+// and a back-projection over the views that see the voxel, normalised by their number:
+//   f(p) = 2 pi sum_{v seen} Q_v / L^2 / #{v seen}   (projected row inside [0, nt - 1]).
 //   R'(gamma_k, t) = R(gamma_k, t) D cos(gamma_k) D / sqrt(D^2 + zeta^2),  zeta = t dso/dsd
 //   Q(gamma_n, t)  = tau sum_k R'(gamma_k, t) g((n - k) tau),  g even, zero at even n != 0
 //   f(p)           = dbeta sum_v Q_v(gamma(p), t(p)) / L(p)^2     (bilinear in gamma, t)
@@ -50,7 +52,9 @@ __global__ void __launch_bounds__(256) fbp_filter_kernel(DevGeom g, const float*
     }
 }
 
-// Thread = voxel (z fastest, as the image layout): dbeta sum_v Q_v(gamma, t) / L^2.
+// Thread = voxel (z fastest, as the image layout): dbeta sum_v Q_v(gamma, t) / L^2; helical:
+// the views whose source height is within the cone's z reach of the voxel (dg.zhalf), those
+// whose projected row lies on the detector counted and averaged.
 __global__ void __launch_bounds__(256) fbp_back_kernel(DevGeom g, const float* __restrict__ q, float* __restrict__ x,
                                                       int count) {
     const size_t N = (size_t)g.nx * g.ny * g.nz;
@@ -62,12 +66,30 @@ __global__ void __launch_bounds__(256) fbp_back_kernel(DevGeom g, const float* _
     const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
     const float zc = g.zb0 + ((float)iz + 0.5f) * g.dz;   // voxel centre (axial: z_s = 0)
     const int ns = g.ns, nt = g.nt;
+    const bool helical = g.kind == 2 && g.dzs > 0.0f;
+    int v0 = 0, v1 = count;
+    if (helical) {   // views whose source height can be within the cone's reach of the voxel
+        const float zr = zc - g.zs0;
+        v0 = max(0, (int)floorf((zr - g.zhalf) / g.dzs) - 1);
+        v1 = min(count, (int)ceilf((zr + g.zhalf) / g.dzs) + 2);
+    }
     float acc = 0.0f;
-    for (int v = 0; v < count; v++) {
+    int seen = 0;
+    for (int v = v0; v < v1; v++) {
         const float4 vw = __ldg(&g.views[v]);
         const float sb = vw.x, cb = vw.y;
         const float along = g.dso + xc * sb - yc * cb, perp = xc * cb + yc * sb;
         const float L2 = along * along + perp * perp;
+        float ur = 0.0f;
+        if (nt > 1) {
+            // (z - z_s) / dz from the view table's exact split of the source height
+            const float dzr = ((float)iz + 0.5f - vw.z) - vw.w;
+            ur = dzr * g.dz * g.dsd / sqrtf(L2) / g.dt + g.rbase;
+            if (helical) {
+                if (!(ur >= 0.0f && ur <= (float)(nt - 1))) continue;
+                seen++;
+            }
+        }
         const float uc = atan2f(perp, along) * g.dsd_ds + g.cbase;
         const int k0 = __float2int_rd(uc);
         const float fk = uc - (float)k0;
@@ -78,7 +100,6 @@ __global__ void __launch_bounds__(256) fbp_back_kernel(DevGeom g, const float* _
             const float b = (k0 + 1 >= 0 && k0 + 1 < ns) ? __ldg(&qv[k0 + 1]) : 0.0f;
             val = a + fk * (b - a);
         } else {
-            const float ur = zc * g.dsd / sqrtf(L2) / g.dt + g.rbase;
             const int r0 = __float2int_rd(ur);
             const float fr = ur - (float)r0;
             float s = 0.0f;
@@ -95,7 +116,10 @@ __global__ void __launch_bounds__(256) fbp_back_kernel(DevGeom g, const float* _
         }
         acc += val / L2;
     }
-    x[j] = acc * (6.283185307179586f / (float)count);
+    if (helical)
+        x[j] = seen ? acc * (6.283185307179586f / (float)seen) : 0.0f;
+    else
+        x[j] = acc * (6.283185307179586f / (float)count);
 }
 
 }  // namespace ct

@@ -753,6 +753,9 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 #ifndef CT_BACK3D_PAIR
 #define CT_BACK3D_PAIR 0   // 1: two views per slice walk (one accumulator update per slice for both); A/B: slower (64 registers, 4 CTAs/SM: c5 11.25 -> 12.38 ms)
 #endif
+#ifndef CT_BACK3D_PREFETCH
+#define CT_BACK3D_PREFETCH 1   // L1 prefetch of the next view's detector rows
+#endif
 #ifndef CT_BACK3D_MINB
 // one view per walk: 5 CTAs/SM (A/B c3, c5: beats 4 by 2-3 %; 3 is 12 % slower); two views per
 // walk need 64 registers (48 spill ~200 bytes)
@@ -958,6 +961,19 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
             __syncwarp();
             const int nb = min(32, count - vb);
             for (int j = 0; j < nb; j += NQ) {
+#if CT_BACK3D_PREFETCH
+                // L1 prefetch of the next view's detector rows ([channel][row] block of n * nt
+                // floats, contiguous): their loads in step (1) then hit L1 instead of waiting on L2
+                if (j + NQ < nb) {
+                    const int* tn = reinterpret_cast<const int*>(&tab[j + NQ]);
+                    const int cn = tn[kMaxFoot], nn = tn[kMaxFoot + 1];
+                    const int lines = (nn * nt * 4 + 127) >> 7;
+                    if (nn > 0 && lane < lines) {
+                        const float* pp = y + ((size_t)(vb + j + NQ) * ns + cn) * nt + lane * 32;
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(pp));
+                    }
+                }
+#endif
                 Foot fa, fb;
                 load_foot(&tab[j], fa);
                 if (NQ == 2 && j + 1 < nb) load_foot(&tab[j + 1], fb); else fb.n = 0;

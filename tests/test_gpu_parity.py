@@ -510,18 +510,37 @@ def test_fbp_small(ct, O, name):
     assert rel_l2(I.to_oracle_image(xg), xo, f"fbp {name}") <= 1e-4
 
 
-def test_fbp_full_size_c2_and_helical_rejected(ct, O):
-    """c2 FBP of the synthetic scan vs the oracle (rel L2 <= 1e-4); helical -> CT_EUNSUPPORTED."""
+def test_fbp_full_size_c2_and_partial_orbit_rejected(ct, O):
+    """c2 FBP of the synthetic scan vs the oracle (rel L2 <= 1e-4); a circular orbit that is
+    not one full turn -> CT_EUNSUPPORTED."""
     cfg = I.config("c2")
     d = I.synthesize(cfg)
     geo = ct.Geometry(cfg.geom)
     xg = geo.fbp(d["y"].cuda()).cpu().numpy()
     xo = O.fbp(cfg.geom, I.to_oracle_sino(d["y"]))
     assert rel_l2(I.to_oracle_image(xg), xo, "fbp full-size c2") <= 1e-4
-    gh = geoms_small()["helical_c4"]
-    with pytest.raises(ct.CTError, match="EUNSUPPORTED|helical"):
-        ct.Geometry(gh).fbp(torch.zeros(ct.Geometry(gh).sino_shape(gh["na"]), device="cuda"))
+    half = GU.geom("cone_axial", nx=12, nz=6, dx=0.9766, dz=0.625, ns=24, ds=1.0239, nt=8, dt=1.0964, na=24, turns=0.5)
+    with pytest.raises(ct.CTError, match="EUNSUPPORTED"):
+        ct.Geometry(half).fbp(torch.zeros(ct.Geometry(half).sino_shape(24), device="cuda"))
 
+
+@pytest.mark.parametrize("name", ["helical_c4", "helical_c5", "c5_coarse"])
+def test_fbp_helical(ct, O, name):
+    """Helical FBP initial image (reading B-FBP-H: back-projection over the views that see the
+    voxel, normalised by their number) vs the oracle: small helical geometries on random data,
+    and the c5 scan (full detector and 6888 views) on a coarse 128^2 x 16 grid with its data."""
+    if name == "c5_coarse":
+        g = I.slab_geom(dict(I.config("c5").geom, nx=128, ny=128, dx=4 * 0.9766, dy=4 * 0.9766), 152, 168)
+        cfg = I.ScanConfig("c5", g, 24, 1, 1.0, 1.0, 26, 5e4, 0.0, "body3d", body_z=70.0)
+        y = I.synthesize(cfg, device="cuda", views_per_chunk=8)["y"]
+    else:
+        g = geoms_small()[name]
+        y = torch.rand((g["na"], g["ns"], g["nt"]), device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    geo = ct.Geometry(g)
+    xg = geo.fbp(y).cpu().numpy()
+    xo = O.fbp(g, I.to_oracle_sino(y.cpu()))
+    assert np.abs(xo).max() > 0
+    assert rel_l2(I.to_oracle_image(xg), xo, f"fbp helical {name}") <= 1e-4
 
 def test_oslalm_from_fbp_init(ct, O):
     """OS-LALM started from the FBP image matches the oracle started from its own FBP."""
