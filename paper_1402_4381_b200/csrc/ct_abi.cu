@@ -61,6 +61,9 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 #ifndef CT_FWD3D2_MINB
 #define CT_FWD3D2_MINB 5
 #endif
+#ifndef CT_FWD3D2_YSPLIT
+#define CT_FWD3D2_YSPLIT 0   // OS-LALM projections in two launches over image-row halves (L2 working set)
+#endif
 #ifndef CT_FWD3D2_TC_HEL
 #define CT_FWD3D2_TC_HEL 26   // helical scans; A/B (c4, c5): 26 (6 CTAs/SM) beats 22, 32, 40, 48
 #endif
@@ -446,23 +449,35 @@ static cudaError_t launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const 
 
 template <int TC, int NW, int H, bool RESID, int MINB>
 static cudaError_t launch_fwd3d2(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
-                                 const float* w, float scale, const int2* ext, cudaStream_t st) {
+                                 const float* w, float scale, const int2* ext, cudaStream_t st, float* part) {
     constexpr size_t smem = fwd3d2_smem<TC, NW>();
-    cudaError_t e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, RESID, MINB>, smem);
+    cudaError_t e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, false, MINB>, smem);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, RESID, MINB>, smem);
     if (e != cudaSuccess) return e;
     dim3 grid((dg.ns + TC - 1) / TC, v.count);
-    fwd3d2_kernel<TC, NW, H, RESID, MINB><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale, ext);
+    if (part) {   // y-split: rows [0, ny/2) into `part`, then rows [ny/2, ny) + part through the epilogue
+        const int yh = dg.ny / 2;
+        fwd3d2_kernel<TC, NW, H, false, MINB><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, part, nullptr,
+                                                                          nullptr, 1.0f, ext, 0, yh, nullptr);
+        fwd3d2_kernel<TC, NW, H, RESID, MINB><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale,
+                                                                          ext, yh, dg.ny, part);
+        g_launches += 1;
+    } else {
+        fwd3d2_kernel<TC, NW, H, RESID, MINB><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale,
+                                                                          ext, 0, dg.ny, nullptr);
+    }
     return cudaSuccess;
 }
 
 // Pair-row forward (nt <= 64): tile width and resident CTAs per SM by scan kind (A/B, c3-c5)
 template <int H, bool RESID>
 static cudaError_t launch_fwd3d2_sel(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
-                                     const float* w, float scale, const int2* ext, cudaStream_t st) {
+                                     const float* w, float scale, const int2* ext, cudaStream_t st, float* part) {
     if (dg.kind == CT_CONE_HELICAL)
         return launch_fwd3d2<CT_FWD3D2_TC_HEL, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB_HEL>(dg, v, x, out, yobs, w, scale,
-                                                                                        ext, st);
-    return launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB>(dg, v, x, out, yobs, w, scale, ext, st);
+                                                                                        ext, st, part);
+    return launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB>(dg, v, x, out, yobs, w, scale, ext, st,
+                                                                                part);
 }
 
 // Per-call forward-projection scratch (owned by the caller of launch_fwd, so concurrent
@@ -472,6 +487,7 @@ static cudaError_t launch_fwd3d2_sel(const DevGeom& dg, ct_views v, const float*
 struct FwdScratch {
     unsigned long long* acc2d;
     int2* ext;
+    float* part = nullptr;   // cone, nt <= 64: first half's sums of the y-split forward (nullptr: no split)
 };
 
 template <bool RESID>
@@ -515,11 +531,11 @@ static int launch_fwd(const ct_geom* g, ct_views v, const float* x, float* out, 
         }
         dim3 grid((dg.ns + TC - 1) / TC, v.count);
         if (dg.nt <= 32 && CT_FWD3D_PAIR)
-            CT_CUDA((launch_fwd3d2_sel<2, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st)));
+            CT_CUDA((launch_fwd3d2_sel<2, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st, fs.part)));
         else if (dg.nt <= 32)
             CT_CUDA((launch_fwd3d<TC, 32, RESID>(dg, grid, v, x, out, yobs, w, scale, fs.ext, st)));
         else if (dg.nt <= 64 && CT_FWD3D_PAIR)
-            CT_CUDA((launch_fwd3d2_sel<1, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st)));
+            CT_CUDA((launch_fwd3d2_sel<1, RESID>(dg, v, x, out, yobs, w, scale, fs.ext, st, fs.part)));
         else if (dg.nt <= 64)
             CT_CUDA((launch_fwd3d<TC, 64, RESID>(dg, grid, v, x, out, yobs, w, scale, fs.ext, st)));
         else
@@ -944,7 +960,13 @@ static bool use_band(const ct_geom* g, const ct_oslalm_cfg* c) {
     return iy1 > iy0;
 }
 
-static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16], size_t* total) {
+// y-split forward (two launches over image-row halves) for the OS-LALM state's
+// projections of cone scans with nt <= 64 (the pair-row kernel)
+static bool use_ysplit(const ct_geom* g) {
+    return CT_FWD3D2_YSPLIT && g->d.kind != CT_FAN2D && g->d.nt <= 64 && CT_FWD3D_PAIR && g->d.ny >= 2;
+}
+
+static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[20], size_t* total) {
     int iy0, iy1;
     size_t S;
     slab_geometry(g, g->nranks, g->rank, &iy0, &iy1, &S);
@@ -974,13 +996,14 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[16
     // whole subsets too; cone column extents)
     off[14] = o; o += fwd_scratch_bytes(g, maxcount);
     off[15] = o; o += use_band(g, c) ? 4 * align256(N * 4) : 0;   // band exchange buffers
+    off[16] = o; o += use_ysplit(g) ? align256(sino * 4) : 0;         // y-split forward partial sums
     *total = o;
 }
 
 extern "C" int ct_oslalm_state_bytes(const ct_geom* g, const ct_oslalm_cfg* c, size_t* out) {
     if (!g || !out) return fail(CT_EINVAL, "ct_oslalm_state_bytes: null argument");
     if (int e = check_cfg(g, c)) return e;
-    size_t off[16];
+    size_t off[20];
     state_layout(g, c, off, out);
     return CT_OK;
 }
@@ -989,7 +1012,7 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
                                       ct_oslalm_state** out) {
     if (!g || !ws || !out) return fail(CT_EINVAL, "ct_oslalm_state_create: null argument");
     if (int e = check_cfg(g, c)) return e;
-    size_t off[16], total;
+    size_t off[20], total;
     state_layout(g, c, off, &total);
     if (bytes < total) return fail(CT_ENOMEM, "workspace of %zu bytes < required %zu", bytes, total);
     if ((uintptr_t)ws & 255) return fail(CT_EINVAL, "workspace must be 256-byte aligned");
@@ -1027,6 +1050,7 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
     }
     s->xi_ex = (double*)(b + off[11]);
     s->fs = fwd_scratch_at(g, b + off[14]);
+    if (use_ysplit(g)) s->fs.part = (float*)(b + off[16]);
     s->band = use_band(g, c) ? 1 : 0;
     if (s->band)
         for (int i = 0; i < 4; i++) s->bbuf[i] = (float*)(b + off[15] + i * align256(s->Npad * 4));

@@ -429,11 +429,15 @@ __device__ __forceinline__ void acc_pair(float2* p, const Foot& f0, float2 A0, c
 }
 
 template <int TC, int NW, int H, bool RESID, int MINB>
+// [ya, yb): the image rows (iy) this launch projects (the y-split forward projects the two
+// halves in two launches so that each launch's working set of x is half a view's slice
+// window; `addend` (nullable) holds the first half's sums, added before the epilogue).
 __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int first, int stride,
                                                                      const float* __restrict__ x, float* __restrict__ out,
                                                                      const float* __restrict__ yobs,
                                                                      const float* __restrict__ wts, float scale,
-                                                                     const int2* __restrict__ ext) {
+                                                                     const int2* __restrict__ ext, int ya, int yb,
+                                                                     const float* __restrict__ addend) {
     constexpr int TCP = fwd3d2_tcp<TC>(), CB = fwd3d2_base();
     constexpr int LW = 32 / H;   // lanes per column (row pairs)
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -453,13 +457,18 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
     for (int c = 0; c < TCP; c++) Pg[c * LW] = make_float2(0.0f, 0.0f);
     const Wedge w = make_wedge(g, vw.x, vw.y, c0, TC);
     const int nz = g.nz;
-    for (int L = gi; L < w.nlines; L += NW) {
+    // lines: image rows [ya, yb), or every image column trimmed to rows [ya, yb)
+    for (int L = (w.rows ? ya : 0) + gi; L < (w.rows ? yb : w.nlines); L += NW) {
         int lo, hi;
         wedge_line(g, w, L, lo, hi);
         if (ext) {
             const int2 e = __ldg(&ext[w.rows ? L : g.ny + L]);
             lo = max(lo, e.x);
             hi = min(hi, e.y);
+        }
+        if (!w.rows) {
+            lo = max(lo, ya);
+            hi = min(hi, yb - 1);
         }
         if (lo > hi) continue;
         const int n_in = hi - lo + 1;
@@ -549,6 +558,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
 #pragma unroll
         for (int q = 0; q < NW * H; q++) s += Pf[(q * TCP + c + CB) * RW + rr];
         const size_t oi = ((size_t)k * g.ns + c0 + c) * g.nt + rr;
+        if (addend) s += addend[oi];
         if (RESID) {
             const size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
             const float yo = yobs ? __ldg(&yobs[gidx]) : 0.0f;

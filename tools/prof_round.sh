@@ -10,7 +10,7 @@ for c in c2 c3 c4; do python bench.py --config $c --steps 5 --warmup 3 --no-e2e 
 # launch list of bench steps (cold, serialised: compare shares): 2 timed steps of c5
 B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 $B > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_c5.csv $B > gpurun_out/ncu_launch.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ct::|fwd3d|back3d|sqs_update|extent|xi_|mask_|init_scalars|zero_offmask|count_vv|l2_read" -c 5000 --csv --log-file gpurun_out/launches_c5.csv $B > gpurun_out/ncu_launch.log 2>&1
 python tools/launch_summary.py gpurun_out/launches_c5.csv > gpurun_out/launches_c5_summary.txt
 # one full capture of each c5 step kernel inside an OS-LALM iteration + DRAM traffic
 python tools/prof_iter.py c5 2 > gpurun_out/prof_iter.log 2>&1 && \
