@@ -62,7 +62,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 #define CT_FWD3D2_MINB 5
 #endif
 #ifndef CT_FWD3D2_YSPLIT
-#define CT_FWD3D2_YSPLIT 0   // OS-LALM projections in two launches over image-row halves (L2 working set)
+#define CT_FWD3D2_YSPLIT 0   // 1: OS-LALM projections in two launches over image-row halves (L2 working set; A/B: c5 11.44 -> 11.68, c4 3.34 -> 3.74 ms, off)
 #endif
 #ifndef CT_FWD3D2_TC_HEL
 #define CT_FWD3D2_TC_HEL 26   // helical scans; A/B (c4, c5): 26 (6 CTAs/SM) beats 22, 32, 40, 48

@@ -764,7 +764,7 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 #define CT_BACK3D_PAIR 0   // 1: two views per slice walk (one accumulator update per slice for both); A/B: slower (64 registers, 4 CTAs/SM: c5 11.25 -> 12.38 ms)
 #endif
 #ifndef CT_BACK3D_PREFETCH
-#define CT_BACK3D_PREFETCH 1   // L1 prefetch of the next view's detector rows
+#define CT_BACK3D_PREFETCH 0   // 1: L1 prefetch of the next view's detector rows (A/B: c5 11.32 -> 13.08 ms, off)
 #endif
 #ifndef CT_BACK3D_MINB
 // one view per walk: 5 CTAs/SM (A/B c3, c5: beats 4 by 2-3 %; 3 is 12 % slower); two views per
