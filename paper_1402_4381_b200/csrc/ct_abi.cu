@@ -65,10 +65,13 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 #define CT_FWD3D2_YSPLIT 0   // 1: OS-LALM projections in two launches over image-row halves (L2 working set; A/B: c5 11.44 -> 11.68, c4 3.34 -> 3.74 ms, off)
 #endif
 #ifndef CT_FWD3D2_TC_HEL
-#define CT_FWD3D2_TC_HEL 26   // helical scans; A/B (c4, c5): 26 (6 CTAs/SM) beats 22, 32, 40, 48
+#define CT_FWD3D2_TC_HEL 26   // helical scans; A/B (c4, c5): 26 (24 warps/SM) beats 22, 32, 40, 48
+#endif
+#ifndef CT_FWD3D2_NW_HEL
+#define CT_FWD3D2_NW_HEL 8    // 3 CTAs of 8 warps (A/B: c5 11.42 -> 11.29, c4 3.35 -> 3.18 ms vs 6 of 4; 12 of 2: slower)
 #endif
 #ifndef CT_FWD3D2_MINB_HEL
-#define CT_FWD3D2_MINB_HEL 6
+#define CT_FWD3D2_MINB_HEL 3
 #endif
 #ifndef CT_FWD3D2_NW
 #define CT_FWD3D2_NW 4    // warps (row groups) per CTA (8: c3 -1 %, c5 +12 %)
@@ -474,8 +477,8 @@ template <int H, bool RESID>
 static cudaError_t launch_fwd3d2_sel(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
                                      const float* w, float scale, const int2* ext, cudaStream_t st, float* part) {
     if (dg.kind == CT_CONE_HELICAL)
-        return launch_fwd3d2<CT_FWD3D2_TC_HEL, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB_HEL>(dg, v, x, out, yobs, w, scale,
-                                                                                        ext, st, part);
+        return launch_fwd3d2<CT_FWD3D2_TC_HEL, CT_FWD3D2_NW_HEL, H, RESID, CT_FWD3D2_MINB_HEL>(dg, v, x, out, yobs, w,
+                                                                                            scale, ext, st, part);
     return launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB>(dg, v, x, out, yobs, w, scale, ext, st,
                                                                                 part);
 }

@@ -920,7 +920,38 @@ struct SliceWalk {
         const float tz = fmaf(zi, dz_rho, hdz);
         return sqrt_approx(fmaf(tz, tz, 1.0f)) * (up - pf);
     }
+    // PF at the slice edge zi (clamped to the view's rows)
+    __device__ __forceinline__ float pf_at(float zi) const {
+        const float u = fminf(fmaxf(fmaf(zi, inv_kz, ubl), 0.0f), fnr);
+        const int k = __float2int_rd(u);
+        const float2 qp = QP[k];
+        return fmaf(u - (float)k, qp.y, qp.x);
+    }
+    // Blocked walk, one pass: lane l takes the S consecutive slices S l .. S l + S - 1 of the walk
+    // (edges S l .. S l + S, the last from lane l + 1's first edge), i.e. 32 S - 1 slices with
+    // one shuffle per lane instead of S passes of 31 (the per-pass work: loop, shuffle, edge
+    // bookkeeping is paid once).  Lane 31's last slice has no upper edge: it adds 0.  acc0 =
+    // accumulator of the walk's first slice.
+    template <int S>
+    __device__ __forceinline__ void walk_blocked(float* acc0, int lane) const {
+        const float zb = zl - (float)lane + (float)(S * lane);   // this lane's first edge
+        float pf[S];
+#pragma unroll
+        for (int e = 0; e < S; e++) pf[e] = pf_at(zb + (float)e);
+        const float up = __shfl_down_sync(0xffffffffu, pf[0], 1);
+        float* a = acc0 + S * lane;
+#pragma unroll
+        for (int e = 0; e < S; e++) {
+            const float hi = e + 1 < S ? pf[e + 1] : (lane < 31 ? up : pf[e]);
+            const float tz = fmaf(zb + (float)e, dz_rho, hdz);
+            a[e] = fmaf(sqrt_approx(fmaf(tz, tz, 1.0f)), hi - pf[e], a[e]);
+        }
+    }
 };
+
+#ifndef CT_BACK3D_BLOCKED
+#define CT_BACK3D_BLOCKED 1   // one blocked pass (S = 2..4 slices per lane) for windows of 32..127 slices
+#endif
 
 // NTM: detector-row specialisation, 64 or 32 (every row in one pass, nt a compile-time
 // constant) or 0 (general nt: the rows the active slices meet).
@@ -1029,8 +1060,15 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                     }
                 } else {
                     const SliceWalk& w1 = va ? wa : wb;
+                    // one blocked pass covers 32 S - 1 slices (tail lanes clamp to 0 or land in the
+                    // padding: z0 + 32 S - 1 <= nz + kBackPad - 1 since nzs >= 32 (S - 1))
+                    if (CT_BACK3D_BLOCKED && nzs > 31 && nzs <= 63) w1.walk_blocked<2>(acc + z0, lane);
+                    else if (CT_BACK3D_BLOCKED && nzs > 63 && nzs <= 95) w1.walk_blocked<3>(acc + z0, lane);
+                    else if (CT_BACK3D_BLOCKED && nzs > 95 && nzs <= 127) w1.walk_blocked<4>(acc + z0, lane);
+                    else {
 #pragma unroll 1   // (A/B: the compiler's unrolled version needs more registers, -5 %)
-                    for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) accl[s0] += w1.contrib(sf);
+                        for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) accl[s0] += w1.contrib(sf);
+                    }
                 }
                 __syncwarp();
             }
