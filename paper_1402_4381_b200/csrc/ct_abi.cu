@@ -821,7 +821,9 @@ struct GraphEntry {
     const void* key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int curG = -1;
     size_t nodes = 0;
+    unsigned long long used = 0;   // replay counter value of the last use (LRU replacement)
 };
+constexpr int kGraphCache = 4;   // (buffers, G parity) combinations kept instantiated
 
 struct ct_oslalm_state {
     const ct_geom* g;
@@ -862,7 +864,8 @@ struct ct_oslalm_state {
     int log_slot = -1;
     cudaStream_t cap = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-    GraphEntry graphs[2];
+    GraphEntry graphs[kGraphCache];
+    unsigned long long replays = 0;
     // diagnostic per-kernel timing
     int timing = 0;
     std::vector<cudaEvent_t> evpool;
@@ -1591,7 +1594,13 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
         if (e.exec && e.curG == s->curG && memcmp(e.key, key, sizeof(key)) == 0) ge = &e;
     int startG = s->curG;
     if (!ge) {
-        ge = s->graphs[0].exec == nullptr || s->graphs[0].curG == s->curG ? &s->graphs[0] : &s->graphs[1];
+        // an empty slot, else the least recently used one (a caller alternating data buffers,
+        // e.g. double-buffered inputs, keeps one instantiated graph per buffer set)
+        ge = &s->graphs[0];
+        for (auto& e : s->graphs) {
+            if (!e.exec) { ge = &e; break; }
+            if (e.used < ge->used) ge = &e;
+        }
         if (ge->exec) { cudaGraphExecDestroy(ge->exec); ge->exec = nullptr; }
         cudaGraph_t graph;
         CT_CUDA(cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal));
@@ -1621,6 +1630,7 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
     }
     CT_CUDA(cudaEventRecord(s->ev_in, st));
     CT_CUDA(cudaStreamWaitEvent(s->cap, s->ev_in, 0));
+    ge->used = ++s->replays;
     CT_CUDA(cudaGraphLaunch(ge->exec, s->cap));
     CT_CUDA(cudaEventRecord(s->ev_out, s->cap));
     CT_CUDA(cudaStreamWaitEvent(st, s->ev_out, 0));

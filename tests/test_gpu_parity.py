@@ -528,9 +528,9 @@ def test_fbp_full_size_c2_and_partial_orbit_rejected(ct, O):
 def test_fbp_helical(ct, O, name):
     """Helical FBP initial image (reading B-FBP-H: back-projection over the views that see the
     voxel, normalised by their number) vs the oracle: small helical geometries on random data,
-    and the c5 scan (full detector and 6888 views) on a coarse 128^2 x 16 grid with its data."""
+    and the c5 scan (full detector and 6888 views) on the central 128^2 x 16 voxels with its data."""
     if name == "c5_coarse":
-        g = I.slab_geom(dict(I.config("c5").geom, nx=128, ny=128, dx=4 * 0.9766, dy=4 * 0.9766), 152, 168)
+        g = I.slab_geom(dict(I.config("c5").geom, nx=128, ny=128), 152, 168)   # central 125 mm x 10 mm
         cfg = I.ScanConfig("c5", g, 24, 1, 1.0, 1.0, 26, 5e4, 0.0, "body3d", body_z=70.0)
         y = I.synthesize(cfg, device="cuda", views_per_chunk=8)["y"]
     else:
