@@ -327,6 +327,9 @@ constexpr size_t fwd3d_smem() {
 #ifndef CT_FWD3D2_UNPRED
 #define CT_FWD3D2_UNPRED 0
 #endif
+#ifndef CT_FWD3D2_INTERIOR
+#define CT_FWD3D2_INTERIOR 1   // interior columns (every touched slice inside the volume) skip the volume predicates
+#endif
 #ifndef CT_FWD3D2_KS
 #define CT_FWD3D2_KS 1     // per-column slice-window specialisation (3 / 4 / 5 slices per row pair)
 #endif
@@ -338,9 +341,11 @@ constexpr size_t fwd3d_smem() {
 // lo in [z0, z0 + 1), i.e. slices z0 .. z0 + KS - 1 when 1 + 2 kz <= KS (KS = 3: kz <= 1,
 // KS = 4: kz <= 1.5, KS = 5: kz < 2); chosen per column (warp-uniform), so near-source
 // columns (small kz) do not pay for the far side's longer windows.
-template <int KS>
+// INTERIOR: every slice the column's row pairs can touch lies inside the volume (flagged in
+// the table by a negative kz), so only the slices past hi need a predicate.
+template <int KS, bool INTERIOR>
 __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __restrict__ x, int l, int nz) {
-    const float kz = f.ax.kz;
+    const float kz = fabsf(f.ax.kz);
     const float lo = fmaf((float)(2 * l), kz, f.ax.qf);
     const float mid = lo + kz, hi = mid + kz;
     const int i0 = __float2int_rd(lo);
@@ -353,7 +358,7 @@ __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __r
     for (int m = 0; m < KS; m++) {
         const float tz = fmaf((float)m, f.ax.dz_rho, tz0);
         // slices past hi get weight 0 below; skipping their loads saves L1 traffic (CT_FWD3D2_UNPRED = 1: load them)
-        const bool in = (unsigned)(iz0 + m) < (unsigned)nz && (CT_FWD3D2_UNPRED || m < 2 || z0 + (float)m < hi);
+        const bool in = (INTERIOR || (unsigned)(iz0 + m) < (unsigned)nz) && (CT_FWD3D2_UNPRED || m < 2 || z0 + (float)m < hi);
         const float v = in ? __ldg(xp + m) : 0.0f;
         xl[m] = v * sqrt_approx(fmaf(tz, tz, 1.0f));
     }
@@ -490,6 +495,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                 f.ax.qf = qf - 0.5f * f.ax.kz - g.rbase * f.ax.kz;
                 f.ax.inv_kz = (0.5f - qf) * f.ax.dz_rho;   // tzc
                 f.rows = (iy * g.nx + ix) * nz + f.ax.qi;
+                // interior column: the slices of every lane's row pair (up to 5 past floor(lo)) lie
+                // in the volume -> flagged by a negative kz (its uses take |kz|)
+                if (CT_FWD3D2_INTERIOR && f.ax.kz < 2.0f) {
+                    const int zlo = f.ax.qi + __float2int_rd(f.ax.qf);
+                    const int zhi = f.ax.qi + __float2int_rd(fmaf((float)(2 * (LW - 1)), f.ax.kz, f.ax.qf)) + 4;
+                    if (zlo >= 0 && zhi <= nz - 1) f.ax.kz = -f.ax.kz;
+                }
                 tab[lane] = f;
             }
             __syncwarp();
@@ -501,28 +513,37 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                 if (j + 1 < nq) load_foot(&tab[j + 1], f1); else f1.n = 0;
                 if (f0.n <= 0 && f1.n <= 0) continue;
                 float2 A0 = make_float2(0.0f, 0.0f), A1 = A0;
-                const float kzm = fmaxf(f0.n > 0 ? f0.ax.kz : 0.0f, f1.n > 0 ? f1.ax.kz : 0.0f);
+                const float kz0 = fabsf(f0.ax.kz), kz1 = fabsf(f1.ax.kz);
+                const float kzm = fmaxf(f0.n > 0 ? kz0 : 0.0f, f1.n > 0 ? kz1 : 0.0f);
+                // interior pair (or a single interior column): no volume predicates
+                const bool inter = (f0.n <= 0 || f0.ax.kz < 0.0f) && (f1.n <= 0 || f1.ax.kz < 0.0f);
+#define CT_FWD3D2_AXIAL(KS_)                                                                   \
+    if (inter) {                                                                               \
+        if (f0.n > 0) A0 = fwd_axial_pair<KS_, true>(f0, x, ll, nz);                           \
+        if (f1.n > 0) A1 = fwd_axial_pair<KS_, true>(f1, x, ll, nz);                           \
+    } else {                                                                                   \
+        if (f0.n > 0) A0 = fwd_axial_pair<KS_, false>(f0, x, ll, nz);                          \
+        if (f1.n > 0) A1 = fwd_axial_pair<KS_, false>(f1, x, ll, nz);                          \
+    }
                 if (CT_FWD3D2_KS && kzm <= 0.999f) {
-                    if (f0.n > 0) A0 = fwd_axial_pair<3>(f0, x, ll, nz);
-                    if (f1.n > 0) A1 = fwd_axial_pair<3>(f1, x, ll, nz);
+                    CT_FWD3D2_AXIAL(3)
                 } else if (CT_FWD3D2_KS && kzm <= 1.499f) {
-                    if (f0.n > 0) A0 = fwd_axial_pair<4>(f0, x, ll, nz);
-                    if (f1.n > 0) A1 = fwd_axial_pair<4>(f1, x, ll, nz);
+                    CT_FWD3D2_AXIAL(4)
                 } else if (kzm < 2.0f) {
-                    if (f0.n > 0) A0 = fwd_axial_pair<5>(f0, x, ll, nz);
-                    if (f1.n > 0) A1 = fwd_axial_pair<5>(f1, x, ll, nz);
+                    CT_FWD3D2_AXIAL(5)
                 } else {
                     if (f0.n > 0) {
-                        const float l0 = fmaf((float)(2 * ll), f0.ax.kz, f0.ax.qf);
-                        A0 = make_float2(fwd_axial_row(f0, x, l0, l0 + f0.ax.kz, nz),
-                                         fwd_axial_row(f0, x, l0 + f0.ax.kz, l0 + 2.0f * f0.ax.kz, nz));
+                        const float l0 = fmaf((float)(2 * ll), kz0, f0.ax.qf);
+                        A0 = make_float2(fwd_axial_row(f0, x, l0, l0 + kz0, nz),
+                                         fwd_axial_row(f0, x, l0 + kz0, l0 + 2.0f * kz0, nz));
                     }
                     if (f1.n > 0) {
-                        const float l1 = fmaf((float)(2 * ll), f1.ax.kz, f1.ax.qf);
-                        A1 = make_float2(fwd_axial_row(f1, x, l1, l1 + f1.ax.kz, nz),
-                                         fwd_axial_row(f1, x, l1 + f1.ax.kz, l1 + 2.0f * f1.ax.kz, nz));
+                        const float l1 = fmaf((float)(2 * ll), kz1, f1.ax.qf);
+                        A1 = make_float2(fwd_axial_row(f1, x, l1, l1 + kz1, nz),
+                                         fwd_axial_row(f1, x, l1 + kz1, l1 + 2.0f * kz1, nz));
                     }
                 }
+#undef CT_FWD3D2_AXIAL
                 const int dd = f1.cA - f0.cA;
                 if (H == 2 && f0.n > 0 && f1.n > 0 && dd >= -3 && dd <= 3) {
                     // adjacent columns' footprints overlap: one read-modify-write per channel of
