@@ -1,5 +1,7 @@
 """Long GPU-vs-oracle OS-LALM comparisons at full size (builder-run evidence, too slow for the
--m gpu suite): python tools/parity_long.py c3 20 [out.json]
+-m gpu suite): python tools/parity_long.py c3 20 [out.json] [nz_keep]
+nz_keep: keep only the central nz_keep slices of the volume (full planes, detector and views;
+the helical configs' oracle cost at full size is hours).
 Writes the RMS / max difference over S (HU), the restart decisions and the rho trajectory
 agreement after every iteration."""
 import json
@@ -19,7 +21,12 @@ from paper_1402_4381_b200 import inputs as I  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 n_iter = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 out = sys.argv[3] if len(sys.argv) > 3 else f"gpurun_out/parity_long_{name}.json"
+nz_keep = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 cfg = I.config(name)
+if nz_keep:
+    z0 = (cfg.geom["nz"] - nz_keep) // 2
+    cfg = I.ScanConfig(cfg.name, I.slab_geom(cfg.geom, z0, z0 + nz_keep), cfg.M, cfg.n_iter, cfg.beta, cfg.delta,
+                       cfg.nbr, cfg.I0, cfg.sigma, cfg.recipe, cfg.body_z, dict(cfg.extra))
 g = cfg.geom
 d = I.synthesize(cfg, device="cuda", views_per_chunk=8 if not cfg.is2d else 128)
 m0 = I.support_mask(cfg, device="cuda")
@@ -44,7 +51,7 @@ t_or = time.time() - t0
 log = np.array(logs)
 Sm = So > 0
 xg = xs[-1]
-res = {"config": name, "iters": n_iter, "M": cfg.M,
+res = {"config": name, "nz_keep": nz_keep or cfg.geom.get("nz", 1), "iters": n_iter, "M": cfg.M,
        "rms_HU": math.sqrt(((xg - xo)[Sm] ** 2).mean()) / I.HU,
        "max_abs_HU": float(np.abs(xg - xo)[Sm].max() / I.HU),
        "image_rms_HU": math.sqrt((xo[Sm] ** 2).mean()) / I.HU,
