@@ -343,7 +343,9 @@ int ct_comm_get_unique_id(void* nccl_uid_out128);
  *                     block +- the cone's z reach), and its next forward projection reads x only
  *                     there: only those z-band blocks are exchanged (grouped send / receive, a
  *                     fixed rank-order sum), plus one boundary row each way for the stencil and
- *                     one full all-gather per outer iteration;
+ *                     one full all-gather per outer iteration.  The partial back-projection runs
+ *                     one destination row slab at a time and each slab's blocks are sent on an
+ *                     internal communication stream while the next slab is computed;
  *   CT_EXCHANGE_AUTO  BAND for helical scans with 2..16 ranks each owning >= 1 image row, else FULL
  *                     (the default).
  * Call before creating OS-LALM states.  CT_EINVAL for an unknown mode, CT_EUNSUPPORTED for BAND

@@ -61,6 +61,9 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 #ifndef CT_FWD3D2_MINB
 #define CT_FWD3D2_MINB 5
 #endif
+#ifndef CT_BAND_OVERLAP
+#define CT_BAND_OVERLAP 1   // band exchange: send each destination slab's blocks while the next slab is back-projected
+#endif
 #ifndef CT_FWD3D2_YSPLIT
 #define CT_FWD3D2_YSPLIT 0   // 1: OS-LALM projections in two launches over image-row halves (L2 working set; A/B: c5 11.44 -> 11.68, c4 3.34 -> 3.74 ms, off)
 #endif
@@ -564,11 +567,15 @@ static size_t back_nblocks(const ct_geom* g) {
     return (size_t)gr.x * gr.y * gr.z;
 }
 
+// rows [row0, row1) of the image (cone beam; row1 < 0: every row)
 template <int EPI>
-static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, const GupdArgs& ga, cudaStream_t st) {
+static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, const GupdArgs& ga, cudaStream_t st,
+                       int row0 = 0, int row1 = -1) {
     const DevGeom& dg = g->dg;
     dim3 grid;
     back_grid(g, grid);
+    if (row1 < 0) row1 = dg.ny;
+    if (dg.kind != CT_FAN2D) grid.y = (unsigned)std::max(1, (row1 - row0 + 1) / 2);
     if (dg.kind == CT_FAN2D)
         if (dg.vrel)
             CT_CUDA(launch_pdl(back2d_kernel<EPI, true>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
@@ -578,13 +585,13 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
         const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * ((size_t)dg.nz + kBackPad);
         if (dg.nt == 64) {
             CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 64>, smem));
-            back3d_kernel<EPI, 64><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+            back3d_kernel<EPI, 64><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga, row0, row1);
         } else if (dg.nt == 32) {
             CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 32>, smem));
-            back3d_kernel<EPI, 32><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+            back3d_kernel<EPI, 32><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga, row0, row1);
         } else {
             CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 0>, smem));
-            back3d_kernel<EPI, 0><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga);
+            back3d_kernel<EPI, 0><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga, row0, row1);
         }
     }
     CT_LAUNCHED(1);
@@ -843,6 +850,9 @@ struct ct_oslalm_state {
     size_t S = 0, off0 = 0, Npad = 0;
     float* xp[2] = {nullptr, nullptr};   // full images (all-gathered), ping-pong
     int band = 0;                        // band-limited exchange (helical row slabs)
+    cudaStream_t cs = nullptr;           // band exchange: communication stream (overlaps the back-projection)
+    cudaEvent_t ev_slab[kMaxBandRanks] = {};
+    cudaEvent_t ev_cs = nullptr;
     float* bbuf[4] = {nullptr, nullptr, nullptr, nullptr};   // reduce send / recv, gather send / recv
     double* xi_ex = nullptr;             // [0] this rank's xi, [1] all-reduced xi, [2..3] BB sums
     float* xprev = nullptr;              // BB: xbar of the previous outer iteration
@@ -1079,6 +1089,11 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
     cudaError_t e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming);
+    if (e == cudaSuccess && s->band) {
+        e = cudaStreamCreateWithFlags(&s->cs, cudaStreamNonBlocking);
+        for (int q = 0; q < s->P && e == cudaSuccess; q++) e = cudaEventCreateWithFlags(&s->ev_slab[q], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_cs, cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) {
         delete s;
         return fail(CT_ECUDA, "state streams: %s", cudaGetErrorString(e));
@@ -1094,6 +1109,10 @@ extern "C" void ct_oslalm_state_destroy(ct_oslalm_state* s) {
         if (ge.exec) cudaGraphExecDestroy(ge.exec);
     for (auto e : s->evpool) cudaEventDestroy(e);
     if (s->cap) cudaStreamDestroy(s->cap);
+    if (s->cs) cudaStreamDestroy(s->cs);
+    for (auto e : s->ev_slab)
+        if (e) cudaEventDestroy(e);
+    if (s->ev_cs) cudaEventDestroy(s->ev_cs);
     if (s->ev_in) cudaEventDestroy(s->ev_in);
     if (s->ev_out) cudaEventDestroy(s->ev_out);
     delete s;
@@ -1262,6 +1281,63 @@ static int band_reduce(ct_oslalm_state* s, int m, const float* Gpart, float* Gne
     return CT_OK;
 }
 
+// Overlapped form of launch_back + band_reduce: the partial back-projection runs one destination
+// row slab at a time (slab order 0..P-1 on every rank); after slab t is done, this rank's band
+// block of it is packed and sent to rank t on the communication stream while slab t + 1 is
+// back-projected (each step t is a grouped exchange in which rank t receives from every other
+// rank).  The sum in rank order then follows on the compute stream.
+static int band_back_reduce(ct_oslalm_state* s, int m, ct_views v, const float* sino, const GupdArgs& ga, float* Gpart,
+                            float* Gnew, cudaStream_t st) {
+    const ct_geom* g = s->g;
+    const int P = s->P, p = s->prank, nx = g->d.nx, nz = g->d.nz;
+    int b0[kMaxBandRanks], b1[kMaxBandRanks], ry[kMaxBandRanks], rn[kMaxBandRanks];
+    for (int q = 0; q < P; q++) {
+        rank_band(g, s->cfg.M, m, q, &b0[q], &b1[q]);
+        rank_rows(g, q, &ry[q], &rn[q]);
+    }
+    const int bl = b1[p] - b0[p];
+    float* rslot[kMaxBandRanks];
+    BandSet bs{};
+    bs.P = P;
+    size_t ro = 0, so = 0;
+    for (int q = 0; q < P; q++) {
+        rslot[q] = s->bbuf[1] + ro;
+        bs.buf[q] = rslot[q];
+        bs.b0[q] = b0[q];
+        bs.b1[q] = b1[q];
+        ro += (size_t)rn[p] * nx * (b1[q] - b0[q]);
+    }
+    CT_CUDA(cudaEventRecord(s->ev_cs, st));
+    CT_CUDA(cudaStreamWaitEvent(s->cs, s->ev_cs, 0));   // the communication stream follows st's prior work
+    for (int t = 0; t < P; t++) {
+        if (int e = launch_back<EPI_STORE>(g, v, sino, Gpart, ga, st, ry[t], ry[t] + rn[t])) return e;
+        CT_CUDA(cudaEventRecord(s->ev_slab[t], st));
+        CT_CUDA(cudaStreamWaitEvent(s->cs, s->ev_slab[t], 0));
+        const size_t n = (size_t)rn[t] * nx * bl;
+        float* dst = t == p ? rslot[p] : s->bbuf[0] + so;
+        if (n) {
+            band_pack_kernel<<<band_grid(n), 256, 0, s->cs>>>(Gpart, dst, ry[t], rn[t], nx, nz, b0[p], bl);
+            CT_LAUNCHED(1);
+        }
+        const float* sptr[kMaxBandRanks];
+        float* rptr[kMaxBandRanks];
+        size_t sc[kMaxBandRanks], rc[kMaxBandRanks];
+        for (int q = 0; q < P; q++) {
+            sptr[q] = dst;
+            sc[q] = (q == t && p != t) ? n : 0;            // my block of slab t -> rank t
+            rptr[q] = rslot[q];
+            rc[q] = (p == t && q != t) ? (size_t)rn[p] * nx * (b1[q] - b0[q]) : 0;   // rank t: every block of its slab
+        }
+        if (int e = comm_rc(g, g->comm->alltoallv(sptr, sc, rptr, rc, s->cs))) return e;
+        if (t != p) so += n;
+    }
+    CT_CUDA(cudaEventRecord(s->ev_cs, s->cs));
+    CT_CUDA(cudaStreamWaitEvent(st, s->ev_cs, 0));
+    band_sum_kernel<<<band_grid((size_t)rn[p] * nx * nz), 256, 0, st>>>(Gnew, ry[p], rn[p], nx, nz, bs);
+    CT_LAUNCHED(1);
+    return CT_OK;
+}
+
 // After the K3 update of this rank's rows of xb: the neighbours' boundary rows (every slice;
 // the next update's stencil) and every other rank's rows inside this rank's band of subset m
 // (its next forward projection) -- replaces the all-gather.
@@ -1375,12 +1451,16 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
         // the ranks' xi (8 bytes), K4 on every rank
         float* Gnew = s->Gbuf[epi == EPI_INIT ? s->curG : s->curG ^ 1];
         int t1 = tmark(s, st);
-        if (int e = launch_back<EPI_STORE>(g, v, s->sino, s->Gtmp, ga, st)) return e;
+        if (s->band && CT_BAND_OVERLAP) {   // per-slab back-projection, blocks sent as each slab completes
+            if (int e = band_back_reduce(s, m, v, s->sino, ga, s->Gtmp, Gnew, st)) return e;
+        } else if (int e = launch_back<EPI_STORE>(g, v, s->sino, s->Gtmp, ga, st)) {
+            return e;
+        }
         tmark_end(s, st, 2, t1);
         int t2 = tmark(s, st);
-        if (s->band) {   // helical: z-band blocks instead of the full reduce-scatter
+        if (s->band && !CT_BAND_OVERLAP) {   // helical: z-band blocks instead of the full reduce-scatter
             if (int e = band_reduce(s, m, s->Gtmp, Gnew, st)) return e;
-        } else {
+        } else if (!s->band) {
             if (int e = comm_rc(g, g->comm->reduce_scatter_sum(s->Gtmp, Gnew + s->off0, s->S, st))) return e;
         }
         const size_t j0 = s->off0, j1 = std::min(s->N, s->off0 + s->S);

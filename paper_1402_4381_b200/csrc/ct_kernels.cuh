@@ -977,8 +977,11 @@ struct SliceWalk {
 // NTM: detector-row specialisation, 64 or 32 (every row in one pass, nt a compile-time
 // constant) or 0 (general nt: the rows the active slices meet).
 template <int EPI, int NTM>
+// Image rows [row0, row1) (the multi-rank band exchange back-projects one destination row slab
+// per launch so that each slab's blocks travel while the next slab is computed).
 __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, int first, int stride, int count,
-                                                    const float* __restrict__ y, float* __restrict__ x, GupdArgs ga) {
+                                                    const float* __restrict__ y, float* __restrict__ x, GupdArgs ga,
+                                                    int row0, int row1) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     constexpr int NQ = CT_BACK3D_PAIR ? 2 : 1;
     Foot* table = reinterpret_cast<Foot*>(sm_raw);
@@ -986,8 +989,8 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
     float* ACC = reinterpret_cast<float*>(QPs + 8 * NQ * (kBackRows + 4));
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ix = blockIdx.x * 4 + (wid & 3);
-    const int iy = blockIdx.y * 2 + (wid >> 2);
-    const bool colok = ix < g.nx && iy < g.ny;
+    const int iy = row0 + blockIdx.y * 2 + (wid >> 2);
+    const bool colok = ix < g.nx && iy < row1;
     const int nt = NTM ? NTM : g.nt, ns = g.ns, nz = g.nz;
     const int col = ((colok ? iy : 0) * g.nx + (colok ? ix : 0)) * nz;
     Foot* tab = table + wid * 32;

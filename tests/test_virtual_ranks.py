@@ -178,6 +178,24 @@ def test_band_exchange_long_helix(ct, O):
         assert np.abs(band[r][0] - full[r][0]).max() <= 1e-5 * np.abs(full[r][0]).max()
 
 
+def test_band_exchange_eight_ranks(ct, O):
+    """Eight virtual ranks (the north_star's 8-GPU split) on a 16-row helical case with the band
+    exchange: every rank owns two image rows and a sixth of a helical turn's views per subset."""
+    g = GU.geom("cone_helical", nx=16, nz=24, dx=0.9766, dz=0.625, ns=28, ds=1.0239, nt=6, dt=1.0964, na=192,
+                turns=4.0, pitch=0.8)
+    ell = [(0.0, 0.0, 0.0, 5.5, 4.5, 6.0, 0.0, 0.02), (1.0, -0.5, 1.0, 2.0, 1.5, 3.0, 0.4, 0.01)]
+    d = I.noisy_data(g, ell, 1e5, 0.0, 85)
+    m0 = torch.ones((g["ny"], g["nx"], g["nz"]), dtype=torch.uint8)
+    base = I.config("c4")
+    outs = run_virtual(ct, [g] * 8, d["y"], d["w"], [m0] * 8, 4, 3, base.beta, base.delta, 26, exchange="band")
+    xo, So, logo = oracle_run(O, g, d["y"], d["w"], m0, 4, 3, base.beta, base.delta, 26)
+    for r in range(8):
+        assert np.array_equal(outs[r][2][:, 2], logo[:, 2]), r
+        e = rms_hu(I.to_oracle_image(outs[r][0]), xo, So)
+        assert e <= 0.5, (r, e)
+        assert np.array_equal(outs[r][0], outs[0][0])
+
+
 def test_virtual_ranks_validation(ct):
     g = GU.small_geoms()["fan_c1"]
     a, b = ct.Geometry(g), ct.Geometry(g)
