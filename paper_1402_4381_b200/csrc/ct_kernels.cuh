@@ -1216,44 +1216,64 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
     const int nx = g.nx, ny = g.ny, nz = g.nz;
     const float rho = (float)*rho_p;
     const float ra = rho * (float)*alpha_p;   // rho alpha (BB)
-    auto load_plane = [&](int slot, int iy) {
-        for (int e = threadIdx.x; e < 340; e += 256) {
-            const int a = e / 34, b = e - a * 34;
-            const int ix = ix0 - 1 + a, iz = z0 - 1 + b;
+    // this thread's (at most two) halo-plane elements: position and in-grid flags do not depend
+    // on the plane (computed once); x and the mask byte are loaded independently
+    int pe[2], pix[2], piz[2];
+    bool pin[2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+        const int e = threadIdx.x + 256 * q;
+        const int a = e / 34, b = e - a * 34;
+        pe[q] = e < 340 ? e : -1;
+        pix[q] = ix0 - 1 + a;
+        piz[q] = z0 - 1 + b;
+        pin[q] = e < 340 && pix[q] >= 0 && pix[q] < nx;
+    }
+    auto load_plane = [&](float* P, int iy) {
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            if (pe[q] < 0) continue;
             float v = __int_as_float(0x7fc00000);   // NaN: not in S
-            if (iy >= 0 && iy < ny && ix >= 0 && ix < nx) {
+            if (pin[q] && iy >= 0 && iy < ny) {
+                const int iz = piz[q], c = iy * nx + pix[q];
                 if (iz >= 0 && iz < nz) {
-                    const int j = (iy * nx + ix) * nz + iz;
-                    if (__ldg(&m[j])) v = __ldg(&x[j]);
+                    const int j = c * nz + iz;
+                    const uint8_t mm = __ldg(&m[j]);
+                    const float xv = __ldg(&x[j]);
+                    if (mm) v = xv;
                 } else {
-                    const int c = iy * nx + ix;
                     if (iz == -1 && hz.lo && hz.mlo[c]) v = hz.lo[c];
                     if (iz == nz && hz.hi && hz.mhi[c]) v = hz.hi[c];
                 }
             }
-            Pl[slot][a][b] = v;
+            P[pe[q]] = v;
         }
     };
-    load_plane(0, iy0 - 1);
-    load_plane(1, iy0);
+    // rotating planes iy - 1, iy, iy + 1 (pointer rotation instead of slot arithmetic)
+    float* Pp = &Pl[0][0][0];
+    float* Pc = &Pl[1][0][0];
+    float* Pn = &Pl[2][0][0];
+    load_plane(Pp, iy0 - 1);
+    load_plane(Pc, iy0);
     const int ix = ix0 + tx, iz = z0 + tz;
     const bool inb = ix < nx && iz < nz;
     constexpr float r2 = 0.70710678118654752f, r3 = 0.57735026918962576f;
+    const int own = (tx + 1) * 34 + tz + 1;   // this voxel's offset in a plane
     for (int t = 0; t < kK3Y; t++) {
         const int iy = iy0 + t;
         if (iy >= iy_end) break;
-        load_plane((t + 2) % 3, iy + 1);
+        load_plane(Pn, iy + 1);
         __syncthreads();
         if (inb) {
             const int j = (iy * nx + ix) * nz + iz;
-            const float xj = Pl[(t + 1) % 3][tx + 1][tz + 1];
+            const float xj = Pc[own];
             if (xj != xj) {
                 xn[j] = 0.0f;   // off S
             } else {
                 float gr = 0.0f, cu = 0.0f;
 #pragma unroll
                 for (int oy = -1; oy <= 1; oy++) {
-                    const int sl = (t + 1 + oy + 3) % 3;
+                    const float* Ps = oy < 0 ? Pp : (oy == 0 ? Pc : Pn);
 #pragma unroll
                     for (int ox = -1; ox <= 1; ox++)
 #pragma unroll
@@ -1261,7 +1281,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                             if (oy == 0 && ox == 0 && oz == 0) continue;
                             const int d2 = oy * oy + ox * ox + oz * oz;
                             const float wgt = d2 == 1 ? 1.0f : (d2 == 2 ? r2 : r3);
-                            const float xk = Pl[sl][tx + 1 + ox][tz + 1 + oz];
+                            const float xk = Ps[own + ox * 34 + oz];
                             if (xk == xk) {
                                 float dpsi, om;
                                 fair(xj - xk, inv_delta, dpsi, om);
@@ -1276,6 +1296,10 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
             }
         }
         __syncthreads();
+        float* tp = Pp;   // iy + 1 becomes the centre plane
+        Pp = Pc;
+        Pc = Pn;
+        Pn = tp;
     }
 }
 
