@@ -314,8 +314,10 @@ int ct_oslalm_run(const ct_geom* g, const ct_oslalm_cfg* cfg, const ct_oslalm_da
  * image: the partial back-projections are combined by ncclReduceScatter (fp32) into the row
  * slabs, the g-update, xi partial and K3 update run on the rank's slab, xi is all-reduced
  * (fp64, 8 bytes) and the updated slabs are all-gathered (ncclAllGather) for the next forward
- * projection.  The FISTA inner solver all-reduces full images instead.  D_L sums the ranks'
- * partial back-projections with ncclAllReduce.  NCCL is loaded at run time (libnccl.so.2);
+ * projection (helical scans by default exchange only z-band blocks instead, overlapped with
+ * the back-projection: ct_comm_set_exchange).  The FISTA inner solver all-reduces full images
+ * instead.  D_L sums the ranks' partial back-projections with ncclAllReduce.  NCCL is loaded
+ * at run time (libnccl.so.2);
  * CT_ENCCL if unavailable.  Call before creating OS-LALM states (CT_ESTATE otherwise).
  */
 int ct_comm_init(ct_geom* g, int rank, int nranks, const void* nccl_uid);
