@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                     const int zhi = f.ax.qi + __float2int_rd(fmaf((float)(2 * (LW - 1)), f.ax.kz, f.ax.qf)) + 4;
                     if (zlo >= 0 && zhi <= nz - 1) f.ax.kz = -f.ax.kz;
                 }
+                if (f.n <= 0) f.ax.kz = 0.0f;   // empty column: kz = 0 (the pair dispatch below needs no count test)
                 tab[lane] = f;
             }
             __syncwarp();
@@ -509,14 +510,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
             for (int j0 = 0; j0 < nq; j0 += 2 * H) {
                 const int j = j0 + 2 * hf;   // this stream's two columns
                 Foot f0, f1;
-                if (j < nq) load_foot(&tab[j], f0); else f0.n = 0;
-                if (j + 1 < nq) load_foot(&tab[j + 1], f1); else f1.n = 0;
+                if (j < nq) load_foot(&tab[j], f0); else { f0.n = 0; f0.ax.kz = 0.0f; }
+                if (j + 1 < nq) load_foot(&tab[j + 1], f1); else { f1.n = 0; f1.ax.kz = 0.0f; }
                 if (f0.n <= 0 && f1.n <= 0) continue;
                 float2 A0 = make_float2(0.0f, 0.0f), A1 = A0;
                 const float kz0 = fabsf(f0.ax.kz), kz1 = fabsf(f1.ax.kz);
-                const float kzm = fmaxf(f0.n > 0 ? kz0 : 0.0f, f1.n > 0 ? kz1 : 0.0f);
-                // interior pair (or a single interior column): no volume predicates
-                const bool inter = (f0.n <= 0 || f0.ax.kz < 0.0f) && (f1.n <= 0 || f1.ax.kz < 0.0f);
+                const float kzm = fmaxf(kz0, kz1);   // empty columns carry kz = 0
+                // interior pair (or a single interior column; empty ones carry kz = 0): no volume predicates
+                const bool inter = f0.ax.kz <= 0.0f && f1.ax.kz <= 0.0f;
 #define CT_FWD3D2_AXIAL(KS_)                                                                   \
     if (inter) {                                                                               \
         if (f0.n > 0) A0 = fwd_axial_pair<KS_, true>(f0, x, ll, nz);                           \
