@@ -785,9 +785,6 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 #ifndef CT_BACK3D_PAIR
 #define CT_BACK3D_PAIR 0   // 1: two views per slice walk (one accumulator update per slice for both); A/B: slower (64 registers, 4 CTAs/SM: c5 11.25 -> 12.38 ms)
 #endif
-#ifndef CT_BACK3D_PIPE
-#define CT_BACK3D_PIPE 0   // 1: software-pipelined detector-row loads (64-row detector)
-#endif
 #ifndef CT_BACK3D_PREFETCH
 #define CT_BACK3D_PREFETCH 0   // 1: L1 prefetch of the next view's detector rows (A/B: c5 11.32 -> 13.08 ms, off)
 #endif
@@ -1043,64 +1040,6 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
             }
             __syncwarp();
             const int nb = min(32, count - vb);
-#if CT_BACK3D_PIPE
-            if (NTM == 64 && NQ == 1) {
-                // 64-row detector, software-pipelined rows: view j + 1's detector rows (footprints of
-                // <= 4 channels) are loaded before view j's scan and slice walk, which hide their latency
-                float2 pv[4];
-                int pn = -1;
-                for (int j = 0; j < nb; j++) {
-                    Foot fa;
-                    load_foot(&tab[j], fa);
-                    float2 nv[4];
-                    int nn = -1;
-                    if (j + 1 < nb) {
-                        const int* tn = reinterpret_cast<const int*>(&tab[j + 1]);
-                        const int cn = tn[kMaxFoot], n1 = tn[kMaxFoot + 1];
-                        if (n1 > 0 && n1 <= 4) {
-                            const float2* yr = reinterpret_cast<const float2*>(y + ((size_t)(vb + j + 1) * ns + cn) * 64) + lane;
-#pragma unroll
-                            for (int c = 0; c < 4; c++) nv[c] = c < n1 ? __ldg(yr + c * 32) : make_float2(0.0f, 0.0f);
-                            nn = n1;
-                        }
-                    }
-                    if (fa.n > 0) {
-                        float q0 = 0.0f, q1 = 0.0f;
-                        if (pn > 0) {   // weights past n are 0
-#pragma unroll
-                            for (int c = 0; c < 4; c++) {
-                                q0 = fmaf(fa.w[c], pv[c].x, q0);
-                                q1 = fmaf(fa.w[c], pv[c].y, q1);
-                            }
-                        } else {
-                            const float2* yr = reinterpret_cast<const float2*>(y + ((size_t)(vb + j) * ns + fa.cA) * 64) + lane;
-                            if (fa.n <= 3) filt_rows2<3>(yr, 32, true, fa, q0, q1);
-                            else if (fa.n <= 4) filt_rows2<4>(yr, 32, true, fa, q0, q1);
-                            else filt_rows2<kMaxFoot>(yr, 32, true, fa, q0, q1);
-                        }
-                        back3d_qp64(q0, q1, lane, QPA);
-                        __syncwarp();
-                        const int z0 = fa.rows & 0xffff, nzs = fa.rows >> 16;
-                        SliceWalk w1;
-                        w1.init(fa, g, z0, lane, 0, 64, QPA);
-                        if (CT_BACK3D_BLOCKED && nzs > 31 && nzs <= 63) w1.walk_blocked<2>(acc + z0, lane);
-                        else if (CT_BACK3D_BLOCKED && nzs > 63 && nzs <= 95) w1.walk_blocked<3>(acc + z0, lane);
-                        else if (CT_BACK3D_BLOCKED && nzs > 95 && nzs <= 127) w1.walk_blocked<4>(acc + z0, lane);
-                        else {
-                            float* accl = acc + z0 + lane;
-                            float sf = 0.0f;
-#pragma unroll 1
-                            for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) accl[s0] += w1.contrib(sf);
-                        }
-                        __syncwarp();
-                    }
-#pragma unroll
-                    for (int c = 0; c < 4; c++) pv[c] = nv[c];
-                    pn = nn;
-                }
-                continue;
-            }
-#endif
             for (int j = 0; j < nb; j += NQ) {
 #if CT_BACK3D_PREFETCH
                 // L1 prefetch of the next view's detector rows ([channel][row] block of n * nt
