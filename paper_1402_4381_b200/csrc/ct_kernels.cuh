@@ -930,12 +930,15 @@ __device__ __forceinline__ void back3d_qp64(float q0, float q1, int lane, float2
 // Per-view constants of the slice walk (step (2)): the slice edge zi (voxel units relative to
 // the view's qi, minus qf) maps to the detector-row coordinate u = zi inv_kz + ubl in [0, nr].
 struct SliceWalk {
+    float zbase;     // edge of the walk's first slice z0 (voxel units relative to qi, minus qf)
     float zl;        // this lane's edge in pass 0 of a walk starting at slice z0
     float inv_kz, ubl, fnr, dz_rho, hdz;
     const float2* QP;
-    __device__ __forceinline__ void init(const Foot& f, const DevGeom& g, int z0, int lane, int r_lo, int nr,
+    // flane = (float)lane (computed once per thread)
+    __device__ __forceinline__ void init(const Foot& f, const DevGeom& g, int z0, float flane, int r_lo, int nr,
                                          const float2* qp) {
-        zl = (float)(z0 + lane - f.ax.qi) - f.ax.qf;
+        zbase = (float)(z0 - f.ax.qi) - f.ax.qf;
+        zl = zbase + flane;
         inv_kz = f.ax.inv_kz;
         ubl = g.rbase + 0.5f - (float)r_lo;
         fnr = (float)nr;
@@ -969,8 +972,8 @@ struct SliceWalk {
     // bookkeeping is paid once).  Lane 31's last slice has no upper edge: it adds 0.  acc0 =
     // accumulator of the walk's first slice.
     template <int S>
-    __device__ __forceinline__ void walk_blocked(float* acc0, int lane) const {
-        const float zb = zl - (float)lane + (float)(S * lane);   // this lane's first edge
+    __device__ __forceinline__ void walk_blocked(float* acc0, int lane, float flane) const {
+        const float zb = fmaf((float)S, flane, zbase);   // this lane's first edge
         float pf[S];
 #pragma unroll
         for (int e = 0; e < S; e++) pf[e] = pf_at(zb + (float)e);
@@ -1003,6 +1006,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
     float2* QPs = reinterpret_cast<float2*>(sm_raw + sizeof(Foot) * 8 * 32);
     float* ACC = reinterpret_cast<float*>(QPs + 8 * NQ * (kBackRows + 4));
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const float flane = (float)lane;
     const int ix = blockIdx.x * 4 + (wid & 3);
     const int iy = row0 + blockIdx.y * 2 + (wid >> 2);
     const bool colok = ix < g.nx && iy < row1;
@@ -1040,6 +1044,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
             }
             __syncwarp();
             const int nb = min(32, count - vb);
+            const float* yb = y + (size_t)vb * ns * nt;   // this batch's views
             for (int j = 0; j < nb; j += NQ) {
 #if CT_BACK3D_PREFETCH
                 // L1 prefetch of the next view's detector rows ([channel][row] block of n * nt
@@ -1061,8 +1066,9 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 if (!va && !vbv) continue;
                 // (1) filtered rows Q(r) = sum_c lphi F_s(c) y[k][c][r] and their prefix sums
                 int rla = 0, nra = 0, rlb = 0, nrb = 0;
-                if (va) back3d_rows<NTM>(g, fa, y + ((size_t)(vb + j) * ns + fa.cA) * nt, lane, QPA, rla, nra);
-                if (vbv) back3d_rows<NTM>(g, fb, y + ((size_t)(vb + j + 1) * ns + fb.cA) * nt, lane, QPB, rlb, nrb);
+                // (32-bit offsets within the batch: count * ns * nt < 2^31, validated at create)
+                if (va) back3d_rows<NTM>(g, fa, yb + (j * ns + fa.cA) * nt, lane, QPA, rla, nra);
+                if (vbv) back3d_rows<NTM>(g, fb, yb + ((j + 1) * ns + fb.cA) * nt, lane, QPB, rlb, nrb);
                 __syncwarp();
                 // (2) the union of the views' active slices (lanes = slices): per view the integral
                 //     of the row-wise constant Q over the slice's extent on the detector,
@@ -1075,8 +1081,8 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 const int z0 = va ? (vbv ? min(zaA, zaB) : zaA) : zaB;
                 const int nzs = (va ? (vbv ? max(zeA, zeB) : zeA) : zeB) - z0;
                 SliceWalk wa, wb;
-                if (va) wa.init(fa, g, z0, lane, rla, nra, QPA);
-                if (vbv) wb.init(fb, g, z0, lane, rlb, nrb, QPB);
+                if (va) wa.init(fa, g, z0, flane, rla, nra, QPA);
+                if (vbv) wb.init(fb, g, z0, flane, rlb, nrb, QPB);
                 float* accl = acc + z0 + lane;
                 float sf = 0.0f;   // (float)s0
 #if CT_DEBUG_CHECKS
@@ -1101,9 +1107,9 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                     const SliceWalk& w1 = va ? wa : wb;
                     // one blocked pass covers 32 S - 1 slices (tail lanes clamp to 0 or land in the
                     // padding: z0 + 32 S - 1 <= nz + kBackPad - 1 since nzs >= 32 (S - 1))
-                    if (CT_BACK3D_BLOCKED && nzs > 31 && nzs <= 63) w1.walk_blocked<2>(acc + z0, lane);
-                    else if (CT_BACK3D_BLOCKED && nzs > 63 && nzs <= 95) w1.walk_blocked<3>(acc + z0, lane);
-                    else if (CT_BACK3D_BLOCKED && nzs > 95 && nzs <= 127) w1.walk_blocked<4>(acc + z0, lane);
+                    if (CT_BACK3D_BLOCKED && nzs > 31 && nzs <= 63) w1.walk_blocked<2>(acc + z0, lane, flane);
+                    else if (CT_BACK3D_BLOCKED && nzs > 63 && nzs <= 95) w1.walk_blocked<3>(acc + z0, lane, flane);
+                    else if (CT_BACK3D_BLOCKED && nzs > 95 && nzs <= 127) w1.walk_blocked<4>(acc + z0, lane, flane);
                     else {
 #pragma unroll 1   // (A/B: the compiler's unrolled version needs more registers, -5 %)
                         for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) accl[s0] += w1.contrib(sf);
