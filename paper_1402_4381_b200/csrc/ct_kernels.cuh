@@ -785,6 +785,9 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 #ifndef CT_BACK3D_PAIR
 #define CT_BACK3D_PAIR 0   // 1: two views per slice walk (one accumulator update per slice for both); A/B: slower (64 registers, 4 CTAs/SM: c5 11.25 -> 12.38 ms)
 #endif
+#ifndef CT_BACK3D_ROWS2V
+#define CT_BACK3D_ROWS2V 1   // 64-row detector: two views per rows phase (half-warps, float4 rows)
+#endif
 #ifndef CT_BACK3D_PREFETCH
 #define CT_BACK3D_PREFETCH 0   // 1: L1 prefetch of the next view's detector rows (A/B: c5 11.32 -> 13.08 ms, off)
 #endif
@@ -1045,6 +1048,74 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
             __syncwarp();
             const int nb = min(32, count - vb);
             const float* yb = y + (size_t)vb * ns * nt;   // this batch's views
+#if CT_BACK3D_ROWS2V
+            if (NTM == 64 && NQ == 1) {
+                // 64-row detector, two views per rows phase: half-warp h filters view j + h (lane
+                // = four rows, float4 loads), a 16-lane scan per half; then each view's slice walk
+                // on the whole warp.  Per view this halves the row loads and scan steps.
+                const int h = lane >> 4, l16 = lane & 15;
+                float2* QPh = QPA + h * 66;   // two 65-entry tables in the warp's 132 slots
+                for (int j = 0; j < nb; j += 2) {
+                    Foot fh;
+                    load_foot(&tab[min(j + h, nb - 1)], fh);   // (a finite record for the idle half)
+                    if (j + h >= nb) fh.n = 0;
+                    const int nmax = __reduce_max_sync(0xffffffffu, fh.n > 0 ? fh.n : 0);
+                    if (nmax <= 0) continue;
+                    float q0 = 0.0f, q1 = 0.0f, q2 = 0.0f, q3 = 0.0f;
+                    {
+                        const float4* yr = reinterpret_cast<const float4*>(yb + ((j + h) * ns + fh.cA) * 64) + l16;
+#define CT_B3_ROWS4(NC_)                                                                      \
+    {                                                                                         \
+        float4 vv[NC_];                                                                       \
+        _Pragma("unroll") for (int c = 0; c < NC_; c++)                                       \
+            vv[c] = c < fh.n ? __ldg(yr + c * 16) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);       \
+        _Pragma("unroll") for (int c = 0; c < NC_; c++) {                                     \
+            q0 = fmaf(fh.w[c], vv[c].x, q0);                                                  \
+            q1 = fmaf(fh.w[c], vv[c].y, q1);                                                  \
+            q2 = fmaf(fh.w[c], vv[c].z, q2);                                                  \
+            q3 = fmaf(fh.w[c], vv[c].w, q3);                                                  \
+        }                                                                                     \
+    }
+                        if (nmax <= 3) CT_B3_ROWS4(3)
+                        else if (nmax <= 4) CT_B3_ROWS4(4)
+                        else CT_B3_ROWS4(kMaxFoot)
+#undef CT_B3_ROWS4
+                    }
+                    const float s4 = (q0 + q1) + (q2 + q3);
+                    float inc = s4;
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) {
+                        const float t = __shfl_up_sync(0xffffffffu, inc, o, 16);
+                        if (l16 >= o) inc += t;
+                    }
+                    const float ex = inc - s4, e1 = ex + q0, e2 = e1 + q1, e3 = e2 + q2;
+                    reinterpret_cast<float4*>(QPh)[2 * l16] = make_float4(ex, q0, e1, q1);
+                    reinterpret_cast<float4*>(QPh)[2 * l16 + 1] = make_float4(e2, q2, e3, q3);
+                    if (l16 == 15) QPh[64] = make_float2(inc, 0.0f);
+                    __syncwarp();
+#pragma unroll 1
+                    for (int v2 = 0; v2 < 2 && j + v2 < nb; v2++) {
+                        Foot fw;
+                        load_foot(&tab[j + v2], fw);
+                        if (fw.n <= 0) continue;
+                        const int z0 = fw.rows & 0xffff, nzs = fw.rows >> 16;
+                        SliceWalk w1;
+                        w1.init(fw, g, z0, flane, 0, 64, QPA + v2 * 66);
+                        if (CT_BACK3D_BLOCKED && nzs > 31 && nzs <= 63) w1.walk_blocked<2>(acc + z0, lane, flane);
+                        else if (CT_BACK3D_BLOCKED && nzs > 63 && nzs <= 95) w1.walk_blocked<3>(acc + z0, lane, flane);
+                        else if (CT_BACK3D_BLOCKED && nzs > 95 && nzs <= 127) w1.walk_blocked<4>(acc + z0, lane, flane);
+                        else {
+                            float* accl = acc + z0 + lane;
+                            float sf = 0.0f;
+#pragma unroll 1
+                            for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) accl[s0] += w1.contrib(sf);
+                        }
+                        __syncwarp();
+                    }
+                }
+                continue;
+            }
+#endif
             for (int j = 0; j < nb; j += NQ) {
 #if CT_BACK3D_PREFETCH
                 // L1 prefetch of the next view's detector rows ([channel][row] block of n * nt
