@@ -786,7 +786,7 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 #define CT_BACK3D_PAIR 0   // 1: two views per slice walk (one accumulator update per slice for both); A/B: slower (64 registers, 4 CTAs/SM: c5 11.25 -> 12.38 ms)
 #endif
 #ifndef CT_BACK3D_ROWS2V
-#define CT_BACK3D_ROWS2V 1   // 64-row detector: two views per rows phase (half-warps, float4 rows)
+#define CT_BACK3D_ROWS2V 0   // 1: two views per rows phase (half-warps; 64- and 32-row detectors); A/B c5 10.73 -> 10.85 ms
 #endif
 #ifndef CT_BACK3D_PREFETCH
 #define CT_BACK3D_PREFETCH 0   // 1: L1 prefetch of the next view's detector rows (A/B: c5 11.32 -> 13.08 ms, off)
@@ -1049,49 +1049,64 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
             const int nb = min(32, count - vb);
             const float* yb = y + (size_t)vb * ns * nt;   // this batch's views
 #if CT_BACK3D_ROWS2V
-            if (NTM == 64 && NQ == 1) {
-                // 64-row detector, two views per rows phase: half-warp h filters view j + h (lane
-                // = four rows, float4 loads), a 16-lane scan per half; then each view's slice walk
-                // on the whole warp.  Per view this halves the row loads and scan steps.
+            if ((NTM == 64 || NTM == 32) && NQ == 1) {
+                // 64- / 32-row detector, two views per rows phase: half-warp h filters view j + h
+                // (lane = NTM / 16 rows: float4 / float2 loads), a 16-lane scan per half; then each
+                // view's slice walk on the whole warp.  Per view this halves the row loads and the
+                // scan steps.
+                constexpr int RL = NTM / 16 > 0 ? NTM / 16 : 1, QS = NTM + 2;   // rows per lane, table stride
                 const int h = lane >> 4, l16 = lane & 15;
-                float2* QPh = QPA + h * 66;   // two 65-entry tables in the warp's 132 slots
+                float2* QPh = QPA + h * QS;   // two (NTM + 1)-entry tables in the warp's 132 slots
                 for (int j = 0; j < nb; j += 2) {
                     Foot fh;
                     load_foot(&tab[min(j + h, nb - 1)], fh);   // (a finite record for the idle half)
                     if (j + h >= nb) fh.n = 0;
                     const int nmax = __reduce_max_sync(0xffffffffu, fh.n > 0 ? fh.n : 0);
                     if (nmax <= 0) continue;
-                    float q0 = 0.0f, q1 = 0.0f, q2 = 0.0f, q3 = 0.0f;
+                    float q[4] = {0.0f, 0.0f, 0.0f, 0.0f};
                     {
-                        const float4* yr = reinterpret_cast<const float4*>(yb + ((j + h) * ns + fh.cA) * 64) + l16;
-#define CT_B3_ROWS4(NC_)                                                                      \
-    {                                                                                         \
-        float4 vv[NC_];                                                                       \
-        _Pragma("unroll") for (int c = 0; c < NC_; c++)                                       \
-            vv[c] = c < fh.n ? __ldg(yr + c * 16) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);       \
-        _Pragma("unroll") for (int c = 0; c < NC_; c++) {                                     \
-            q0 = fmaf(fh.w[c], vv[c].x, q0);                                                  \
-            q1 = fmaf(fh.w[c], vv[c].y, q1);                                                  \
-            q2 = fmaf(fh.w[c], vv[c].z, q2);                                                  \
-            q3 = fmaf(fh.w[c], vv[c].w, q3);                                                  \
-        }                                                                                     \
+                        const float* yrow = yb + ((j + h) * ns + fh.cA) * NTM + RL * l16;
+#define CT_B3_ROWS(NC_)                                                                                       \
+    {                                                                                                         \
+        float4 vv[NC_];                                                                                       \
+        _Pragma("unroll") for (int c = 0; c < NC_; c++) {                                                     \
+            if (RL == 4)                                                                                      \
+                vv[c] = c < fh.n ? __ldg(reinterpret_cast<const float4*>(yrow + c * NTM)) : make_float4(0, 0, 0, 0); \
+            else {                                                                                            \
+                const float2 t2 = c < fh.n ? __ldg(reinterpret_cast<const float2*>(yrow + c * NTM)) : make_float2(0, 0); \
+                vv[c] = make_float4(t2.x, t2.y, 0.0f, 0.0f);                                                  \
+            }                                                                                                 \
+        }                                                                                                     \
+        _Pragma("unroll") for (int c = 0; c < NC_; c++) {                                                     \
+            q[0] = fmaf(fh.w[c], vv[c].x, q[0]);                                                              \
+            q[1] = fmaf(fh.w[c], vv[c].y, q[1]);                                                              \
+            if (RL == 4) {                                                                                    \
+                q[2] = fmaf(fh.w[c], vv[c].z, q[2]);                                                          \
+                q[3] = fmaf(fh.w[c], vv[c].w, q[3]);                                                          \
+            }                                                                                                 \
+        }                                                                                                     \
     }
-                        if (nmax <= 3) CT_B3_ROWS4(3)
-                        else if (nmax <= 4) CT_B3_ROWS4(4)
-                        else CT_B3_ROWS4(kMaxFoot)
-#undef CT_B3_ROWS4
+                        if (nmax <= 3) CT_B3_ROWS(3)
+                        else if (nmax <= 4) CT_B3_ROWS(4)
+                        else CT_B3_ROWS(kMaxFoot)
+#undef CT_B3_ROWS
                     }
-                    const float s4 = (q0 + q1) + (q2 + q3);
-                    float inc = s4;
+                    const float sl = RL == 4 ? (q[0] + q[1]) + (q[2] + q[3]) : q[0] + q[1];
+                    float inc = sl;
 #pragma unroll
                     for (int o = 1; o < 16; o <<= 1) {
                         const float t = __shfl_up_sync(0xffffffffu, inc, o, 16);
                         if (l16 >= o) inc += t;
                     }
-                    const float ex = inc - s4, e1 = ex + q0, e2 = e1 + q1, e3 = e2 + q2;
-                    reinterpret_cast<float4*>(QPh)[2 * l16] = make_float4(ex, q0, e1, q1);
-                    reinterpret_cast<float4*>(QPh)[2 * l16 + 1] = make_float4(e2, q2, e3, q3);
-                    if (l16 == 15) QPh[64] = make_float2(inc, 0.0f);
+                    const float ex = inc - sl, e1 = ex + q[0];
+                    if (RL == 4) {
+                        const float e2 = e1 + q[1], e3 = e2 + q[2];
+                        reinterpret_cast<float4*>(QPh)[2 * l16] = make_float4(ex, q[0], e1, q[1]);
+                        reinterpret_cast<float4*>(QPh)[2 * l16 + 1] = make_float4(e2, q[2], e3, q[3]);
+                    } else {
+                        reinterpret_cast<float4*>(QPh)[l16] = make_float4(ex, q[0], e1, q[1]);
+                    }
+                    if (l16 == 15) QPh[NTM] = make_float2(inc, 0.0f);
                     __syncwarp();
 #pragma unroll 1
                     for (int v2 = 0; v2 < 2 && j + v2 < nb; v2++) {
@@ -1100,7 +1115,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                         if (fw.n <= 0) continue;
                         const int z0 = fw.rows & 0xffff, nzs = fw.rows >> 16;
                         SliceWalk w1;
-                        w1.init(fw, g, z0, flane, 0, 64, QPA + v2 * 66);
+                        w1.init(fw, g, z0, flane, 0, NTM, QPA + v2 * QS);
                         if (CT_BACK3D_BLOCKED && nzs > 31 && nzs <= 63) w1.walk_blocked<2>(acc + z0, lane, flane);
                         else if (CT_BACK3D_BLOCKED && nzs > 63 && nzs <= 95) w1.walk_blocked<3>(acc + z0, lane, flane);
                         else if (CT_BACK3D_BLOCKED && nzs > 95 && nzs <= 127) w1.walk_blocked<4>(acc + z0, lane, flane);
