@@ -125,6 +125,24 @@ def test_back_accumulate_and_empty_views(ct):
         geo.back(p, (5, 1, g["na"]))
 
 
+def test_determinism_3d_iteration(ct):
+    """Bit-reproducible OS-LALM iterations in 3D (helical, 26 neighbours): two fresh states on
+    the same inputs give identical images (no float atomics anywhere on the path)."""
+    g = GU.small_geoms()["helical_c5"]
+    ell = [(0.0, 0.0, 0.0, 4.0, 3.5, 2.5, 0.0, 0.02)]
+    d = I.noisy_data(g, ell, 1e5, 0.0, 3)
+    geo = ct.Geometry(g)
+    dl, S = geo.sqs_denom(d["w"].cuda(), torch.ones(geo.img_shape, dtype=torch.uint8).cuda())
+    outs = []
+    for _ in range(2):
+        sol = ct.OSLALM(geo, 4, beta=2.0 ** 10, delta=2e-4, nbr=26)
+        sol.set_data(d["y"].cuda(), d["w"].cuda(), dl, S)
+        x = torch.zeros(geo.img_shape, device="cuda")
+        sol.run(x, 3)
+        outs.append(x)
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_determinism(ct):
     g = I.config("c1").geom
     geo = ct.Geometry(g)
