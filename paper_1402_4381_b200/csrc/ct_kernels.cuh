@@ -785,8 +785,13 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 #ifndef CT_BACK3D_PAIR
 #define CT_BACK3D_PAIR 0   // 1: two views per slice walk (one accumulator update per slice for both); A/B: slower (64 registers, 4 CTAs/SM: c5 11.25 -> 12.38 ms)
 #endif
-#ifndef CT_BACK3D_ROWS2V
-#define CT_BACK3D_ROWS2V 0   // 1: two views per rows phase (half-warps; 64- and 32-row detectors); A/B c5 10.73 -> 10.85 ms
+// two views per rows phase (half-warps): A/B 32-row detector c4 4.04 -> 3.90 ms (on), 64-row
+// detector c5 10.73 -> 10.85 ms (off)
+#ifndef CT_BACK3D_ROWS2V_32
+#define CT_BACK3D_ROWS2V_32 1
+#endif
+#ifndef CT_BACK3D_ROWS2V_64
+#define CT_BACK3D_ROWS2V_64 0
 #endif
 #ifndef CT_BACK3D_PREFETCH
 #define CT_BACK3D_PREFETCH 0   // 1: L1 prefetch of the next view's detector rows (A/B: c5 11.32 -> 13.08 ms, off)
@@ -1048,8 +1053,8 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
             __syncwarp();
             const int nb = min(32, count - vb);
             const float* yb = y + (size_t)vb * ns * nt;   // this batch's views
-#if CT_BACK3D_ROWS2V
-            if ((NTM == 64 || NTM == 32) && NQ == 1) {
+#if CT_BACK3D_ROWS2V_32 || CT_BACK3D_ROWS2V_64
+            if (((NTM == 64 && CT_BACK3D_ROWS2V_64) || (NTM == 32 && CT_BACK3D_ROWS2V_32)) && NQ == 1) {
                 // 64- / 32-row detector, two views per rows phase: half-warp h filters view j + h
                 // (lane = NTM / 16 rows: float4 / float2 loads), a 16-lane scan per half; then each
                 // view's slice walk on the whole warp.  Per view this halves the row loads and the
