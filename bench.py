@@ -506,9 +506,12 @@ def main():
             Te = sum(es[2 * i].elapsed_time(es[2 * i + 1]) for i in range(K)) / 1e3
             mode = "serial (L2 flushed between steps)"
         Te = allreduce_max(Te, ws)
+        torch.cuda.synchronize()
         e2e = {"value": work_step * K / Te, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(x.numel() * 4),
-               "ms_per_step": 1e3 * Te / K, "copies": mode}
+               "ms_per_step": 1e3 * Te / K, "copies": mode,
+               # the last read-back is the final iterate (the pipeline's ordering check)
+               "readback_matches_device": bool(torch.equal(x_h, x.cpu()))}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
