@@ -1631,7 +1631,7 @@ static int ensure_initialised(ct_oslalm_state* s, const ct_oslalm_data* d, float
     return CT_OK;
 }
 
-static int check_data(const ct_geom* g, const ct_oslalm_data* d, const float* x) {
+static int check_data(const ct_oslalm_data* d, const float* x) {
     if (!d || !d->y || !d->w || !d->dl || !d->mask || !x) return fail(CT_EINVAL, "ct_oslalm: null data pointer");
     return CT_OK;
 }
@@ -1656,7 +1656,7 @@ extern "C" int ct_oslalm_iter(const ct_geom* g, const ct_oslalm_cfg* cfg, const 
         for (auto& ge : s->graphs)
             if (ge.exec) { cudaGraphExecDestroy(ge.exec); ge.exec = nullptr; }
     }
-    if (int e = check_data(g, d, x)) return e;
+    if (int e = check_data(d, x)) return e;
     if (g->nranks != s->P || g->rank != s->prank || (g->comm != nullptr) != s->has_comm)
         return fail(CT_ESTATE, "communicator changed after state creation (create the state after ct_comm_init)");
     DeviceGuard guard(g->d.device);

@@ -241,7 +241,15 @@ struct VirtualComm : Comm {
     const char* kind() const override { return "virtual"; }
     const char* last_err() const override { return err; }
     int run(int op, const void* send, const void* send2, void* recv, void* recv2, size_t n, int dt, cudaStream_t st) {
-        VirtualGroup::Slot s{op, send, send2, recv, recv2, n, dt, st};
+        VirtualGroup::Slot s{};
+        s.op = op;
+        s.send = send;
+        s.send2 = send2;
+        s.recv = recv;
+        s.recv2 = recv2;
+        s.n = n;
+        s.dt = dt;
+        s.st = st;
         return grp->collective(rank, s, err, sizeof(err));
     }
     int allreduce_sum(const void* send, void* recv, size_t n, int dt, cudaStream_t st) override {
@@ -260,7 +268,10 @@ struct VirtualComm : Comm {
     }
     int alltoallv(const float* const* send, const size_t* scount, float* const* recv, const size_t* rcount,
                   cudaStream_t st) override {
-        VirtualGroup::Slot s{VirtualGroup::OP_ALLTOALLV, nullptr, nullptr, nullptr, nullptr, 0, COMM_F32, st};
+        VirtualGroup::Slot s{};
+        s.op = VirtualGroup::OP_ALLTOALLV;
+        s.dt = COMM_F32;
+        s.st = st;
         s.vs.assign(send, send + nranks);
         s.vsc.assign(scount, scount + nranks);
         s.vr.assign(recv, recv + nranks);
