@@ -368,7 +368,9 @@ int ct_comm_set_exchange(ct_geom* g, int mode);
  * own stream (ct_oslalm_iter / ct_sqs_denom of all ranks concurrently, in the same order);
  * the collective's copies and fixed-order (rank 0..P-1) sum kernels run on a group stream
  * ordered by CUDA events after every rank's stream, and every rank's stream waits for them.
- * No kernel waits on another kernel.  Replaces any communicator attached before.
+ * No kernel waits on another kernel.  Replaces any communicator attached before.  (The one
+ * exception to "no allocation after create": the group allocates a device staging buffer
+ * for its sums at the first collective that needs a larger one.)
  * Errors: CT_EINVAL (null / duplicate handles, different devices), CT_EUNSUPPORTED (zslab on
  * a fan geometry), CT_ECUDA.  A failed exchange returns CT_ENCCL on every rank.
  */
