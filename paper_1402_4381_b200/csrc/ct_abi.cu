@@ -1533,10 +1533,15 @@ static int enqueue_iteration(ct_oslalm_state* s, const ct_oslalm_data* d, float*
                         if (g->rank > 0) { hz.lo = s->zrecv[0]; hz.mlo = s->zmask[0]; }
                         if (g->rank < g->nranks - 1) { hz.hi = s->zrecv[1]; hz.mhi = s->zmask[1]; }
                     }
-                    sqs_update3d_kernel<<<dim3((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (ry1 - ry0 + kK3Y - 1) / kK3Y),
-                                          256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl, d->mask,
-                                                        &s->sc->rho, &s->sc->alpha, (float)c.reg.beta, inv_d, ry0,
-                                                        ry1, hz);
+                    const dim3 grid((g->dg.nx + 7) / 8, (g->dg.nz + 31) / 32, (ry1 - ry0 + kK3Y - 1) / kK3Y);
+                    if (hz.lo || hz.hi)
+                        sqs_update3d_kernel<true><<<grid, 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl,
+                                                                        d->mask, &s->sc->rho, &s->sc->alpha,
+                                                                        (float)c.reg.beta, inv_d, ry0, ry1, hz);
+                    else
+                        sqs_update3d_kernel<false><<<grid, 256, 0, st>>>(g->dg, xa, xb, s->Gbuf[s->curG], s->gs, d->dl,
+                                                                         d->mask, &s->sc->rho, &s->sc->alpha,
+                                                                         (float)c.reg.beta, inv_d, ry0, ry1, hz);
                 }
                 CT_LAUNCHED(1);
             }

@@ -285,4 +285,21 @@ __device__ __forceinline__ void fair(float t, float inv_delta, float& dpsi, floa
     dpsi = t * omega;
 }
 
+// Branch-free form for the shared-memory stencils: voxels outside S (or outside the grid)
+// are stored as +inf, so t = xj - xk = -inf, v = inf, omega = rcp(inf) = +0 (PTX
+// rcp.approx: +-inf -> +-0) and dpsi = max(t, -FLT_MAX) omega = -0: an excluded pair adds
+// exactly zero, and for an included pair the values are those of fair() (same operations).
+// (A/B, c5 K3: the NaN form's per-neighbour branch kept the ADU pipe 68 % busy.)
+constexpr unsigned kOffS = 0x7f800000u;   // +inf: not in S
+__device__ __forceinline__ void fair_masked(float xj, float xk, float inv_delta, float& dpsi, float& omega) {
+    const float t = xj - xk;
+    const float v = fmaf(fabsf(t), inv_delta, 1.0f);
+#if CT_FAIR_RCP_APPROX
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(omega) : "f"(v));
+#else
+    omega = __frcp_rn(v);   // correctly rounded: rcp(inf) = +0 as well
+#endif
+    dpsi = fmaxf(t, -3.40282347e38f) * omega;
+}
+
 }  // namespace ct

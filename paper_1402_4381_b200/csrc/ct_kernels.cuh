@@ -1309,11 +1309,12 @@ __global__ void __launch_bounds__(256) resid_kernel(float* __restrict__ s, const
 
 // 3D (26-neighbour) K3 with shared-memory planes: block = 8 (ix) x 32 (z) voxels
 // marching along iy; three planes of x (with a one-voxel halo) rotate through
-// shared memory, voxels outside S (or outside the grid) are stored as NaN so the
-// "both voxels in S" pair rule is one comparison and the stencil needs no bounds
-// checks.  Streams G, g, D_L once and writes x' once (21 B/voxel of HBM).
+// shared memory, voxels outside S (or outside the grid) are stored as +inf so the
+// "both voxels in S" pair rule costs no branch (fair_masked) and the stencil needs no
+// bounds checks.  Streams G, g, D_L once and writes x' once (21 B/voxel of HBM).
 constexpr int kK3Y = 8;
 
+template <bool HALO>
 __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
                                                           const float* __restrict__ G, const float* __restrict__ gs,
                                                           const float* __restrict__ dl, const uint8_t* __restrict__ m,
@@ -1321,42 +1322,46 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                                                           const double* __restrict__ alpha_p, float beta, float inv_delta,
                                                           int iy_begin, int iy_end, ZHalo hz) {
     // updates rows [iy_begin, iy_end) (multi-rank: this rank's slab; x is the full image).
-    // z-slab ranks: hz holds the neighbours' boundary slices (z = -1, z = nz) and their mask.
+    // HALO (z-slab ranks): hz holds the neighbours' boundary slices (z = -1, z = nz) and their mask.
     __shared__ float Pl[3][10][34];
     const int tz = threadIdx.x & 31, tx = threadIdx.x >> 5;
     const int ix0 = blockIdx.x * 8, z0 = blockIdx.y * 32, iy0 = iy_begin + blockIdx.z * kK3Y;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
     const float rho = (float)*rho_p;
     const float ra = rho * (float)*alpha_p;   // rho alpha (BB)
-    // this thread's (at most two) halo-plane elements: position and in-grid flags do not depend
-    // on the plane (computed once); x and the mask byte are loaded independently
-    int pe[2], pix[2], piz[2];
+    // this thread's (at most two) halo-plane elements: slot, in-plane offset and in-grid flag
+    // do not depend on the plane (computed once).  The loads are unconditional (clamped to
+    // element 0 outside the grid) and selected afterwards: no branches per plane.
+    int pe[2], pj[2], pc[2], ph[2];
     bool pin[2];
 #pragma unroll
     for (int q = 0; q < 2; q++) {
         const int e = threadIdx.x + 256 * q;
         const int a = e / 34, b = e - a * 34;
-        pe[q] = e < 340 ? e : -1;
-        pix[q] = ix0 - 1 + a;
-        piz[q] = z0 - 1 + b;
-        pin[q] = e < 340 && pix[q] >= 0 && pix[q] < nx;
+        const int ex = ix0 - 1 + a, ez = z0 - 1 + b;
+        const bool inx = e < 340 && ex >= 0 && ex < nx;
+        pe[q] = e < 340 ? e : 0;
+        pin[q] = inx && ez >= 0 && ez < nz;
+        pj[q] = pin[q] ? ex * nz + ez : 0;
+        pc[q] = inx ? ex : 0;
+        ph[q] = !HALO || !inx ? 0 : (ez == -1 ? 1 : (ez == nz ? 2 : 0));   // halo slice below / above
     }
+    const bool two = threadIdx.x + 256 < 340;   // warp-uniform except in one warp
     auto load_plane = [&](float* P, int iy) {
+        const bool rowok = iy >= 0 && iy < ny;
+        const int rb = rowok ? iy * nx * nz : 0;
 #pragma unroll
         for (int q = 0; q < 2; q++) {
-            if (pe[q] < 0) continue;
-            float v = __int_as_float(0x7fc00000);   // NaN: not in S
-            if (pin[q] && iy >= 0 && iy < ny) {
-                const int iz = piz[q], c = iy * nx + pix[q];
-                if (iz >= 0 && iz < nz) {
-                    const int j = c * nz + iz;
-                    const uint8_t mm = __ldg(&m[j]);
-                    const float xv = __ldg(&x[j]);
-                    if (mm) v = xv;
-                } else {
-                    if (iz == -1 && hz.lo && hz.mlo[c]) v = hz.lo[c];
-                    if (iz == nz && hz.hi && hz.mhi[c]) v = hz.hi[c];
-                }
+            if (q == 1 && !two) break;
+            const bool ok = rowok && pin[q];
+            const int j = ok ? rb + pj[q] : 0;
+            const uint8_t mm = __ldg(&m[j]);
+            const float xv = __ldg(&x[j]);
+            float v = ok && mm ? xv : __uint_as_float(kOffS);   // not in S
+            if (HALO && rowok && ph[q]) {
+                const int c = iy * nx + pc[q];
+                if (ph[q] == 1 && hz.lo && hz.mlo[c]) v = hz.lo[c];
+                if (ph[q] == 2 && hz.hi && hz.mhi[c]) v = hz.hi[c];
             }
             P[pe[q]] = v;
         }
@@ -1379,7 +1384,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
         if (inb) {
             const int j = (iy * nx + ix) * nz + iz;
             const float xj = Pc[own];
-            if (xj != xj) {
+            if (xj == __uint_as_float(kOffS)) {
                 xn[j] = 0.0f;   // off S
             } else {
                 float gr = 0.0f, cu = 0.0f;
@@ -1393,13 +1398,10 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                             if (oy == 0 && ox == 0 && oz == 0) continue;
                             const int d2 = oy * oy + ox * ox + oz * oz;
                             const float wgt = d2 == 1 ? 1.0f : (d2 == 2 ? r2 : r3);
-                            const float xk = Ps[own + ox * 34 + oz];
-                            if (xk == xk) {
-                                float dpsi, om;
-                                fair(xj - xk, inv_delta, dpsi, om);
-                                gr += wgt * dpsi;
-                                cu += wgt * om;
-                            }
+                            float dpsi, om;
+                            fair_masked(xj, Ps[own + ox * 34 + oz], inv_delta, dpsi, om);   // 0 off S
+                            gr += wgt * dpsi;
+                            cu += wgt * om;
                         }
                 }
                 const float sdir = rho * __ldg(&G[j]) + (1.0f - rho) * __ldg(&gs[j]);
@@ -1416,7 +1418,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
 }
 
 // 2D (8-neighbour) K3 with a shared-memory tile: block = 32 (ix) x 8 (iy) pixels, the
-// 34 x 10 halo tile of x holds NaN outside S or the grid (pair rule = one comparison).
+// 34 x 10 halo tile of x holds +inf outside S or the grid (pair rule without a branch).
 __global__ void __launch_bounds__(256) sqs_update2d_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
                                                           const float* __restrict__ G, const float* __restrict__ gs,
                                                           const float* __restrict__ dl, const uint8_t* __restrict__ m,
@@ -1462,12 +1464,12 @@ __global__ void __launch_bounds__(256) sqs_update2d_kernel(DevGeom g, const floa
 #pragma unroll
     for (int q = 0; q < 2; q++) {
         const int e = threadIdx.x + 256 * q;
-        if (e < 340) (&T[0][0])[e] = me[q] ? xe[q] : __int_as_float(0x7fc00000);   // NaN: not in S
+        if (e < 340) (&T[0][0])[e] = me[q] ? xe[q] : __uint_as_float(kOffS);   // not in S
     }
     __syncthreads();
     if (!own) return;
     const float xj = T[ty + 1][tx + 1];
-    if (xj != xj) {
+    if (xj == __uint_as_float(kOffS)) {
         xn[j] = 0.0f;   // off S
         return;
     }
@@ -1479,13 +1481,10 @@ __global__ void __launch_bounds__(256) sqs_update2d_kernel(DevGeom g, const floa
         for (int ox = -1; ox <= 1; ox++) {
             if (oy == 0 && ox == 0) continue;
             const float wgt = (oy * oy + ox * ox) == 1 ? 1.0f : r2;
-            const float xk = T[ty + 1 + oy][tx + 1 + ox];
-            if (xk == xk) {
-                float dpsi, om;
-                fair(xj - xk, inv_delta, dpsi, om);
-                gr += wgt * dpsi;
-                cu += wgt * om;
-            }
+            float dpsi, om;
+            fair_masked(xj, T[ty + 1 + oy][tx + 1 + ox], inv_delta, dpsi, om);   // 0 off S
+            gr += wgt * dpsi;
+            cu += wgt * om;
         }
     const float sdir = rho * Gj + (1.0f - rho) * gj;
     const float den = ra * dlj + 2.0f * beta * cu;
