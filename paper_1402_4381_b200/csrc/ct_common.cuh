@@ -269,6 +269,27 @@ __device__ __forceinline__ double ld_dep(const double* p) {
 }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
+// L2 eviction-priority hints (PTX createpolicy + .L2::cache_hint): a fractional policy with
+// fraction 1.0 applies to every access made with it.
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float ldg_pol(const float* a, unsigned long long pol) {
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void stg_pol(float* a, float v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+
 // Fair potential pieces (reading G3/G14)
 #ifndef CT_FAIR_RCP_APPROX
 #define CT_FAIR_RCP_APPROX 1

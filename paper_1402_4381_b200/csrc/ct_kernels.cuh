@@ -343,8 +343,12 @@ constexpr size_t fwd3d_smem() {
 // columns (small kz) do not pay for the far side's longer windows.
 // INTERIOR: every slice the column's row pairs can touch lies inside the volume (flagged in
 // the table by a negative kz), so only the slices past hi need a predicate.
+#ifndef CT_FWD3D2_XHINT
+#define CT_FWD3D2_XHINT 0   // 1: x slice loads carry an L2 evict_last policy, the epilogue's y / W / out evict_first
+#endif
 template <int KS, bool INTERIOR>
-__device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __restrict__ x, int l, int nz) {
+__device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __restrict__ x, int l, int nz,
+                                                 unsigned long long pol = 0) {
     const float kz = fabsf(f.ax.kz);
     const float lo = fmaf((float)(2 * l), kz, f.ax.qf);
     const float mid = lo + kz, hi = mid + kz;
@@ -359,7 +363,7 @@ __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __r
         const float tz = fmaf((float)m, f.ax.dz_rho, tz0);
         // slices past hi get weight 0 below; skipping their loads saves L1 traffic (CT_FWD3D2_UNPRED = 1: load them)
         const bool in = (INTERIOR || (unsigned)(iz0 + m) < (unsigned)nz) && (CT_FWD3D2_UNPRED || m < 2 || z0 + (float)m < hi);
-        const float v = in ? __ldg(xp + m) : 0.0f;
+        const float v = in ? (CT_FWD3D2_XHINT ? ldg_pol(xp + m, pol) : __ldg(xp + m)) : 0.0f;
         xl[m] = v * sqrt_approx(fmaf(tz, tz, 1.0f));
     }
     // row 2l: [lo, mid] meets slices z0 .. z0 + 2 (lo >= z0, kz < 2)
@@ -389,6 +393,23 @@ __device__ __forceinline__ float fwd_axial_row(const Foot& f, const float* __res
     }
     return A;
 }
+
+// Empty column of the pair-row forward's table (misses the tile, or past the batch): kz = 0 and a
+// walk that reads x[0 .. 4] (CT_FWD3D2_BOTH evaluates both columns of a pair without branches,
+// so that their slice loads issue together; the sums of an empty column are never accumulated).
+// nx ny nz >= 5 whenever an interior column exists (its window has >= 5 slices).
+__device__ __forceinline__ void empty_foot(Foot& f) {
+    f.n = 0;
+    f.rows = 0;
+    f.ax.kz = 0.0f;
+    f.ax.qf = 0.0f;
+    f.ax.qi = 0;
+    f.ax.dz_rho = 0.0f;
+    f.ax.inv_kz = 0.0f;
+}
+#ifndef CT_FWD3D2_BOTH
+#define CT_FWD3D2_BOTH 1   // both columns of a pair evaluated unconditionally (their loads issue together)
+#endif
 
 // Accumulator updates of the pair-row forward: p points at the first channel's row pair.
 #ifndef CT_FWD3D2_ACC4
@@ -462,6 +483,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
     for (int c = 0; c < TCP; c++) Pg[c * LW] = make_float2(0.0f, 0.0f);
     const Wedge w = make_wedge(g, vw.x, vw.y, c0, TC);
     const int nz = g.nz;
+    const unsigned long long xpol = CT_FWD3D2_XHINT ? l2_evict_last() : 0ull;
     // lines: image rows [ya, yb), or every image column trimmed to rows [ya, yb)
     for (int L = (w.rows ? ya : 0) + gi; L < (w.rows ? yb : w.nlines); L += NW) {
         int lo, hi;
@@ -502,7 +524,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                     const int zhi = f.ax.qi + __float2int_rd(fmaf((float)(2 * (LW - 1)), f.ax.kz, f.ax.qf)) + 4;
                     if (zlo >= 0 && zhi <= nz - 1) f.ax.kz = -f.ax.kz;
                 }
-                if (f.n <= 0) f.ax.kz = 0.0f;   // empty column: kz = 0 (the pair dispatch below needs no count test)
+                if (f.n <= 0) empty_foot(f);   // kz = 0: the pair dispatch below needs no count test
                 tab[lane] = f;
             }
             __syncwarp();
@@ -510,8 +532,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
             for (int j0 = 0; j0 < nq; j0 += 2 * H) {
                 const int j = j0 + 2 * hf;   // this stream's two columns
                 Foot f0, f1;
-                if (j < nq) load_foot(&tab[j], f0); else { f0.n = 0; f0.ax.kz = 0.0f; }
-                if (j + 1 < nq) load_foot(&tab[j + 1], f1); else { f1.n = 0; f1.ax.kz = 0.0f; }
+                if (j < nq) load_foot(&tab[j], f0); else empty_foot(f0);
+                if (j + 1 < nq) load_foot(&tab[j + 1], f1); else empty_foot(f1);
                 if (f0.n <= 0 && f1.n <= 0) continue;
                 float2 A0 = make_float2(0.0f, 0.0f), A1 = A0;
                 const float kz0 = fabsf(f0.ax.kz), kz1 = fabsf(f1.ax.kz);
@@ -519,12 +541,18 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                 // interior pair (or a single interior column; empty ones carry kz = 0): no volume predicates
                 const bool inter = f0.ax.kz <= 0.0f && f1.ax.kz <= 0.0f;
 #define CT_FWD3D2_AXIAL(KS_)                                                                   \
-    if (inter) {                                                                               \
-        if (f0.n > 0) A0 = fwd_axial_pair<KS_, true>(f0, x, ll, nz);                           \
-        if (f1.n > 0) A1 = fwd_axial_pair<KS_, true>(f1, x, ll, nz);                           \
+    if (CT_FWD3D2_BOTH && inter) {                                                             \
+        A0 = fwd_axial_pair<KS_, true>(f0, x, ll, nz, xpol);                                   \
+        A1 = fwd_axial_pair<KS_, true>(f1, x, ll, nz, xpol);                                   \
+    } else if (CT_FWD3D2_BOTH) {                                                               \
+        A0 = fwd_axial_pair<KS_, false>(f0, x, ll, nz, xpol);                                  \
+        A1 = fwd_axial_pair<KS_, false>(f1, x, ll, nz, xpol);                                  \
+    } else if (inter) {                                                                        \
+        if (f0.n > 0) A0 = fwd_axial_pair<KS_, true>(f0, x, ll, nz, xpol);                     \
+        if (f1.n > 0) A1 = fwd_axial_pair<KS_, true>(f1, x, ll, nz, xpol);                     \
     } else {                                                                                   \
-        if (f0.n > 0) A0 = fwd_axial_pair<KS_, false>(f0, x, ll, nz);                          \
-        if (f1.n > 0) A1 = fwd_axial_pair<KS_, false>(f1, x, ll, nz);                          \
+        if (f0.n > 0) A0 = fwd_axial_pair<KS_, false>(f0, x, ll, nz, xpol);                    \
+        if (f1.n > 0) A1 = fwd_axial_pair<KS_, false>(f1, x, ll, nz, xpol);                    \
     }
                 if (CT_FWD3D2_KS && kzm <= 0.999f) {
                     CT_FWD3D2_AXIAL(3)
@@ -581,7 +609,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
         for (int q = 0; q < NW * H; q++) s += Pf[(q * TCP + c + CB) * RW + rr];
         const size_t oi = ((size_t)k * g.ns + c0 + c) * g.nt + rr;
         if (addend) s += addend[oi];
-        if (RESID) {
+        if (CT_FWD3D2_XHINT) {   // streamed once: evict first
+            const unsigned long long ef = l2_evict_first();
+            if (RESID) {
+                const size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
+                const float yo = yobs ? ldg_pol(&yobs[gidx], ef) : 0.0f;
+                stg_pol(&out[oi], scale * ldg_pol(&wts[gidx], ef) * (s - yo), ef);
+            } else {
+                stg_pol(&out[oi], s, ef);
+            }
+        } else if (RESID) {
             const size_t gidx = ((size_t)v * g.ns + c0 + c) * g.nt + rr;
             const float yo = yobs ? __ldg(&yobs[gidx]) : 0.0f;
             out[oi] = scale * __ldg(&wts[gidx]) * (s - yo);

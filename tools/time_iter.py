@@ -10,6 +10,14 @@ import torch  # noqa: E402
 from paper_1402_4381_b200 import ctlib  # noqa: E402
 from paper_1402_4381_b200 import inputs as I  # noqa: E402
 
+if os.environ.get("CT_L2_PERSIST_MB"):   # experiment: L2 set-aside for evict_last / persisting accesses
+    import ctypes
+    import glob
+    torch.zeros(1, device="cuda")
+    rt = ctypes.CDLL(sorted(glob.glob(os.path.join(os.path.dirname(torch.__file__), "lib", "libcudart*.so*")) +
+                            glob.glob("/usr/local/cuda/lib64/libcudart.so*"))[0])
+    rc = rt.cudaDeviceSetLimit(6, ctypes.c_size_t(int(os.environ["CT_L2_PERSIST_MB"]) << 20))   # cudaLimitPersistingL2CacheSize
+    print("persisting L2 limit rc", rc, file=sys.stderr)
 name = sys.argv[1] if len(sys.argv) > 1 else "c5"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 cfg = I.config(name)
