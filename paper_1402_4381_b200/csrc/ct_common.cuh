@@ -207,6 +207,17 @@ __device__ __forceinline__ float sqrt_approx(float v) {
     return r;
 }
 
+#ifndef CT_LPOLY
+#define CT_LPOLY 0
+#endif
+// l_theta of the production projectors (fwd3d2 / back3d).  CT_LPOLY: from h = tz / sqrt(2)
+// (the tables carry dz / rho pre-scaled by 1/sqrt(2)), sqrt(1 + tz^2) ~= 1 + h^2, relative error
+// <= tz^4 / 8 -- one FFMA instead of FFMA + MUFU on the slice loads' dependency chain.
+constexpr float kLtScale = CT_LPOLY ? 0.70710678118654752f : 1.0f;
+__device__ __forceinline__ float ltheta_of(float tz) {
+    return CT_LPOLY ? fmaf(tz, tz, 1.0f) : sqrt_approx(fmaf(tz, tz, 1.0f));
+}
+
 __device__ __forceinline__ float ltheta(const Axial& ax, int iz) {
     float tz = ((float)(iz - ax.qi) + 0.5f - ax.qf) * ax.dz_rho;
     return sqrt_approx(fmaf(tz, tz, 1.0f));
@@ -321,6 +332,19 @@ __device__ __forceinline__ void fair_masked(float xj, float xk, float inv_delta,
     omega = __frcp_rn(v);   // correctly rounded: rcp(inf) = +0 as well
 #endif
     dpsi = fmaxf(t, -3.40282347e38f) * omega;
+}
+// Accumulating form: g += psi'(t) = max(t, -FLT_MAX) omega (one FFMA), c += omega.
+__device__ __forceinline__ void fair_masked_acc(float xj, float xk, float inv_delta, float& g, float& c) {
+    const float t = xj - xk;
+    const float v = fmaf(fabsf(t), inv_delta, 1.0f);
+    float omega;
+#if CT_FAIR_RCP_APPROX
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(omega) : "f"(v));
+#else
+    omega = __frcp_rn(v);
+#endif
+    g = fmaf(fmaxf(t, -3.40282347e38f), omega, g);
+    c += omega;
 }
 
 }  // namespace ct

@@ -364,7 +364,7 @@ __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __r
         // slices past hi get weight 0 below; skipping their loads saves L1 traffic (CT_FWD3D2_UNPRED = 1: load them)
         const bool in = (INTERIOR || (unsigned)(iz0 + m) < (unsigned)nz) && (CT_FWD3D2_UNPRED || m < 2 || z0 + (float)m < hi);
         const float v = in ? (CT_FWD3D2_XHINT ? ldg_pol(xp + m, pol) : __ldg(xp + m)) : 0.0f;
-        xl[m] = v * sqrt_approx(fmaf(tz, tz, 1.0f));
+        xl[m] = v * ltheta_of(tz);
     }
     // row 2l: [lo, mid] meets slices z0 .. z0 + 2 (lo >= z0, kz < 2)
     const float a1 = fminf(z0 + 1.0f, mid), a2 = fminf(z0 + 2.0f, mid);
@@ -389,7 +389,7 @@ __device__ __forceinline__ float fwd_axial_row(const Foot& f, const float* __res
     for (int m = m0; m <= m1; m++) {
         const float tz = fmaf((float)m, f.ax.dz_rho, f.ax.inv_kz);
         const float ov = fminf((float)m + 1.0f, hi) - fmaxf((float)m, lo);
-        A = fmaf(__ldg(x + f.rows + m) * sqrt_approx(fmaf(tz, tz, 1.0f)), fmaxf(ov, 0.0f), A);
+        A = fmaf(__ldg(x + f.rows + m) * ltheta_of(tz), fmaxf(ov, 0.0f), A);
     }
     return A;
 }
@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                 for (int j = 0; j < kMaxFoot; j++) f.w[j] *= f.ax.inv_kz;
                 const float qf = f.ax.qf;
                 f.ax.qf = qf - 0.5f * f.ax.kz - g.rbase * f.ax.kz;
+                f.ax.dz_rho *= kLtScale;                   // (ltheta_of)
                 f.ax.inv_kz = (0.5f - qf) * f.ax.dz_rho;   // tzc
                 f.rows = (iy * g.nx + ix) * nz + f.ax.qi;
                 // interior column: the slices of every lane's row pair (up to 5 past floor(lo)) lie
@@ -987,8 +988,8 @@ struct SliceWalk {
         inv_kz = f.ax.inv_kz;
         ubl = g.rbase + 0.5f - (float)r_lo;
         fnr = (float)nr;
-        dz_rho = f.ax.dz_rho;
-        hdz = 0.5f * f.ax.dz_rho;
+        dz_rho = f.ax.dz_rho * kLtScale;   // (ltheta_of)
+        hdz = 0.5f * dz_rho;
         QP = qp;
     }
     // l_theta-weighted integral of the row-wise constant Q over this lane's slice in the pass at
@@ -1002,7 +1003,7 @@ struct SliceWalk {
         const float pf = fmaf(u - (float)k, qp.y, qp.x);
         const float up = __shfl_down_sync(0xffffffffu, pf, 1);
         const float tz = fmaf(zi, dz_rho, hdz);
-        return sqrt_approx(fmaf(tz, tz, 1.0f)) * (up - pf);
+        return ltheta_of(tz) * (up - pf);
     }
     // PF at the slice edge zi (clamped to the view's rows)
     __device__ __forceinline__ float pf_at(float zi) const {
@@ -1028,7 +1029,7 @@ struct SliceWalk {
         for (int e = 0; e < S; e++) {
             const float hi = e + 1 < S ? pf[e + 1] : (lane < 31 ? up : pf[e]);
             const float tz = fmaf(zb + (float)e, dz_rho, hdz);
-            a[e] = fmaf(sqrt_approx(fmaf(tz, tz, 1.0f)), hi - pf[e], a[e]);
+            a[e] = fmaf(ltheta_of(tz), hi - pf[e], a[e]);
         }
     }
 };
@@ -1350,6 +1351,9 @@ __global__ void __launch_bounds__(256) resid_kernel(float* __restrict__ s, const
 // "both voxels in S" pair rule costs no branch (fair_masked) and the stencil needs no
 // bounds checks.  Streams G, g, D_L once and writes x' once (21 B/voxel of HBM).
 constexpr int kK3Y = 8;
+#ifndef CT_K3_CLASS
+#define CT_K3_CLASS 1   // per-distance-class Fair sums in the 26-neighbour K3 (A/B c5 0.689 -> 0.679 ms)
+#endif
 
 template <bool HALO>
 __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const float* __restrict__ x, float* __restrict__ xn,
@@ -1425,6 +1429,26 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                 xn[j] = 0.0f;   // off S
             } else {
                 float gr = 0.0f, cu = 0.0f;
+#if CT_K3_CLASS
+                // per distance class (6 faces, 12 edges, 8 corners) sum t omega and omega, weight
+                // the three class sums at the end: one FFMA and one FADD per neighbour instead of
+                // FMUL + 2 FFMA (the weights are common to a class)
+                float gs3[3] = {0.0f, 0.0f, 0.0f}, cs3[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int oy = -1; oy <= 1; oy++) {
+                    const float* Ps = oy < 0 ? Pp : (oy == 0 ? Pc : Pn);
+#pragma unroll
+                    for (int ox = -1; ox <= 1; ox++)
+#pragma unroll
+                        for (int oz = -1; oz <= 1; oz++) {
+                            if (oy == 0 && ox == 0 && oz == 0) continue;
+                            const int cl = oy * oy + ox * ox + oz * oz - 1;
+                            fair_masked_acc(xj, Ps[own + ox * 34 + oz], inv_delta, gs3[cl], cs3[cl]);   // 0 off S
+                        }
+                }
+                gr = fmaf(r3, gs3[2], fmaf(r2, gs3[1], gs3[0]));
+                cu = fmaf(r3, cs3[2], fmaf(r2, cs3[1], cs3[0]));
+#else
 #pragma unroll
                 for (int oy = -1; oy <= 1; oy++) {
                     const float* Ps = oy < 0 ? Pp : (oy == 0 ? Pc : Pn);
@@ -1441,6 +1465,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                             cu += wgt * om;
                         }
                 }
+#endif
                 const float sdir = rho * __ldg(&G[j]) + (1.0f - rho) * __ldg(&gs[j]);
                 const float den = ra * __ldg(&dl[j]) + 2.0f * beta * cu;
                 xn[j] = fmaxf(xj - __fdividef(sdir + beta * gr, den), 0.0f);
