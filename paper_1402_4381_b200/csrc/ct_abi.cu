@@ -400,6 +400,14 @@ extern "C" int ct_geom_create(const ct_geom_desc* d, ct_geom** out) {
     dg.fpar = dg_fpar;
     dg.fspan = dg_fspan;
     dg.vrel = CT_VREL ? dg_vrel : 0;
+    {
+        // polynomial l_theta (ltheta_of) where every tz = (z - z_s) / rho a fwd3d2 / back3d pair can
+        // weight is small: |z - z_s| <= (row extent) rho / dsd + one slice, rho >= dso - rmax
+        const double rb = (nt - 1) / 2.0 + (is2d ? 0.0 : d->offt);
+        const double rowmax = std::max(fabs(-0.5 - rb), fabs(nt - 0.5 - rb));
+        const double tzmax = is2d ? 1.0 : rowmax * d->dt / d->dsd + d->dz / (d->dso - rmax);
+        dg.lpoly = (CT_LPOLY && CT_FWD3D_PAIR && !is2d && nt <= 64 && tzmax <= (double)kLpolyTzMax) ? 1 : 0;
+    }
     gd.vz = g->d_vz;
     *out = g;
     return CT_OK;
@@ -453,37 +461,43 @@ static cudaError_t launch_fwd3d(const DevGeom& dg, dim3 grid, ct_views v, const 
     return cudaSuccess;
 }
 
-template <int TC, int NW, int H, bool RESID, int MINB>
+template <int TC, int NW, int H, bool RESID, int MINB, bool LP>
 static cudaError_t launch_fwd3d2(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
                                  const float* w, float scale, const int2* ext, cudaStream_t st, float* part) {
     constexpr size_t smem = fwd3d2_smem<TC, NW>();
-    cudaError_t e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, false, MINB>, smem);
-    if (e == cudaSuccess) e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, RESID, MINB>, smem);
+    cudaError_t e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, false, MINB, LP>, smem);
+    if (e == cudaSuccess) e = ensure_dyn_smem((const void*)fwd3d2_kernel<TC, NW, H, RESID, MINB, LP>, smem);
     if (e != cudaSuccess) return e;
     dim3 grid((dg.ns + TC - 1) / TC, v.count);
     if (part) {   // y-split: rows [0, ny/2) into `part`, then rows [ny/2, ny) + part through the epilogue
         const int yh = dg.ny / 2;
-        fwd3d2_kernel<TC, NW, H, false, MINB><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, part, nullptr,
+        fwd3d2_kernel<TC, NW, H, false, MINB, LP><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, part, nullptr,
                                                                           nullptr, 1.0f, ext, 0, yh, nullptr);
-        fwd3d2_kernel<TC, NW, H, RESID, MINB><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale,
+        fwd3d2_kernel<TC, NW, H, RESID, MINB, LP><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale,
                                                                           ext, yh, dg.ny, part);
         g_launches += 1;
     } else {
-        fwd3d2_kernel<TC, NW, H, RESID, MINB><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale,
+        fwd3d2_kernel<TC, NW, H, RESID, MINB, LP><<<grid, NW * 32, smem, st>>>(dg, v.first, v.stride, x, out, yobs, w, scale,
                                                                           ext, 0, dg.ny, nullptr);
     }
     return cudaSuccess;
 }
 
 // Pair-row forward (nt <= 64): tile width and resident CTAs per SM by scan kind (A/B, c3-c5)
+template <int H, bool RESID, bool LP>
+static cudaError_t launch_fwd3d2_kind(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
+                                      const float* w, float scale, const int2* ext, cudaStream_t st, float* part) {
+    if (dg.kind == CT_CONE_HELICAL)
+        return launch_fwd3d2<CT_FWD3D2_TC_HEL, CT_FWD3D2_NW_HEL, H, RESID, CT_FWD3D2_MINB_HEL, LP>(dg, v, x, out, yobs,
+                                                                                                w, scale, ext, st, part);
+    return launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB, LP>(dg, v, x, out, yobs, w, scale, ext,
+                                                                                    st, part);
+}
 template <int H, bool RESID>
 static cudaError_t launch_fwd3d2_sel(const DevGeom& dg, ct_views v, const float* x, float* out, const float* yobs,
                                      const float* w, float scale, const int2* ext, cudaStream_t st, float* part) {
-    if (dg.kind == CT_CONE_HELICAL)
-        return launch_fwd3d2<CT_FWD3D2_TC_HEL, CT_FWD3D2_NW_HEL, H, RESID, CT_FWD3D2_MINB_HEL>(dg, v, x, out, yobs, w,
-                                                                                            scale, ext, st, part);
-    return launch_fwd3d2<CT_FWD3D2_TC, CT_FWD3D2_NW, H, RESID, CT_FWD3D2_MINB>(dg, v, x, out, yobs, w, scale, ext, st,
-                                                                                part);
+    if (dg.lpoly) return launch_fwd3d2_kind<H, RESID, true>(dg, v, x, out, yobs, w, scale, ext, st, part);
+    return launch_fwd3d2_kind<H, RESID, false>(dg, v, x, out, yobs, w, scale, ext, st, part);
 }
 
 // Per-call forward-projection scratch (owned by the caller of launch_fwd, so concurrent
@@ -583,16 +597,18 @@ static int launch_back(const ct_geom* g, ct_views v, const float* y, float* x, c
             CT_CUDA(launch_pdl(back2d_kernel<EPI, false>, grid, dim3(256), 0, st, dg, v.first, v.stride, v.count, y, x, ga));
     else {
         const size_t smem = back3d_smem_fixed() + sizeof(float) * 8 * ((size_t)dg.nz + kBackPad);
-        if (dg.nt == 64) {
-            CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 64>, smem));
-            back3d_kernel<EPI, 64><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga, row0, row1);
-        } else if (dg.nt == 32) {
-            CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 32>, smem));
-            back3d_kernel<EPI, 32><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga, row0, row1);
-        } else {
-            CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, 0>, smem));
-            back3d_kernel<EPI, 0><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga, row0, row1);
-        }
+#define CT_B3_LAUNCH(NTM_, LP_)                                                                               \
+    {                                                                                                        \
+        CT_CUDA(ensure_dyn_smem((const void*)back3d_kernel<EPI, NTM_, LP_>, smem));                          \
+        back3d_kernel<EPI, NTM_, LP_><<<grid, 256, smem, st>>>(dg, v.first, v.stride, v.count, y, x, ga, row0, row1); \
+    }
+        if (dg.nt == 64 && dg.lpoly) CT_B3_LAUNCH(64, true)
+        else if (dg.nt == 64) CT_B3_LAUNCH(64, false)
+        else if (dg.nt == 32 && dg.lpoly) CT_B3_LAUNCH(32, true)
+        else if (dg.nt == 32) CT_B3_LAUNCH(32, false)
+        else if (dg.lpoly) CT_B3_LAUNCH(0, true)
+        else CT_B3_LAUNCH(0, false)
+#undef CT_B3_LAUNCH
     }
     CT_LAUNCHED(1);
     return CT_OK;

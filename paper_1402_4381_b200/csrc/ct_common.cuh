@@ -52,6 +52,7 @@ struct DevGeom {
     float zhalf;              // bound on |z - z_s| of any voxel a view can see (mm)
     int fpar, fspan;          // fan 2D forward: lane-parity buffers P and tile channel-span bound
     int vrel;                 // fan 2D: vertex positions relative to a per-block reference ray (1) or absolute (0)
+    int lpoly;                // cone, nt <= 64: polynomial l_theta in fwd3d2 / back3d (ltheta_of)
     const float4* views;      // per view: (sin beta, cos beta, qi, qf) with
                               // (z_s - zb0)/dz = qi + qf, qi integer (exact in fp32)
 };
@@ -208,14 +209,18 @@ __device__ __forceinline__ float sqrt_approx(float v) {
 }
 
 #ifndef CT_LPOLY
-#define CT_LPOLY 0
+#define CT_LPOLY 1   // 0: never use the polynomial l_theta (ct_geom_create leaves DevGeom::lpoly = 0)
 #endif
-// l_theta of the production projectors (fwd3d2 / back3d).  CT_LPOLY: from h = tz / sqrt(2)
-// (the tables carry dz / rho pre-scaled by 1/sqrt(2)), sqrt(1 + tz^2) ~= 1 + h^2, relative error
-// <= tz^4 / 8 -- one FFMA instead of FFMA + MUFU on the slice loads' dependency chain.
-constexpr float kLtScale = CT_LPOLY ? 0.70710678118654752f : 1.0f;
+// l_theta of the production projectors (fwd3d2 / back3d).  LP (DevGeom::lpoly, set at create when
+// every tz a projector can meet satisfies |tz| <= kLpolyTzMax): the tables carry dz / rho
+// pre-scaled by 1/sqrt(2), so h = tz / sqrt(2) and sqrt(1 + tz^2) ~= 1 + h^2 with relative error
+// <= tz^4 / 8 <= 5.2e-6 -- one FFMA instead of FFMA + MUFU on the slice loads' dependency chain.
+constexpr float kLpolyTzMax = 0.08f;
+template <bool LP>
+__host__ __device__ constexpr float lt_scale() { return LP ? 0.70710678118654752f : 1.0f; }
+template <bool LP>
 __device__ __forceinline__ float ltheta_of(float tz) {
-    return CT_LPOLY ? fmaf(tz, tz, 1.0f) : sqrt_approx(fmaf(tz, tz, 1.0f));
+    return LP ? fmaf(tz, tz, 1.0f) : sqrt_approx(fmaf(tz, tz, 1.0f));
 }
 
 __device__ __forceinline__ float ltheta(const Axial& ax, int iz) {

@@ -346,7 +346,7 @@ constexpr size_t fwd3d_smem() {
 #ifndef CT_FWD3D2_XHINT
 #define CT_FWD3D2_XHINT 0   // 1: x slice loads carry an L2 evict_last policy, the epilogue's y / W / out evict_first
 #endif
-template <int KS, bool INTERIOR>
+template <int KS, bool INTERIOR, bool LP>
 __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __restrict__ x, int l, int nz,
                                                  unsigned long long pol = 0) {
     const float kz = fabsf(f.ax.kz);
@@ -364,7 +364,7 @@ __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __r
         // slices past hi get weight 0 below; skipping their loads saves L1 traffic (CT_FWD3D2_UNPRED = 1: load them)
         const bool in = (INTERIOR || (unsigned)(iz0 + m) < (unsigned)nz) && (CT_FWD3D2_UNPRED || m < 2 || z0 + (float)m < hi);
         const float v = in ? (CT_FWD3D2_XHINT ? ldg_pol(xp + m, pol) : __ldg(xp + m)) : 0.0f;
-        xl[m] = v * ltheta_of(tz);
+        xl[m] = v * ltheta_of<LP>(tz);
     }
     // row 2l: [lo, mid] meets slices z0 .. z0 + 2 (lo >= z0, kz < 2)
     const float a1 = fminf(z0 + 1.0f, mid), a2 = fminf(z0 + 2.0f, mid);
@@ -383,13 +383,14 @@ __device__ __forceinline__ float2 fwd_axial_pair(const Foot& f, const float* __r
 }
 
 // General form (kz >= 2, rarely: very fine slices): one row [lo, hi].
+template <bool LP>
 __device__ __forceinline__ float fwd_axial_row(const Foot& f, const float* __restrict__ x, float lo, float hi, int nz) {
     float A = 0.0f;
     const int m0 = max(__float2int_rd(lo), -f.ax.qi), m1 = min(__float2int_rd(hi), nz - 1 - f.ax.qi);
     for (int m = m0; m <= m1; m++) {
         const float tz = fmaf((float)m, f.ax.dz_rho, f.ax.inv_kz);
         const float ov = fminf((float)m + 1.0f, hi) - fmaxf((float)m, lo);
-        A = fmaf(__ldg(x + f.rows + m) * ltheta_of(tz), fmaxf(ov, 0.0f), A);
+        A = fmaf(__ldg(x + f.rows + m) * ltheta_of<LP>(tz), fmaxf(ov, 0.0f), A);
     }
     return A;
 }
@@ -454,7 +455,7 @@ __device__ __forceinline__ void acc_pair(float2* p, const Foot& f0, float2 A0, c
     }
 }
 
-template <int TC, int NW, int H, bool RESID, int MINB>
+template <int TC, int NW, int H, bool RESID, int MINB, bool LP>
 // [ya, yb): the image rows (iy) this launch projects (the y-split forward projects the two
 // halves in two launches so that each launch's working set of x is half a view's slice
 // window; `addend` (nullable) holds the first half's sums, added before the epilogue).
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                 for (int j = 0; j < kMaxFoot; j++) f.w[j] *= f.ax.inv_kz;
                 const float qf = f.ax.qf;
                 f.ax.qf = qf - 0.5f * f.ax.kz - g.rbase * f.ax.kz;
-                f.ax.dz_rho *= kLtScale;                   // (ltheta_of)
+                f.ax.dz_rho *= lt_scale<LP>();             // (ltheta_of)
                 f.ax.inv_kz = (0.5f - qf) * f.ax.dz_rho;   // tzc
                 f.rows = (iy * g.nx + ix) * nz + f.ax.qi;
                 // interior column: the slices of every lane's row pair (up to 5 past floor(lo)) lie
@@ -543,17 +544,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                 const bool inter = f0.ax.kz <= 0.0f && f1.ax.kz <= 0.0f;
 #define CT_FWD3D2_AXIAL(KS_)                                                                   \
     if (CT_FWD3D2_BOTH && inter) {                                                             \
-        A0 = fwd_axial_pair<KS_, true>(f0, x, ll, nz, xpol);                                   \
-        A1 = fwd_axial_pair<KS_, true>(f1, x, ll, nz, xpol);                                   \
+        A0 = fwd_axial_pair<KS_, true, LP>(f0, x, ll, nz, xpol);                                   \
+        A1 = fwd_axial_pair<KS_, true, LP>(f1, x, ll, nz, xpol);                                   \
     } else if (CT_FWD3D2_BOTH) {                                                               \
-        A0 = fwd_axial_pair<KS_, false>(f0, x, ll, nz, xpol);                                  \
-        A1 = fwd_axial_pair<KS_, false>(f1, x, ll, nz, xpol);                                  \
+        A0 = fwd_axial_pair<KS_, false, LP>(f0, x, ll, nz, xpol);                                  \
+        A1 = fwd_axial_pair<KS_, false, LP>(f1, x, ll, nz, xpol);                                  \
     } else if (inter) {                                                                        \
-        if (f0.n > 0) A0 = fwd_axial_pair<KS_, true>(f0, x, ll, nz, xpol);                     \
-        if (f1.n > 0) A1 = fwd_axial_pair<KS_, true>(f1, x, ll, nz, xpol);                     \
+        if (f0.n > 0) A0 = fwd_axial_pair<KS_, true, LP>(f0, x, ll, nz, xpol);                     \
+        if (f1.n > 0) A1 = fwd_axial_pair<KS_, true, LP>(f1, x, ll, nz, xpol);                     \
     } else {                                                                                   \
-        if (f0.n > 0) A0 = fwd_axial_pair<KS_, false>(f0, x, ll, nz, xpol);                    \
-        if (f1.n > 0) A1 = fwd_axial_pair<KS_, false>(f1, x, ll, nz, xpol);                    \
+        if (f0.n > 0) A0 = fwd_axial_pair<KS_, false, LP>(f0, x, ll, nz, xpol);                    \
+        if (f1.n > 0) A1 = fwd_axial_pair<KS_, false, LP>(f1, x, ll, nz, xpol);                    \
     }
                 if (CT_FWD3D2_KS && kzm <= 0.999f) {
                     CT_FWD3D2_AXIAL(3)
@@ -564,13 +565,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) fwd3d2_kernel(DevGeom g, int fi
                 } else {
                     if (f0.n > 0) {
                         const float l0 = fmaf((float)(2 * ll), kz0, f0.ax.qf);
-                        A0 = make_float2(fwd_axial_row(f0, x, l0, l0 + kz0, nz),
-                                         fwd_axial_row(f0, x, l0 + kz0, l0 + 2.0f * kz0, nz));
+                        A0 = make_float2(fwd_axial_row<LP>(f0, x, l0, l0 + kz0, nz),
+                                         fwd_axial_row<LP>(f0, x, l0 + kz0, l0 + 2.0f * kz0, nz));
                     }
                     if (f1.n > 0) {
                         const float l1 = fmaf((float)(2 * ll), kz1, f1.ax.qf);
-                        A1 = make_float2(fwd_axial_row(f1, x, l1, l1 + kz1, nz),
-                                         fwd_axial_row(f1, x, l1 + kz1, l1 + 2.0f * kz1, nz));
+                        A1 = make_float2(fwd_axial_row<LP>(f1, x, l1, l1 + kz1, nz),
+                                         fwd_axial_row<LP>(f1, x, l1 + kz1, l1 + 2.0f * kz1, nz));
                     }
                 }
 #undef CT_FWD3D2_AXIAL
@@ -975,6 +976,7 @@ __device__ __forceinline__ void back3d_qp64(float q0, float q1, int lane, float2
 
 // Per-view constants of the slice walk (step (2)): the slice edge zi (voxel units relative to
 // the view's qi, minus qf) maps to the detector-row coordinate u = zi inv_kz + ubl in [0, nr].
+template <bool LP>
 struct SliceWalk {
     float zbase;     // edge of the walk's first slice z0 (voxel units relative to qi, minus qf)
     float zl;        // this lane's edge in pass 0 of a walk starting at slice z0
@@ -988,7 +990,7 @@ struct SliceWalk {
         inv_kz = f.ax.inv_kz;
         ubl = g.rbase + 0.5f - (float)r_lo;
         fnr = (float)nr;
-        dz_rho = f.ax.dz_rho * kLtScale;   // (ltheta_of)
+        dz_rho = f.ax.dz_rho * lt_scale<LP>();   // (ltheta_of)
         hdz = 0.5f * dz_rho;
         QP = qp;
     }
@@ -1003,7 +1005,7 @@ struct SliceWalk {
         const float pf = fmaf(u - (float)k, qp.y, qp.x);
         const float up = __shfl_down_sync(0xffffffffu, pf, 1);
         const float tz = fmaf(zi, dz_rho, hdz);
-        return ltheta_of(tz) * (up - pf);
+        return ltheta_of<LP>(tz) * (up - pf);
     }
     // PF at the slice edge zi (clamped to the view's rows)
     __device__ __forceinline__ float pf_at(float zi) const {
@@ -1029,7 +1031,7 @@ struct SliceWalk {
         for (int e = 0; e < S; e++) {
             const float hi = e + 1 < S ? pf[e + 1] : (lane < 31 ? up : pf[e]);
             const float tz = fmaf(zb + (float)e, dz_rho, hdz);
-            a[e] = fmaf(ltheta_of(tz), hi - pf[e], a[e]);
+            a[e] = fmaf(ltheta_of<LP>(tz), hi - pf[e], a[e]);
         }
     }
 };
@@ -1040,7 +1042,7 @@ struct SliceWalk {
 
 // NTM: detector-row specialisation, 64 or 32 (every row in one pass, nt a compile-time
 // constant) or 0 (general nt: the rows the active slices meet).
-template <int EPI, int NTM>
+template <int EPI, int NTM, bool LP>
 // Image rows [row0, row1) (the multi-rank band exchange back-projects one destination row slab
 // per launch so that each slab's blocks travel while the next slab is computed).
 __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, int first, int stride, int count,
@@ -1157,7 +1159,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                         load_foot(&tab[j + v2], fw);
                         if (fw.n <= 0) continue;
                         const int z0 = fw.rows & 0xffff, nzs = fw.rows >> 16;
-                        SliceWalk w1;
+                        SliceWalk<LP> w1;
                         w1.init(fw, g, z0, flane, 0, NTM, QPA + v2 * QS);
                         if (CT_BACK3D_BLOCKED && nzs > 31 && nzs <= 63) w1.walk_blocked<2>(acc + z0, lane, flane);
                         else if (CT_BACK3D_BLOCKED && nzs > 63 && nzs <= 95) w1.walk_blocked<3>(acc + z0, lane, flane);
@@ -1209,7 +1211,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 const int zaB = fb.rows & 0xffff, zeB = zaB + (fb.rows >> 16);
                 const int z0 = va ? (vbv ? min(zaA, zaB) : zaA) : zaB;
                 const int nzs = (va ? (vbv ? max(zeA, zeB) : zeA) : zeB) - z0;
-                SliceWalk wa, wb;
+                SliceWalk<LP> wa, wb;
                 if (va) wa.init(fa, g, z0, flane, rla, nra, QPA);
                 if (vbv) wb.init(fb, g, z0, flane, rlb, nrb, QPB);
                 float* accl = acc + z0 + lane;
@@ -1233,7 +1235,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                         accl[s0] += c;
                     }
                 } else {
-                    const SliceWalk& w1 = va ? wa : wb;
+                    const SliceWalk<LP>& w1 = va ? wa : wb;
                     // one blocked pass covers 32 S - 1 slices (tail lanes clamp to 0 or land in the
                     // padding: z0 + 32 S - 1 <= nz + kBackPad - 1 since nzs >= 32 (S - 1))
                     if (CT_BACK3D_BLOCKED && nzs > 31 && nzs <= 63) w1.walk_blocked<2>(acc + z0, lane, flane);

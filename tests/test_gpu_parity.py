@@ -70,7 +70,29 @@ def geoms_small():
                                  dt=1.0964, na=20, offz=0.3, offt=0.4)
     gs["helical_fine_kz"] = GU.geom("cone_helical", nx=10, nz=40, dx=0.9766, dz=0.25, ns=21, ds=1.0239, nt=36,
                                     dt=1.0964, na=30, turns=2.0, pitch=0.7, start=5.0)
+    # steep cones (|tz| > 0.08): the exact-sqrt l_theta instances of fwd3d2 / back3d (every
+    # geometry above takes the polynomial form)
+    gs["axial_steep"] = GU.geom("cone_axial", nx=12, nz=10, dx=2.0, dz=2.0, ns=30, ds=4.0, nt=40, dt=4.0, na=24,
+                                dso=250.0, dsd=400.0)
+    gs["helical_steep"] = GU.geom("cone_helical", nx=10, nz=16, dx=2.0, dz=2.0, ns=30, ds=4.0, nt=34, dt=4.0, na=40,
+                                  dso=250.0, dsd=400.0, turns=2.0, pitch=0.6, start=9.0)
     return gs
+
+
+def lpoly_tz_bound(g):
+    """The |tz| bound ct_geom_create gates the polynomial l_theta on (restated, not imported)."""
+    rb = (g["nt"] - 1) / 2.0 + g["offt"]
+    rowmax = max(abs(-0.5 - rb), abs(g["nt"] - 0.5 - rb))
+    rmax = math.hypot(0.5 * (g["nx"] - 1) * g["dx"] + abs(g["offx"]) + g["dx"],
+                      0.5 * (g["ny"] - 1) * g["dy"] + abs(g["offy"]) + g["dy"])
+    return rowmax * g["dt"] / g["dsd"] + g["dz"] / (g["dso"] - rmax)
+
+
+def test_steep_geometries_take_the_exact_ltheta():
+    gs = geoms_small()
+    assert lpoly_tz_bound(gs["axial_steep"]) > 0.08 and lpoly_tz_bound(gs["helical_steep"]) > 0.08
+    for k in ("axial_c3", "helical_c5", "axial_rows41", "helical_fine_kz"):
+        assert lpoly_tz_bound(gs[k]) <= 0.08, k
 
 
 def rand_image(g, seed, shape_abi):
@@ -96,7 +118,7 @@ def test_fwd_back_small(ct, O, name):
         assert rel_l2(I.to_oracle_image(bg), bo, f"back {name} {views}") <= 1e-4, name
 
 
-@pytest.mark.parametrize("name", ["fan_c2", "axial_c3", "helical_c5"])
+@pytest.mark.parametrize("name", ["fan_c2", "axial_c3", "helical_c5", "axial_steep", "helical_steep"])
 def test_adjoint_gpu(ct, name):
     g = geoms_small()[name]
     geo = ct.Geometry(g)
