@@ -1353,6 +1353,9 @@ __global__ void __launch_bounds__(256) resid_kernel(float* __restrict__ s, const
 // "both voxels in S" pair rule costs no branch (fair_masked) and the stencil needs no
 // bounds checks.  Streams G, g, D_L once and writes x' once (21 B/voxel of HBM).
 constexpr int kK3Y = 8;
+#ifndef CT_K3_PIPE
+#define CT_K3_PIPE 0   // 1: software-pipelined planes (4 rotating buffers, one barrier per step; A/B c5 0.670 -> 0.683 ms, off)
+#endif
 #ifndef CT_K3_CLASS
 #define CT_K3_CLASS 1   // per-distance-class Fair sums in the 26-neighbour K3 (A/B c5 0.689 -> 0.679 ms)
 #endif
@@ -1366,7 +1369,7 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                                                           int iy_begin, int iy_end, ZHalo hz) {
     // updates rows [iy_begin, iy_end) (multi-rank: this rank's slab; x is the full image).
     // HALO (z-slab ranks): hz holds the neighbours' boundary slices (z = -1, z = nz) and their mask.
-    __shared__ float Pl[3][10][34];
+    __shared__ float Pl[CT_K3_PIPE ? 4 : 3][10][34];
     const int tz = threadIdx.x & 31, tx = threadIdx.x >> 5;
     const int ix0 = blockIdx.x * 8, z0 = blockIdx.y * 32, iy0 = iy_begin + blockIdx.z * kK3Y;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
@@ -1390,17 +1393,31 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
         ph[q] = !HALO || !inx ? 0 : (ez == -1 ? 1 : (ez == nz ? 2 : 0));   // halo slice below / above
     }
     const bool two = threadIdx.x + 256 < 340;   // warp-uniform except in one warp
-    auto load_plane = [&](float* P, int iy) {
+    // a plane's elements in two phases: fetch (global loads into registers) and store (the
+    // S / grid selection, the z-slab halo, the shared-memory store), so that a plane's loads
+    // can be in flight while the previous planes' stencils are computed
+    struct PlaneRaw {
+        float xv[2];
+        uint8_t mm[2];
+    };
+    auto fetch_plane = [&](int iy, PlaneRaw& r) {
         const bool rowok = iy >= 0 && iy < ny;
         const int rb = rowok ? iy * nx * nz : 0;
 #pragma unroll
         for (int q = 0; q < 2; q++) {
             if (q == 1 && !two) break;
+            const int j = rowok && pin[q] ? rb + pj[q] : 0;
+            r.mm[q] = __ldg(&m[j]);
+            r.xv[q] = __ldg(&x[j]);
+        }
+    };
+    auto store_plane = [&](float* P, int iy, const PlaneRaw& r) {
+        const bool rowok = iy >= 0 && iy < ny;
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            if (q == 1 && !two) break;
             const bool ok = rowok && pin[q];
-            const int j = ok ? rb + pj[q] : 0;
-            const uint8_t mm = __ldg(&m[j]);
-            const float xv = __ldg(&x[j]);
-            float v = ok && mm ? xv : __uint_as_float(kOffS);   // not in S
+            float v = ok && r.mm[q] ? r.xv[q] : __uint_as_float(kOffS);   // not in S
             if (HALO && rowok && ph[q]) {
                 const int c = iy * nx + pc[q];
                 if (ph[q] == 1 && hz.lo && hz.mlo[c]) v = hz.lo[c];
@@ -1409,12 +1426,25 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
             P[pe[q]] = v;
         }
     };
+    auto load_plane = [&](float* P, int iy) {
+        PlaneRaw r;
+        fetch_plane(iy, r);
+        store_plane(P, iy, r);
+    };
     // rotating planes iy - 1, iy, iy + 1 (pointer rotation instead of slot arithmetic)
     float* Pp = &Pl[0][0][0];
     float* Pc = &Pl[1][0][0];
     float* Pn = &Pl[2][0][0];
+#if CT_K3_PIPE
+    float* Pf = &Pl[3][0][0];   // plane iy + 2, written during step iy
     load_plane(Pp, iy0 - 1);
     load_plane(Pc, iy0);
+    load_plane(Pn, iy0 + 1);
+    __syncthreads();
+#else
+    load_plane(Pp, iy0 - 1);
+    load_plane(Pc, iy0);
+#endif
     const int ix = ix0 + tx, iz = z0 + tz;
     const bool inb = ix < nx && iz < nz;
     constexpr float r2 = 0.70710678118654752f, r3 = 0.57735026918962576f;
@@ -1422,14 +1452,23 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
     for (int t = 0; t < kK3Y; t++) {
         const int iy = iy0 + t;
         if (iy >= iy_end) break;
+#if CT_K3_PIPE
+        // one barrier per step: plane iy + 2 is fetched now and stored after the stencil into the
+        // buffer plane iy - 2 occupied (read in step iy - 1, before the last barrier)
+        const bool more = t + 1 < kK3Y && iy + 1 < iy_end;   // CTA-uniform
+        PlaneRaw nxt;
+        if (more) fetch_plane(iy + 2, nxt);
+#else
         load_plane(Pn, iy + 1);
         __syncthreads();
+#endif
         if (inb) {
             const int j = (iy * nx + ix) * nz + iz;
             const float xj = Pc[own];
             if (xj == __uint_as_float(kOffS)) {
                 xn[j] = 0.0f;   // off S
             } else {
+                const float Gj = __ldg(&G[j]), gsj = __ldg(&gs[j]), dlj = __ldg(&dl[j]);   // (in flight during the stencil)
                 float gr = 0.0f, cu = 0.0f;
 #if CT_K3_CLASS
                 // per distance class (6 faces, 12 edges, 8 corners) sum t omega and omega, weight
@@ -1468,16 +1507,26 @@ __global__ void __launch_bounds__(256) sqs_update3d_kernel(DevGeom g, const floa
                         }
                 }
 #endif
-                const float sdir = rho * __ldg(&G[j]) + (1.0f - rho) * __ldg(&gs[j]);
-                const float den = ra * __ldg(&dl[j]) + 2.0f * beta * cu;
+                const float sdir = rho * Gj + (1.0f - rho) * gsj;
+                const float den = ra * dlj + 2.0f * beta * cu;
                 xn[j] = fmaxf(xj - __fdividef(sdir + beta * gr, den), 0.0f);
             }
         }
+#if CT_K3_PIPE
+        if (more) store_plane(Pf, iy + 2, nxt);
+        __syncthreads();
+        float* tp = Pp;   // iy + 1 becomes the centre plane, iy + 2 the next one
+        Pp = Pc;
+        Pc = Pn;
+        Pn = Pf;
+        Pf = tp;
+#else
         __syncthreads();
         float* tp = Pp;   // iy + 1 becomes the centre plane
         Pp = Pc;
         Pc = Pn;
         Pn = tp;
+#endif
     }
 }
 
