@@ -11,6 +11,7 @@
 // deterministic run to run.  See DESIGN.md §Kernels for the tiling and rooflines.
 #pragma once
 #include "ct_common.cuh"
+#include <type_traits>
 
 namespace ct {
 
@@ -1034,8 +1035,33 @@ struct SliceWalk {
             a[e] = fmaf(ltheta_of<LP>(tz), hi - pf[e], a[e]);
         }
     }
+    // The same pass accumulating into registers (a[e]: slice S lane + e of the walk), for a
+    // group of views that share the walk origin (CT_BACK3D_GROUP).
+    template <int S>
+    __device__ __forceinline__ void walk_reg(float* a, int lane, float flane) const {
+        const float zb = fmaf((float)S, flane, zbase);
+        float pf[S];
+#pragma unroll
+        for (int e = 0; e < S; e++) pf[e] = pf_at(zb + (float)e);
+        const float up = __shfl_down_sync(0xffffffffu, pf[0], 1);
+#pragma unroll
+        for (int e = 0; e < S; e++) {
+            const float hi = e + 1 < S ? pf[e + 1] : (lane < 31 ? up : pf[e]);
+            const float tz = fmaf(zb + (float)e, dz_rho, hdz);
+            a[e] = fmaf(ltheta_of<LP>(tz), hi - pf[e], a[e]);
+        }
+    }
 };
 
+#ifndef CT_BACK3D_GROUP
+// views per register-accumulated group (power of two <= 32; 0: off): the group's views walk the
+// union of their slice windows from one origin, a lane's S slices accumulate in registers and
+// reach the shared-memory accumulator once per group instead of once per view
+#define CT_BACK3D_GROUP 8
+#endif
+#ifndef CT_BACK3D_GROUP_SMEM
+#define CT_BACK3D_GROUP_SMEM 1   // the group unions live in the table (0: in registers across the batch; spills)
+#endif
 #ifndef CT_BACK3D_BLOCKED
 #define CT_BACK3D_BLOCKED 1   // one blocked pass (S = 2..4 slices per lane) for windows of 32..127 slices (A/B: c5 11.31 -> 10.88, c3 1.75 -> 1.69 ms)
 #endif
@@ -1078,6 +1104,7 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
         const float xc = g.x0 + ix * g.dx, yc = g.y0 + iy * g.dy;
         for (int vb = 0; vb < count; vb += 32) {
             const int kk = vb + lane;
+            int gz0 = 0x7fffffff, gz1 = -1;   // this view's active slices [gz0, gz1) (empty: none)
             if (kk < count) {
                 Foot f;
                 column_footprint(g, g.views[first + kk * stride], xc, yc, f);
@@ -1088,8 +1115,23 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 const int zb = min(__float2int_rd(qb) + f.ax.qi, nz - 1);
                 if (!(f.n > 0 && zb >= za)) f.n = 0;
                 f.rows = za | ((zb - za + 1) << 16);
+                if (f.n > 0) {
+                    gz0 = za;
+                    gz1 = zb + 1;
+                }
                 tab[lane] = f;
             }
+#if CT_BACK3D_GROUP
+            // union of the slice windows of each group of CT_BACK3D_GROUP consecutive views, kept in
+            // the group's first record (its ax.kz field, unused after this phase: origin | count << 16)
+#pragma unroll
+            for (int o = 1; o < CT_BACK3D_GROUP; o <<= 1) {
+                gz0 = min(gz0, __shfl_xor_sync(0xffffffffu, gz0, o));
+                gz1 = max(gz1, __shfl_xor_sync(0xffffffffu, gz1, o));
+            }
+            if (CT_BACK3D_GROUP_SMEM && (lane & (CT_BACK3D_GROUP - 1)) == 0 && kk < count)
+                tab[lane].ax.kz = __int_as_float(gz1 > gz0 ? gz0 | ((gz1 - gz0) << 16) : 0);
+#endif
             __syncwarp();
             const int nb = min(32, count - vb);
             const float* yb = y + (size_t)vb * ns * nt;   // this batch's views
@@ -1171,6 +1213,67 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                             for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) accl[s0] += w1.contrib(sf);
                         }
                         __syncwarp();
+                    }
+                }
+                continue;
+            }
+#endif
+#if CT_BACK3D_GROUP
+            if (NQ == 1) {
+                for (int g0 = 0; g0 < nb; g0 += CT_BACK3D_GROUP) {
+                    const int g1 = min(g0 + CT_BACK3D_GROUP, nb);
+#if CT_BACK3D_GROUP_SMEM
+                    const int un = __float_as_int(tab[g0].ax.kz);
+                    const int uz0 = un & 0xffff, nzu = un >> 16;
+#else
+                    const int uz0 = __shfl_sync(0xffffffffu, gz0, g0), nzu = __shfl_sync(0xffffffffu, gz1, g0) - uz0;
+#endif
+                    if (nzu <= 0) continue;   // no view of the group meets the column
+                    // the group's views walk [uz0, uz0 + 32 S - 1) (slices outside a view's own window
+                    // clamp to the same u: exactly 0); a lane's S slices accumulate in registers
+                    auto group = [&](auto SC) {
+                        constexpr int S = decltype(SC)::value;
+                        float a[S];
+#pragma unroll
+                        for (int e = 0; e < S; e++) a[e] = 0.0f;
+                        for (int j = g0; j < g1; j++) {
+                            Foot fa;
+                            load_foot(&tab[j], fa);
+                            if (fa.n <= 0) continue;
+                            int rla = 0, nra = 0;
+                            back3d_rows<NTM>(g, fa, yb + (j * ns + fa.cA) * nt, lane, QPA, rla, nra);
+                            __syncwarp();
+                            SliceWalk<LP> w;
+                            w.init(fa, g, uz0, flane, rla, nra, QPA);
+                            w.template walk_reg<S>(a, lane, flane);
+                            __syncwarp();
+                        }
+                        float* p = acc + uz0 + S * lane;   // < uz0 + 32 S <= nz + kBackPad
+#pragma unroll
+                        for (int e = 0; e < S; e++) p[e] += a[e];
+                    };
+                    if (nzu <= 31) group(std::integral_constant<int, 1>());
+                    else if (nzu <= 63) group(std::integral_constant<int, 2>());
+                    else if (nzu <= 95) group(std::integral_constant<int, 3>());
+                    else if (nzu <= 127) group(std::integral_constant<int, 4>());
+                    else {
+                        // windows wider than one 4-slice blocked pass: per view, passes of 31 slices
+                        for (int j = g0; j < g1; j++) {
+                            Foot fa;
+                            load_foot(&tab[j], fa);
+                            if (fa.n <= 0) continue;
+                            int rla = 0, nra = 0;
+                            back3d_rows<NTM>(g, fa, yb + (j * ns + fa.cA) * nt, lane, QPA, rla, nra);
+                            __syncwarp();
+                            const int z0 = fa.rows & 0xffff, nzs = fa.rows >> 16;
+                            SliceWalk<LP> w;
+                            w.init(fa, g, z0, flane, rla, nra, QPA);
+                            float* accl = acc + z0 + lane;
+                            float sf = 0.0f;
+#pragma unroll 1
+                            for (int s0 = 0; s0 < nzs; s0 += 31, sf += 31.0f) accl[s0] += w.contrib(sf);
+                            __syncwarp();
+                        }
                     }
                 }
                 continue;
