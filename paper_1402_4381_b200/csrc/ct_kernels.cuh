@@ -1057,7 +1057,10 @@ struct SliceWalk {
 // views per register-accumulated group (power of two <= 32; 0: off): the group's views walk the
 // union of their slice windows from one origin, a lane's S slices accumulate in registers and
 // reach the shared-memory accumulator once per group instead of once per view
-#define CT_BACK3D_GROUP 8
+#define CT_BACK3D_GROUP 16   // A/B c5 back: off 10.70, 8 -> 10.25, 16 -> 10.18, 32 -> 10.49 ms (c3 1.66 / 1.61 / 1.59 / 1.60)
+#endif
+#ifndef CT_BACK3D_GROUP_R2V
+#define CT_BACK3D_GROUP_R2V 1   // also in the two-view rows path (32-row detectors)
 #endif
 #ifndef CT_BACK3D_GROUP_SMEM
 #define CT_BACK3D_GROUP_SMEM 1   // the group unions live in the table (0: in registers across the batch; spills)
@@ -1144,12 +1147,13 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                 constexpr int RL = NTM / 16 > 0 ? NTM / 16 : 1, QS = NTM + 2;   // rows per lane, table stride
                 const int h = lane >> 4, l16 = lane & 15;
                 float2* QPh = QPA + h * QS;   // two (NTM + 1)-entry tables in the warp's 132 slots
-                for (int j = 0; j < nb; j += 2) {
+                // rows phase of views j, j + 1 into their prefix tables (false: neither meets the column)
+                auto rows_pair = [&](int j) -> bool {
                     Foot fh;
                     load_foot(&tab[min(j + h, nb - 1)], fh);   // (a finite record for the idle half)
                     if (j + h >= nb) fh.n = 0;
                     const int nmax = __reduce_max_sync(0xffffffffu, fh.n > 0 ? fh.n : 0);
-                    if (nmax <= 0) continue;
+                    if (nmax <= 0) return false;
                     float q[4] = {0.0f, 0.0f, 0.0f, 0.0f};
                     {
                         const float* yrow = yb + ((j + h) * ns + fh.cA) * NTM + RL * l16;
@@ -1195,6 +1199,10 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                     }
                     if (l16 == 15) QPh[NTM] = make_float2(inc, 0.0f);
                     __syncwarp();
+                    return true;
+                };
+                // per-view walks of views j, j + 1 into the shared-memory accumulator
+                auto walk_pair = [&](int j) {
 #pragma unroll 1
                     for (int v2 = 0; v2 < 2 && j + v2 < nb; v2++) {
                         Foot fw;
@@ -1214,7 +1222,52 @@ __global__ void __launch_bounds__(256, CT_BACK3D_MINB) back3d_kernel(DevGeom g, 
                         }
                         __syncwarp();
                     }
+                };
+#if CT_BACK3D_GROUP && CT_BACK3D_GROUP_R2V
+                static_assert(CT_BACK3D_GROUP % 2 == 0, "view groups hold whole view pairs");
+                for (int g0 = 0; g0 < nb; g0 += CT_BACK3D_GROUP) {
+                    const int g1 = min(g0 + CT_BACK3D_GROUP, nb);
+#if CT_BACK3D_GROUP_SMEM
+                    const int un = __float_as_int(tab[g0].ax.kz);
+                    const int uz0 = un & 0xffff, nzu = un >> 16;
+#else
+                    const int uz0 = __shfl_sync(0xffffffffu, gz0, g0), nzu = __shfl_sync(0xffffffffu, gz1, g0) - uz0;
+#endif
+                    if (nzu <= 0) continue;
+                    auto group = [&](auto SC) {
+                        constexpr int S = decltype(SC)::value;
+                        float a[S];
+#pragma unroll
+                        for (int e = 0; e < S; e++) a[e] = 0.0f;
+                        for (int j = g0; j < g1; j += 2) {
+                            if (!rows_pair(j)) continue;
+#pragma unroll 1
+                            for (int v2 = 0; v2 < 2 && j + v2 < nb; v2++) {
+                                Foot fw;
+                                load_foot(&tab[j + v2], fw);
+                                if (fw.n <= 0) continue;
+                                SliceWalk<LP> w;
+                                w.init(fw, g, uz0, flane, 0, NTM, QPA + v2 * QS);
+                                w.template walk_reg<S>(a, lane, flane);
+                                __syncwarp();
+                            }
+                        }
+                        float* p = acc + uz0 + S * lane;
+#pragma unroll
+                        for (int e = 0; e < S; e++) p[e] += a[e];
+                    };
+                    if (nzu <= 31) group(std::integral_constant<int, 1>());
+                    else if (nzu <= 63) group(std::integral_constant<int, 2>());
+                    else if (nzu <= 95) group(std::integral_constant<int, 3>());
+                    else if (nzu <= 127) group(std::integral_constant<int, 4>());
+                    else
+                        for (int j = g0; j < g1; j += 2)
+                            if (rows_pair(j)) walk_pair(j);
                 }
+#else
+                for (int j = 0; j < nb; j += 2)
+                    if (rows_pair(j)) walk_pair(j);
+#endif
                 continue;
             }
 #endif
