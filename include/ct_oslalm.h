@@ -350,6 +350,15 @@ int ct_comm_get_unique_id(void* nccl_uid_out128);
  *                     internal communication stream while the next slab is computed;
  *   CT_EXCHANGE_AUTO  BAND for helical scans with 2..16 ranks each owning >= 1 image row, else FULL
  *                     (the default).
+ * z-slab geometries (ct_comm_init_zslab, helical, 2..16 ranks): FULL all-reduces each subset's
+ * summed sinogram; BAND exchanges the windowed form instead — rank p's partial projection is
+ * non-zero only for the views whose cone reaches its slab (its view window), so it sends every
+ * other rank q only the views both windows hold and sums what it receives in rank order
+ * (ranks sharing a view hold identical sums; views outside the window are not back-projected
+ * onto the slab and are left unspecified in the state's sinogram); AUTO takes BAND when the
+ * busiest rank receives fewer bytes than a ring all-reduce moves per rank, else FULL (every
+ * rank evaluates the same rule from the slab extents gathered at ct_comm_init_zslab).  The
+ * D_L setup (ct_sqs_denom) always all-reduces.
  * Call before creating OS-LALM states.  CT_EINVAL for an unknown mode, CT_EUNSUPPORTED for BAND
  * on a fan-beam geometry (an axial scan's bands cover the whole volume: it runs, exchanging
  * the same bytes as FULL).

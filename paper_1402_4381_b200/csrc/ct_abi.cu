@@ -247,6 +247,9 @@ struct ct_geom {
     Comm* comm = nullptr;    // exchange backend (NcclComm / VirtualComm); owned
     int zslab = 0;   // NEXT-3: this geometry is rank `rank`'s z-slab of the volume (sinogram-domain sums)
     int exchange = CT_EXCHANGE_AUTO;   // row-slab path: full reduce-scatter / all-gather or z-band blocks
+    // z-slab ranks: every rank's slab (lower boundary zb0, slices), gathered at ct_comm_init_zslab
+    std::vector<float> slab_zb0;
+    std::vector<int> slab_nz;
 };
 
 static int comm_rc(const ct_geom* g, int rc) {
@@ -747,8 +750,10 @@ extern "C" int ct_sqs_denom_scratch_bytes(const ct_geom* g, size_t* out) {
 }
 
 static void zslab_window(const ct_geom* g, ct_views v, int* k0, int* k1);
+static bool use_zwin(const ct_geom* g, int M);
+static size_t zwin_floats(const ct_geom* g, int M, int r);
 static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* out, const float* y, const float* w,
-                           float scale, cudaStream_t st, FwdScratch fs);
+                           float scale, cudaStream_t st, FwdScratch fs, float* zbuf = nullptr);
 
 extern "C" int ct_sqs_denom(const ct_geom* g, const float* w, uint8_t* mask, float* dl, void* scratch, void* stream) {
     NvtxRange nvtx_("ct_sqs_denom");
@@ -881,6 +886,7 @@ struct ct_oslalm_state {
     float* zrecv[2] = {nullptr, nullptr};
     uint8_t* zmask[2] = {nullptr, nullptr};
     int zmask_ready = 0;
+    float* zwin = nullptr;               // helical z-slab ranks: the neighbours' window-overlap partials
     double* xi_part;
     FwdScratch fs{nullptr, nullptr};     // this state's forward-projection scratch (own, per state)
     Scalars* sc;
@@ -1029,6 +1035,7 @@ static void state_layout(const ct_geom* g, const ct_oslalm_cfg* c, size_t off[20
     off[14] = o; o += fwd_scratch_bytes(g, maxcount);
     off[15] = o; o += use_band(g, c) ? 4 * align256(N * 4) : 0;   // band exchange buffers
     off[16] = o; o += use_ysplit(g) ? align256(sino * 4) : 0;         // y-split forward partial sums
+    off[17] = o; o += use_zwin(g, c->M) ? align256(std::max<size_t>(1, zwin_floats(g, c->M, g->rank)) * 4) : 0;   // z-slab windowed exchange
     *total = o;
 }
 
@@ -1086,6 +1093,7 @@ extern "C" int ct_oslalm_state_create(const ct_geom* g, const ct_oslalm_cfg* c, 
     s->band = use_band(g, c) ? 1 : 0;
     if (s->band)
         for (int i = 0; i < 4; i++) s->bbuf[i] = (float*)(b + off[15] + i * align256(s->Npad * 4));
+    if (use_zwin(g, c->M)) s->zwin = (float*)(b + off[17]);
     if (g->zslab) {
         const size_t ncols = (size_t)g->d.nx * g->d.ny, fb = align256(ncols * 4);
         s->zsend[0] = (float*)(b + off[13]);
@@ -1178,23 +1186,78 @@ static ct_views rank_views(const ct_geom* g, int M, int m) {
 
 // z-slab ranks (NEXT-3): of views {first + k stride, k < count}, the contiguous range [k0, k1)
 // whose cone can reach this rank's slab (helical: |z - z_s| <= zhalf; axial: all views).
-static void zslab_window(const ct_geom* g, ct_views v, int* k0, int* k1) {
+// zslab_window_of: the same for rank q's slab (extents gathered at ct_comm_init_zslab).
+static void zslab_window_of(const ct_geom* g, ct_views v, double zb0, int nz, int* k0, int* k1) {
     *k0 = 0;
     *k1 = v.count;
     const DevGeom& dg = g->dg;
     if (g->d.kind != CT_CONE_HELICAL || !(dg.dzs > 0.0f) || v.count == 0) return;
-    const double zlo = dg.zb0, zhi = (double)dg.zb0 + (double)dg.nz * dg.dz, zh = (double)dg.zhalf + dg.dz;
+    const double zlo = zb0, zhi = zb0 + (double)nz * dg.dz, zh = (double)dg.zhalf + dg.dz;
     const double vlo = (zlo - zh - dg.zs0) / dg.dzs, vhi = (zhi + zh - dg.zs0) / dg.dzs;
     *k0 = std::max(0, (int)floor((vlo - v.first) / v.stride) - 1);
     *k1 = std::min(v.count, (int)ceil((vhi - v.first) / v.stride) + 2);
     if (*k1 < *k0) *k1 = *k0;
 }
 
+static void zslab_window(const ct_geom* g, ct_views v, int* k0, int* k1) {
+    zslab_window_of(g, v, g->dg.zb0, g->dg.nz, k0, k1);
+}
+
+// overlap [o0, o1) of ranks r's and q's windows of views v (v's indices)
+static void zwin_overlap_rq(const ct_geom* g, ct_views v, int r, int q, int* o0, int* o1) {
+    int a0, a1, b0, b1;
+    zslab_window_of(g, v, g->slab_zb0[r], g->slab_nz[r], &a0, &a1);
+    zslab_window_of(g, v, g->slab_zb0[q], g->slab_nz[q], &b0, &b1);
+    *o0 = std::max(a0, b0);
+    *o1 = std::max(*o0, std::min(a1, b1));
+}
+
+static void zwin_overlap(const ct_geom* g, ct_views v, int q, int* o0, int* o1) {
+    zwin_overlap_rq(g, v, g->rank, q, o0, o1);
+}
+
+// floats rank r receives in the windowed exchange for the largest subset of an M-subset state
+static size_t zwin_floats(const ct_geom* g, int M, int r) {
+    size_t best = 0;
+    for (int m = 0; m < M; m++) {
+        const ct_views v{m, M, (g->d.na - m + M - 1) / M};
+        size_t n = 0;
+        for (int q = 0; q < g->nranks; q++) {
+            if (q == r) continue;
+            int o0, o1;
+            zwin_overlap_rq(g, v, r, q, &o0, &o1);
+            n += (size_t)(o1 - o0);
+        }
+        best = std::max(best, n);
+    }
+    return best * n_cells_view(g);
+}
+
+// Windowed sinogram exchange of the helical z-slab path (2..16 ranks): only the views two
+// ranks' windows share travel, instead of an all-reduce of the whole subset sinogram.  BAND
+// forces it, FULL the all-reduce; AUTO takes it when the busiest rank receives fewer bytes than
+// a ring all-reduce moves per rank (2 (P-1)/P of the subset sinogram; c5: P = 2, 4 yes, P = 8
+// no — the cone's z reach makes neighbouring windows overlap by most of a subset).  Every rank
+// evaluates the same rule on the same slab table, so all ranks agree.
+static bool use_zwin(const ct_geom* g, int M) {
+    if (!(g->zslab && g->comm && g->d.kind == CT_CONE_HELICAL && g->dg.dzs > 0.0f && g->nranks >= 2 &&
+          g->nranks <= kMaxBandRanks && (int)g->slab_nz.size() == g->nranks))
+        return false;
+    if (g->exchange == CT_EXCHANGE_FULL) return false;
+    if (g->exchange == CT_EXCHANGE_BAND) return true;
+    size_t busiest = 0;
+    for (int r = 0; r < g->nranks; r++) busiest = std::max(busiest, zwin_floats(g, M, r));
+    const size_t sub = (size_t)((g->d.na + M - 1) / M) * n_cells_view(g);
+    return (double)busiest < 2.0 * (g->nranks - 1) / g->nranks * (double)sub;
+}
+
 // Forward projection summed over the z-slab ranks: out[k] = sum_slabs A_slab x_slab for
 // views k < v.count (only the rank's view window is projected; other views contribute 0),
-// then s <- scale W (s - y) on every ray (y nullable).
+// then s <- scale W (s - y) on every ray (y nullable).  With `zbuf` (the state's windowed-exchange
+// buffer, use_zwin) only the rank's window is summed (over the ranks sharing each view) and
+// finalised; the rays outside it are left unspecified (nothing back-projects them here).
 static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* out, const float* y, const float* w,
-                           float scale, cudaStream_t st, FwdScratch fs) {
+                           float scale, cudaStream_t st, FwdScratch fs, float* zbuf) {
     const size_t cells = n_cells_view(g);
     int k0, k1;
     zslab_window(g, v, &k0, &k1);
@@ -1204,6 +1267,36 @@ static int zslab_fwd_resid(const ct_geom* g, ct_views v, const float* x, float* 
         if (int e = launch_fwd<false>(g, ct_views{v.first + k0 * v.stride, v.stride, k1 - k0}, x, out + (size_t)k0 * cells,
                                       nullptr, nullptr, 1.0f, st, fs))
             return e;
+    if (zbuf) {
+        // neighbours' partials of the shared views in, rank-order sum + residual on the window
+        const int P = g->nranks, p = g->rank;
+        const float* sptr[kMaxBandRanks];
+        float* rptr[kMaxBandRanks];
+        size_t sc[kMaxBandRanks], rc[kMaxBandRanks], ro = 0;
+        ZWinSet zs{};
+        zs.P = P;
+        zs.self = p;
+        for (int q = 0; q < P; q++) {
+            int o0, o1;
+            zwin_overlap(g, v, q, &o0, &o1);
+            const size_t n = q == p ? 0 : (size_t)(o1 - o0) * cells;
+            sc[q] = rc[q] = n;
+            sptr[q] = out + (size_t)o0 * cells;
+            rptr[q] = zbuf + ro;
+            zs.buf[q] = zbuf + ro;
+            zs.o0[q] = o0 - k0;   // window-relative
+            zs.o1[q] = o1 - k0;
+            ro += n;
+        }
+        if (int e = comm_rc(g, g->comm->alltoallv(sptr, sc, rptr, rc, st))) return e;
+        if (k1 > k0) {
+            const size_t n = (size_t)(k1 - k0) * cells;
+            zwin_sum_resid_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(out + (size_t)k0 * cells, y, w, v.first + k0 * v.stride,
+                                                               v.stride, k1 - k0, (int)cells, scale, zs);
+            CT_LAUNCHED(1);
+        }
+        return CT_OK;   // views outside the window: not back-projected onto this slab (zero footprint)
+    }
     if (int e = allreduce(g, out, (size_t)v.count * cells, st)) return e;
     const size_t n = (size_t)v.count * cells;
     resid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, y, w, v.first, v.stride, v.count, (int)cells, scale);
@@ -1406,7 +1499,7 @@ static int subset_gradient(ct_oslalm_state* s, const ct_oslalm_data* d, const fl
     ct_views v = rank_views(g, M, m);
     int t0 = tmark(s, st);
     if (g->zslab) {
-        if (int e = zslab_fwd_resid(g, v, x, s->sino, d->y, d->w, (float)M, st, s->fs)) return e;
+        if (int e = zslab_fwd_resid(g, v, x, s->sino, d->y, d->w, (float)M, st, s->fs, s->zwin)) return e;
     } else {
         if (int e = launch_fwd<true>(g, v, x, s->sino, d->y, d->w, (float)M, st, s->fs)) return e;
     }
@@ -1804,6 +1897,8 @@ extern "C" int ct_comm_init(ct_geom* g, int rank, int nranks, const void* uid) {
     g->rank = rank;
     g->nranks = nranks;
     g->zslab = 0;
+    g->slab_zb0.clear();
+    g->slab_nz.clear();
     return CT_OK;
 }
 
@@ -1839,6 +1934,12 @@ extern "C" int ct_comm_init_virtual(ct_geom** gs, int nranks, int zslab) {
         gs[r]->rank = r;
         gs[r]->nranks = nranks;
         gs[r]->zslab = zslab ? 1 : 0;
+        gs[r]->slab_zb0.clear();
+        gs[r]->slab_nz.clear();
+        for (int q = 0; zslab && q < nranks; q++) {
+            gs[r]->slab_zb0.push_back(gs[q]->dg.zb0);
+            gs[r]->slab_nz.push_back(gs[q]->dg.nz);
+        }
     }
     return CT_OK;
 }
@@ -1848,5 +1949,27 @@ extern "C" int ct_comm_init_zslab(ct_geom* g, int rank, int nranks, const void* 
     if (g->d.kind == CT_FAN2D) return fail(CT_EUNSUPPORTED, "z-slab decomposition needs a cone-beam geometry");
     if (int e = ct_comm_init(g, rank, nranks, uid)) return e;
     g->zslab = 1;
+    // every rank's slab extent (zb0, nz): the windowed exchange needs the other ranks' view windows
+    DeviceGuard guard(g->d.device);
+    float* dz = nullptr;
+    cudaStream_t st = nullptr;
+    std::vector<float> h(2 * (size_t)nranks);
+    const float mine[2] = {g->dg.zb0, (float)g->dg.nz};
+    cudaError_t ce = cudaMalloc(&dz, h.size() * 4);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaMemcpy(dz + 2 * rank, mine, 8, cudaMemcpyHostToDevice);
+    int rc = ce == cudaSuccess ? g->comm->all_gather(dz + 2 * rank, dz, 2, st) : 0;
+    if (ce == cudaSuccess && !rc) ce = cudaStreamSynchronize(st);
+    if (ce == cudaSuccess && !rc) ce = cudaMemcpy(h.data(), dz, h.size() * 4, cudaMemcpyDeviceToHost);
+    if (st) cudaStreamDestroy(st);
+    if (dz) cudaFree(dz);
+    if (ce != cudaSuccess) return fail(CT_ECUDA, "ct_comm_init_zslab: %s", cudaGetErrorString(ce));
+    if (rc) return comm_rc(g, rc);
+    g->slab_zb0.resize(nranks);
+    g->slab_nz.resize(nranks);
+    for (int q = 0; q < nranks; q++) {
+        g->slab_zb0[q] = h[2 * q];
+        g->slab_nz[q] = (int)h[2 * q + 1];
+    }
     return CT_OK;
 }

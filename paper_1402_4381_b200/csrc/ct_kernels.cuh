@@ -1896,6 +1896,37 @@ __global__ void __launch_bounds__(256) band_sum_kernel(float* __restrict__ dst, 
     }
 }
 
+// Windowed exchange of the helical z-slab path: views k < count of this rank's
+// view window (the views whose cone reaches its slab).  Each ray is summed over the ranks whose
+// windows hold the view, in rank order (the same terms in the same order on every rank that
+// holds the view, so those ranks hold identical sums; ranks outside contribute exactly 0 to
+// the full sum), then s <- scale W (s - y) as resid_kernel does.
+struct ZWinSet {
+    const float* buf[kMaxBandRanks];   // rank q's partial for window views [o0[q], o1[q])
+    int o0[kMaxBandRanks], o1[kMaxBandRanks];
+    int P, self;                       // q = self reads s itself
+};
+
+__global__ void __launch_bounds__(256) zwin_sum_resid_kernel(float* __restrict__ s, const float* __restrict__ yobs,
+                                                            const float* __restrict__ wts, int first, int stride,
+                                                            int count, int cells_per_view, float scale, ZWinSet zs) {
+    const size_t n = (size_t)count * cells_per_view;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i / cells_per_view);
+        const size_t c = i - (size_t)k * cells_per_view;
+        float v = 0.0f;
+        for (int q = 0; q < zs.P; q++) {
+            if (q == zs.self)
+                v += s[i];
+            else if (k >= zs.o0[q] && k < zs.o1[q])
+                v += zs.buf[q][(size_t)(k - zs.o0[q]) * cells_per_view + c];
+        }
+        const size_t gi = (size_t)(first + k * stride) * cells_per_view + c;
+        const float yo = yobs ? __ldg(&yobs[gi]) : 0.0f;
+        s[i] = scale * __ldg(&wts[gi]) * (v - yo);
+    }
+}
+
 // Multi-rank slab path: G+ (already reduce-scattered into G_new[j0, j1)) -> g-update and
 // this rank's xi; the last block stores the rank's fixed-order xi sum in *xi_out (the
 // ranks' sums are then all-reduced and xi_rule_kernel applies K4 on every rank).

@@ -61,6 +61,39 @@ def helical_zhalf(g: dict) -> float:
     return (0.5 * g["nt"] * g["dt"] + 0.5 * abs(g.get("offt", 0.0)) * g["dt"]) * (g["dso"] + rmax) / g["dsd"] + g["dz"]
 
 
+def zslab_window(g: dict, M: int, m: int, z0: int, z1: int) -> tuple[int, int]:
+    """Indices [k0, k1) of subset m's views whose cone can reach slices [z0, z1) of the volume
+    (helical z-slab ranks; mirror of zslab_window_of in ct_abi.cu: source heights within the
+    cone's z reach of the slab, widened by one slice and one / two views)."""
+    count = (g["na"] - m + M - 1) // M
+    if g["kind"] != "cone_helical" or count == 0:
+        return 0, count
+    turns = g["orbit_deg"] / 360.0
+    h = g["pitch"] * g["nt"] * g["dt"] * g["dso"] / g["dsd"]
+    dzs = h / (g["na"] / turns)
+    zs0 = -(g["na"] - 1) / 2.0 * dzs
+    zb0 = -(g["nz"] - 1) / 2.0 * g["dz"] + g.get("offz", 0.0) - 0.5 * g["dz"]
+    zlo, zhi = zb0 + z0 * g["dz"], zb0 + z1 * g["dz"]
+    zh = helical_zhalf(g) + g["dz"]
+    vlo, vhi = (zlo - zh - zs0) / dzs, (zhi + zh - zs0) / dzs
+    k0 = max(0, math.floor((vlo - m) / M) - 1)
+    k1 = min(count, math.ceil((vhi - m) / M) + 2)
+    return k0, max(k0, k1)
+
+
+def zslab_exchange_floats(g: dict, M: int, m: int, rank: int, nranks: int) -> int:
+    """Floats rank `rank` receives in the windowed z-slab exchange of subset m: for every other
+    rank, the views both windows hold, times the detector cells per view."""
+    z0, z1 = rank_zslab(g["nz"], rank, nranks)
+    a0, a1 = zslab_window(g, M, m, z0, z1)
+    n = 0
+    for q in range(nranks):
+        if q != rank:
+            b0, b1 = zslab_window(g, M, m, *rank_zslab(g["nz"], q, nranks))
+            n += max(0, min(a1, b1) - max(a0, b0))
+    return n * g["ns"] * g["nt"]
+
+
 def rank_band(g: dict, M: int, m: int, rank: int, nranks: int) -> tuple[int, int]:
     """Slices [b0, b1) in which `rank`'s partial back-projection of subset m can be non-zero:
     the source heights of its contiguous view block widened by the cone's z reach and one

@@ -252,3 +252,31 @@ def test_rank_band_contains_every_seen_slice():
                 if np.abs(p).max() > 0:
                     assert b0 <= z < b1, (m, r, z, b0, b1)
     assert max(widths) <= 0.75 * g["nz"]
+
+
+def test_zslab_window_contains_every_reaching_view():
+    """Windowed z-slab exchange (helical): every view of a subset whose oracle projection of a
+    rank's slab (all ones) is non-zero lies inside host.zslab_window (the mirror of the
+    library's zslab_window_of), and on a long helix the windows are shorter than a subset
+    (on average; the middle slab's window spans most of a subset — the cone's z reach)."""
+    import numpy as np
+    import oracle as O
+    from paper_1402_4381_b200 import host
+    from tests import geomutil as GU
+    g = GU.geom("cone_helical", nx=12, nz=40, dx=0.9766, dz=0.625, ns=24, ds=1.0239, nt=6, dt=1.0964, na=144,
+                turns=6.0, pitch=0.8)
+    M, P = 4, 3
+    fracs = []
+    for m in range(M):
+        count = O.nviews(g, m, M)
+        for r in range(P):
+            z0, z1 = host.rank_zslab(g["nz"], r, P)
+            k0, k1 = host.zslab_window(g, M, m, z0, z1)
+            fracs.append((k1 - k0) / count)
+            x = np.zeros(O.img_shape(g))
+            x[z0:z1] = 1.0
+            p = O.fwd(g, x, m, M, count).reshape(count, -1)
+            hit = np.nonzero(np.abs(p).max(axis=1) > 0)[0]
+            assert hit.size > 0
+            assert k0 <= hit.min() and hit.max() < k1, (m, r, hit.min(), hit.max(), k0, k1)
+    assert sum(fracs) / len(fracs) <= 0.7

@@ -158,6 +158,35 @@ def test_zslab_path_virtual(ct, O, name, P, bb):
     assert e <= 0.5, (name, P, e)
 
 
+@pytest.mark.parametrize("P", [3, 5])
+def test_zslab_window_exchange_long_helix(ct, O, P):
+    """Windowed exchange of the helical z-slab path: a 6-turn helix over 40 slices
+    split into P slabs, so a view's cone reaches only some of the slabs and only the views two
+    ranks' windows share travel.  2 iterations against the oracle, and the FULL exchange (an
+    all-reduce of every subset sinogram) gives the same image to fp32 rounding."""
+    from paper_1402_4381_b200 import host
+    g = GU.geom("cone_helical", nx=16, nz=40, dx=0.9766, dz=0.625, ns=28, ds=1.0239, nt=6, dt=1.0964, na=144,
+                turns=6.0, pitch=0.8)
+    ell = [(0.0, 0.0, 0.0, 5.5, 4.5, 10.0, 0.0, 0.02), (1.0, -0.5, 3.0, 2.0, 1.5, 3.0, 0.4, 0.01)]
+    d = I.noisy_data(g, ell, 1e5, 0.0, 87)
+    m0 = torch.ones((g["ny"], g["nx"], g["nz"]), dtype=torch.uint8)
+    base = I.config("c4")
+    slabs = [host.rank_zslab(g["nz"], r, P) for r in range(P)]
+    geoms = [I.slab_geom(g, z0, z1) for (z0, z1) in slabs]
+    masks = [m0[..., z0:z1].contiguous() for (z0, z1) in slabs]
+    win = run_virtual(ct, geoms, d["y"], d["w"], masks, 4, 2, base.beta, base.delta, 26, zslab=True,
+                      exchange="band")
+    full = run_virtual(ct, geoms, d["y"], d["w"], masks, 4, 2, base.beta, base.delta, 26, zslab=True,
+                       exchange="full")
+    xo, So, logo = oracle_run(O, g, d["y"], d["w"], m0, 4, 2, base.beta, base.delta, 26)
+    x = np.concatenate([o[0] for o in win], axis=2)
+    xf = np.concatenate([o[0] for o in full], axis=2)
+    for r in range(P):
+        assert np.array_equal(win[r][2][:, 2], logo[:, 2]), r
+    assert rms_hu(I.to_oracle_image(x), xo, So) <= 0.5
+    assert np.abs(x - xf).max() <= 1e-5 * np.abs(xf).max()
+
+
 def test_band_exchange_long_helix(ct, O):
     """Band-limited exchange where the bands are much narrower than the volume: a 6-turn helix
     over 40 slices, 3 ranks (each rank's view block sees about half of the slices), 2
