@@ -138,6 +138,74 @@ def _zslab_worker(rank, ws, port, out):
     dist.destroy_process_group()
 
 
+def _zslab_window_worker(rank, ws, port, out):
+    """Windowed z-slab exchange (helical) with the oracle as the projector: each rank projects
+    its slab for the views of its window (host.zslab_window), sends every other rank the views
+    both windows hold, receives theirs (gloo send / recv) and sums in rank order — on its
+    window this equals the full forward projection (what zwin_sum_resid_kernel forms before the
+    residual)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import oracle as O
+    from paper_1402_4381_b200 import host
+    from paper_1402_4381_b200 import inputs as I
+    from tests import geomutil as GU
+    g = GU.geom("cone_helical", nx=12, nz=40, dx=0.9766, dz=0.625, ns=24, ds=1.0239, nt=6, dt=1.0964, na=144,
+                turns=6.0, pitch=0.8)
+    M = 4
+    rng = np.random.default_rng(5)
+    x = rng.random(O.img_shape(g)) * 0.02
+    slabs = [host.rank_zslab(g["nz"], q, ws) for q in range(ws)]
+    errs = []
+    for m in range(M):
+        count = O.nviews(g, m, M)
+        wins = [host.zslab_window(g, M, m, *slabs[q]) for q in range(ws)]
+        k0, k1 = wins[rank]
+        z0, z1 = slabs[rank]
+        part = torch.from_numpy(np.ascontiguousarray(O.fwd(I.slab_geom(g, z0, z1), x[z0:z1], m + k0 * M, M, k1 - k0)))
+        recv, reqs = {}, []
+        for q in range(ws):
+            if q == rank:
+                continue
+            o0, o1 = max(k0, wins[q][0]), min(k1, wins[q][1])
+            if o1 <= o0:
+                continue
+            reqs.append(dist.isend(part[o0 - k0:o1 - k0].contiguous(), q))
+            recv[q] = (o0, torch.empty((o1 - o0,) + tuple(part.shape[1:]), dtype=part.dtype))
+            reqs.append(dist.irecv(recv[q][1], q))
+        for rq in reqs:
+            rq.wait()
+        tot = torch.zeros_like(part)
+        for q in range(ws):
+            if q == rank:
+                tot += part
+            elif q in recv:
+                o0, buf = recv[q]
+                tot[o0 - k0:o0 - k0 + buf.shape[0]] += buf
+        full = O.fwd(g, x, m, M, count)[k0:k1]
+        errs.append(float(np.abs(tot.numpy() - full).max() / np.abs(full).max()))
+    out.put((rank, max(errs)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_gloo_zslab_window_exchange(ws):
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_zslab_window_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(ws)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert max(e for _, e in res) <= 1e-12, res
+
+
 @pytest.mark.parametrize("ws", [2, 3])   # 3: uneven view blocks / slabs
 def test_gloo_two_rank_zslab(ws):
     import oracle
