@@ -826,12 +826,13 @@ __device__ __forceinline__ double back_epilogue(size_t j, bool valid, float acc,
 #define CT_BACK3D_PAIR 0   // 1: two views per slice walk (one accumulator update per slice for both); A/B: slower (64 registers, 4 CTAs/SM: c5 11.25 -> 12.38 ms)
 #endif
 // two views per rows phase (half-warps): A/B 32-row detector c4 4.04 -> 3.90 ms (on), 64-row
-// detector c5 10.73 -> 10.85 ms (off)
+// detector c5 10.73 -> 10.85 ms without view groups; with view groups (r43) c5 10.18 -> 10.10,
+// c3 1.594 -> 1.580 ms (on)
 #ifndef CT_BACK3D_ROWS2V_32
 #define CT_BACK3D_ROWS2V_32 1
 #endif
 #ifndef CT_BACK3D_ROWS2V_64
-#define CT_BACK3D_ROWS2V_64 0
+#define CT_BACK3D_ROWS2V_64 1
 #endif
 #ifndef CT_BACK3D_PREFETCH
 #define CT_BACK3D_PREFETCH 0   // 1: L1 prefetch of the next view's detector rows (A/B: c5 11.32 -> 13.08 ms, off)
